@@ -1,0 +1,156 @@
+/* gdi-b200 C ABI — the drop-in boundary of the GDI annealing hot path.
+ *
+ * Replaces, for host callers, the reference's in-process CPU annealer
+ * (reference proj/include/ising/anneal.hpp:74-75 `ising::anneal`, implemented
+ * at proj/src/anneal.cpp:132-231) and its exact per-sweep scoring
+ * (proj/src/anneal.cpp:64-70 `cut_of`, proj/src/evaluate.cpp:10-32
+ * `cut_value`/`imbalance`/`score`). Plain C types only: pointers, sizes,
+ * POD structs. No C++ exceptions and no torch types cross this boundary.
+ *
+ * Status codes map 1:1 onto the reference exception taxonomy
+ * (proj/include/ising/errors.hpp:8-38):
+ *   GDI_ERR_CONFIG   -> config_error   (anneal.cpp:24-37 validated())
+ *   GDI_ERR_DOMAIN   -> domain_error   (graph.cpp:47-61 invalid CSR)
+ *   GDI_ERR_CAPACITY -> capacity_error (graph too large for a kernel variant)
+ *   GDI_ERR_RUNTIME  -> std::runtime_error (CUDA failure, no device)
+ * gdi_last_error() returns the thread-local message of the last failure.
+ *
+ * Ownership: host buffers are caller-owned; the library owns device memory.
+ * Threading: every entry point is reentrant; distinct host threads may run
+ * concurrently on distinct graphs/sessions (one CUDA stream per session).
+ * There is no CPU fallback: without a usable sm_100 device calls fail with
+ * GDI_ERR_RUNTIME.
+ */
+#ifndef GDI_H
+#define GDI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDI_ABI_VERSION 1
+
+enum {
+  GDI_OK = 0,
+  GDI_ERR_CONFIG = -1,
+  GDI_ERR_DOMAIN = -2,
+  GDI_ERR_CAPACITY = -3,
+  GDI_ERR_RUNTIME = -4
+};
+
+/* anneal.hpp:13 Strategy */
+enum { GDI_STRATEGY_STANDARD = 0, GDI_STRATEGY_GDI = 1 };
+
+/* Kernel family. EXACT reproduces the reference's deterministic / single
+ * worker mode bit for bit (xoshiro256++ stream 1, visit order 0..n-1;
+ * anneal.cpp:189-202). THROUGHPUT is the reference's pooled racy mode
+ * (anneal.cpp:203-225): vertex-parallel sweeps, Philox counter RNG keyed by
+ * (seed, sweep, vertex), statistically equivalent, not bit-exact. */
+enum { GDI_MODE_EXACT = 0, GDI_MODE_THROUGHPUT = 1 };
+
+/* gdi_params.flags */
+#define GDI_FLAG_TRACE 0x1u     /* record per-sweep cut / balance / timestamp */
+#define GDI_FLAG_SNAPSHOTS 0x2u /* record spins after init and every sweep (hooks) */
+
+typedef struct gdi_graph gdi_graph;     /* device-resident CSR, one device */
+typedef struct gdi_session gdi_session; /* device buffers for R replicas  */
+
+/* anneal.hpp:18-30 AnnealParams (validated) + model.hpp:27-34 Coefficients */
+typedef struct {
+  int32_t sweeps;
+  int32_t strategy; /* GDI_STRATEGY_* */
+  int32_t mode;     /* GDI_MODE_* */
+  uint32_t flags;   /* GDI_FLAG_* */
+  double flip_fraction0;
+  double decay_rate;
+  int64_t a_num;
+  int64_t b_num;
+  int64_t denom;
+} gdi_params;
+
+/* anneal.hpp:39-46 TraceRecord, field for field */
+typedef struct {
+  int64_t hamiltonian_scaled;
+  double hamiltonian;
+  int64_t cut;
+  int64_t imbalance;
+  double flip_probability;
+  double seconds;
+} gdi_trace_rec;
+
+/* evaluate.hpp:9-14 PartitionScore + the balance counter G at the end */
+typedef struct {
+  int64_t cut;
+  int64_t imbalance;
+  int64_t hamiltonian_scaled;
+  double hamiltonian;
+  int64_t balance_counter;
+} gdi_score;
+
+/* Output buffers of one batch; every pointer may be NULL (not wanted).
+ * Row-major over replicas: spins[r*n + i], trace[r*sweeps + k],
+ * snapshots[(r*(sweeps+1) + k)*n + i] (k=0 is the initial state),
+ * counters[r*sweeps + k] = balance counter at barrier k. */
+typedef struct {
+  int8_t* spins;
+  gdi_trace_rec* trace;
+  gdi_score* scores;
+  int8_t* snapshots;
+  int64_t* counters;
+  double seconds; /* out: device time of the sweep kernel(s) */
+} gdi_outputs;
+
+typedef struct {
+  int32_t n;
+  int64_t m;
+  int32_t max_degree;
+  int32_t device;
+  int32_t all_unit_weights;
+  int64_t device_bytes;
+} gdi_graph_info;
+
+int gdi_abi_version(void);
+const char* gdi_last_error(void);
+int gdi_device_count(int* count);
+
+/* Upload a CSR graph (reference layout graph.hpp:66-67, split into arrays):
+ * offsets[n+1] (int64), nbr[offsets[n]] (int32), weights[offsets[n]] or NULL
+ * for all-unit weights. Validates symmetry-free invariants cheaply (ranges,
+ * self loops); the caller's Graph already enforces the rest. */
+int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_t* nbr,
+                     const int32_t* weights, gdi_graph** out);
+int gdi_graph_destroy(gdi_graph* g);
+int gdi_graph_query(const gdi_graph* g, gdi_graph_info* info);
+
+/* One-shot batch: R independent anneals (seeds[r]) of the same problem,
+ * host in / host out. Equivalent to R calls of the reference anneal() with
+ * params.seed = seeds[r]. */
+int gdi_anneal_batch(const gdi_graph* g, const gdi_params* p, const uint64_t* seeds,
+                     int32_t replicas, gdi_outputs* out);
+
+/* Fused exact evaluation (cut, imbalance, H) of R host spin vectors. */
+int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,
+                       int64_t b_num, int64_t denom, gdi_score* scores);
+
+/* Session API: keeps inputs and outputs resident in HBM between launches so
+ * a caller can time the kernels alone. `stream` is a cudaStream_t (NULL: the
+ * session creates its own). launch() is asynchronous on that stream. */
+int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, void* stream,
+                       gdi_session** out);
+int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds);
+int gdi_session_launch(gdi_session* s);
+int gdi_session_sync(gdi_session* s);
+int gdi_session_fetch(gdi_session* s, gdi_outputs* out);
+/* Kernel launches issued per gdi_session_launch (for launch accounting). */
+int gdi_session_launch_count(const gdi_session* s, int32_t* count);
+/* Name of the kernel variant the session selected (static string). */
+const char* gdi_session_kernel(const gdi_session* s);
+int gdi_session_destroy(gdi_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

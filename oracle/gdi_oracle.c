@@ -344,3 +344,22 @@ int orc_anneal_det(int32_t n, const int64_t* offsets, const int32_t* nbr, const 
   }
   return 0;
 }
+
+void orc_rng_draws_seed(uint64_t seed, int64_t count, uint64_t* out) {
+  orc_rng r;
+  orc_rng_seed(&r, seed);
+  for (int64_t i = 0; i < count; i++) out[i] = orc_rng_next(&r);
+}
+
+/* FNV-1a 64 over `count` rows of `len` bytes (SURVEY §8(c) hashing). */
+void orc_fnv1a_rows(const uint8_t* data, int64_t count, int64_t len, uint64_t* out) {
+  for (int64_t r = 0; r < count; r++) {
+    uint64_t h = 1469598103934665603ULL;
+    const uint8_t* p = data + r * len;
+    for (int64_t i = 0; i < len; i++) {
+      h ^= p[i];
+      h *= 1099511628211ULL;
+    }
+    out[r] = h;
+  }
+}

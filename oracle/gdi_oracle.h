@@ -31,6 +31,7 @@ uint64_t orc_rng_next(orc_rng* r);
 uint64_t orc_rng_below(orc_rng* r, uint64_t bound);
 /* Fill out[count] with consecutive raw draws of stream(seed, id). */
 void orc_rng_draws(uint64_t seed, uint64_t stream_id, int64_t count, uint64_t* out);
+void orc_rng_draws_seed(uint64_t seed, int64_t count, uint64_t* out);
 
 /* Generators: edge lists in generation order. Return 0 or a negative code. */
 int orc_gen_random(int32_t n, int64_t m, uint64_t seed, int32_t* eu, int32_t* ev, int32_t* ew);
@@ -59,6 +60,9 @@ int orc_anneal_det(int32_t n, const int64_t* offsets, const int32_t* nbr, const 
                    int64_t a_num, int64_t b_num, int64_t denom, int32_t sweeps, double pf0,
                    double decay, uint64_t seed, int8_t* spins_out, int64_t* trace_out,
                    int64_t* counter_out, double* pf_out, int64_t* stats_out);
+
+/* FNV-1a 64 (offset 1469598103934665603, prime 1099511628211) per row. */
+void orc_fnv1a_rows(const uint8_t* data, int64_t count, int64_t len, uint64_t* out);
 
 #ifdef __cplusplus
 }

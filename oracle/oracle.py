@@ -52,18 +52,23 @@ def lib():
             c.c_double, c.c_double, c.c_uint64, I8P, I64P, I64P, F64P, I64P,
         ]
         L.orc_anneal_det.restype = c.c_int
+        U8P = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        L.orc_fnv1a_rows.argtypes = [U8P, c.c_int64, c.c_int64, U64P]
+        L.orc_fnv1a_rows.restype = None
         _LIB = L
     return _LIB
 
 
-def fnv1a(data: bytes, h: int = 1469598103934665603) -> int:
-    arr = np.frombuffer(data, dtype=np.uint8)
-    h = np.uint64(h)
-    prime = np.uint64(1099511628211)
-    with np.errstate(over="ignore"):
-        for b in arr:
-            h = (h ^ np.uint64(b)) * prime
-    return int(h)
+def fnv1a_rows(rows: np.ndarray) -> list[int]:
+    """FNV-1a 64 of each row's raw bytes."""
+    b = np.ascontiguousarray(rows).view(np.uint8).reshape(rows.shape[0], -1)
+    out = np.empty(b.shape[0], np.uint64)
+    lib().orc_fnv1a_rows(b, b.shape[0], b.shape[1], out)
+    return [int(x) for x in out]
+
+
+def fnv1a(data: bytes) -> int:
+    return fnv1a_rows(np.frombuffer(data, np.uint8).reshape(1, -1))[0]
 
 
 def draws(seed: int, stream: int, count: int) -> np.ndarray:

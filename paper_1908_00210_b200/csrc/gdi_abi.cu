@@ -1,0 +1,437 @@
+// C ABI of libgdi (include/gdi.h): graph upload, sessions, batch anneal and
+// fused evaluation. Everything here is host code around the sm_100a kernels
+// in k1_exact.cu / k2_throughput.cu / k3_eval.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gdi.h"
+#include "kernels.cuh"
+#include "launch.hpp"
+
+using namespace gdi;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(GDI_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define GDI_CUDA(call)                                 \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+// RAII device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t b) {
+    bytes = b;
+    return b ? cudaMalloc(&p, b) : cudaSuccess;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Selects the device and checks it is a Blackwell (sm_100) part: the
+// kernels are compiled for sm_100a only and there is no fallback.
+int use_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(GDI_ERR_RUNTIME, "no CUDA device available (gdi-b200 has no CPU fallback)");
+  if (device < 0 || device >= count)
+    return fail(GDI_ERR_CONFIG, "device index " + std::to_string(device) + " out of range");
+  GDI_CUDA(cudaSetDevice(device));
+  int major = 0;
+  GDI_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) return fail(GDI_ERR_RUNTIME, "gdi-b200 kernels require an sm_100 (B200) device");
+  return GDI_OK;
+}
+
+}  // namespace
+
+struct gdi_graph {
+  int device = 0;
+  GraphStats st;
+  DevBuf off, col, w;
+  int64_t bytes = 0;
+  DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), w.as<int32_t>(), st.n}; }
+};
+
+struct gdi_session {
+  const gdi_graph* g = nullptr;
+  gdi_params p{};
+  int32_t replicas = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ExactPlan plan;
+  std::vector<double> pf;        // flip probability per sweep (iterated product)
+  std::vector<long long> thr;    // integer flip threshold per sweep
+  DevBuf seeds, thr_d, spins, trace, stamps, snaps, final_out;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool launched = false;
+  ~gdi_session() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// AnnealParams::validated() (reference anneal.cpp:24-37) plus the coefficient
+// sanity of MinCutProblem::make_unchecked (model.cpp:76-82).
+int check_params(const gdi_params* p) {
+  if (!p) return fail(GDI_ERR_CONFIG, "params is NULL");
+  if (p->sweeps < 1) return fail(GDI_ERR_CONFIG, "sweeps must be >= 1");
+  if (!(p->flip_fraction0 >= 0.0 && p->flip_fraction0 <= 1.0))
+    return fail(GDI_ERR_CONFIG, "flip_fraction0 must be in [0, 1]");
+  if (!(p->decay_rate > 0.0 && p->decay_rate < 1.0))
+    return fail(GDI_ERR_CONFIG, "decay_rate must be in (0, 1)");
+  if (p->strategy != GDI_STRATEGY_GDI && p->strategy != GDI_STRATEGY_STANDARD)
+    return fail(GDI_ERR_CONFIG, "unknown strategy");
+  if (p->mode != GDI_MODE_EXACT && p->mode != GDI_MODE_THROUGHPUT)
+    return fail(GDI_ERR_CONFIG, "unknown mode");
+  if (p->a_num <= 0 || p->b_num <= 0 || p->denom <= 0)
+    return fail(GDI_ERR_CONFIG, "coefficients must be positive");
+  return GDI_OK;
+}
+
+// pf_k by the reference's iterated product (anneal.cpp:183, :39-45) and the
+// exactly equivalent integer threshold on the 53-bit draw:
+//   (x>>11) * 2^-53 <= pf  <=>  (x>>11) <= floor(pf * 2^53)   (pf > 0)
+void schedule(const gdi_params& p, std::vector<double>& pf, std::vector<long long>& thr) {
+  pf.resize(p.sweeps);
+  thr.resize(p.sweeps);
+  double v = p.flip_fraction0;
+  for (int k = 0; k < p.sweeps; k++) {
+    pf[k] = v;
+    thr[k] = v > 0.0 ? static_cast<long long>(std::floor(std::ldexp(v, 53))) : -1LL;
+    v *= p.decay_rate;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int gdi_abi_version(void) { return GDI_ABI_VERSION; }
+
+const char* gdi_last_error(void) { return g_last_error.c_str(); }
+
+int gdi_device_count(int* count) {
+  if (!count) return fail(GDI_ERR_CONFIG, "count is NULL");
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return GDI_OK;
+}
+
+int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_t* nbr,
+                     const int32_t* weights, gdi_graph** out) {
+  if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (n <= 0) return fail(GDI_ERR_DOMAIN, "graph needs a positive node count");
+  if (!offsets) return fail(GDI_ERR_DOMAIN, "offsets is NULL");
+  const int64_t nnz = offsets[n];
+  if (offsets[0] != 0 || nnz < 0 || (nnz % 2) != 0)
+    return fail(GDI_ERR_DOMAIN, "offsets must start at 0 and hold an even entry count");
+  if (nnz > 0x7fffffffLL) return fail(GDI_ERR_CAPACITY, "more than 2^31-1 adjacency entries");
+  if (nnz > 0 && !nbr) return fail(GDI_ERR_DOMAIN, "nbr is NULL");
+
+  auto g = std::make_unique<gdi_graph>();
+  g->device = device;
+  g->st.n = n;
+  g->st.m = nnz / 2;
+  std::vector<int32_t> off32(static_cast<size_t>(n) + 1);
+  for (int32_t i = 0; i <= n; i++) {
+    if (i > 0 && offsets[i] < offsets[i - 1]) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
+    off32[i] = static_cast<int32_t>(offsets[i]);
+  }
+  bool unit = true;
+  long long max_field = 0;
+  int32_t max_deg = 0;
+  for (int32_t i = 0; i < n; i++) {
+    long long row = 0;
+    for (int64_t e = offsets[i]; e < offsets[i + 1]; e++) {
+      const int32_t v = nbr[e];
+      if (v < 0 || v >= n) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
+      if (v == i) return fail(GDI_ERR_DOMAIN, "self-loop");
+      const long long wv = weights ? weights[e] : 1;
+      if (wv != 1) unit = false;
+      row += wv < 0 ? -wv : wv;
+    }
+    max_field = std::max(max_field, row);
+    max_deg = std::max<int32_t>(max_deg, static_cast<int32_t>(offsets[i + 1] - offsets[i]));
+  }
+  g->st.unit = unit;
+  g->st.max_abs_field = max_field;
+  g->st.max_degree = max_deg;
+
+  int rc = use_device(device);
+  if (rc) return rc;
+  GDI_CUDA(g->off.alloc(off32.size() * sizeof(int32_t)));
+  GDI_CUDA(g->col.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+  GDI_CUDA(cudaMemcpy(g->off.p, off32.data(), off32.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice));
+  if (nnz) GDI_CUDA(cudaMemcpy(g->col.p, nbr, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (!unit) {
+    GDI_CUDA(g->w.alloc(nnz * sizeof(int32_t)));
+    GDI_CUDA(cudaMemcpy(g->w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  g->bytes = static_cast<int64_t>(g->off.bytes + g->col.bytes + g->w.bytes);
+  *out = g.release();
+  return GDI_OK;
+}
+
+int gdi_graph_destroy(gdi_graph* g) {
+  if (g) {
+    cudaSetDevice(g->device);
+    delete g;
+  }
+  return GDI_OK;
+}
+
+int gdi_graph_query(const gdi_graph* g, gdi_graph_info* info) {
+  if (!g || !info) return fail(GDI_ERR_CONFIG, "NULL argument");
+  info->n = g->st.n;
+  info->m = g->st.m;
+  info->max_degree = g->st.max_degree;
+  info->device = g->device;
+  info->all_unit_weights = g->st.unit ? 1 : 0;
+  info->device_bytes = g->bytes;
+  return GDI_OK;
+}
+
+int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, void* stream,
+                       gdi_session** out) {
+  if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (!g) return fail(GDI_ERR_CONFIG, "graph is NULL");
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (replicas < 1) return fail(GDI_ERR_CONFIG, "replicas must be >= 1");
+  if ((rc = use_device(g->device))) return rc;
+
+  auto s = std::make_unique<gdi_session>();
+  s->g = g;
+  s->p = *p;
+  s->replicas = replicas;
+  schedule(s->p, s->pf, s->thr);
+  // Both strategies coincide in the exact mode (reference acceptance.cpp
+  // criterion 8); the throughput kernel is selected in gdi_abi_k2.cu.
+  if (exact_plan(g->st, replicas, &s->plan))
+    return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
+
+  if (stream) {
+    s->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    GDI_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+  }
+  GDI_CUDA(cudaEventCreate(&s->ev0));
+  GDI_CUDA(cudaEventCreate(&s->ev1));
+  const size_t R = replicas, n = g->st.n, S = p->sweeps;
+  GDI_CUDA(s->seeds.alloc(R * sizeof(uint64_t)));
+  GDI_CUDA(s->thr_d.alloc(S * sizeof(long long)));
+  GDI_CUDA(s->spins.alloc(R * n));
+  GDI_CUDA(s->final_out.alloc(R * sizeof(DevTrace)));
+  if (p->flags & GDI_FLAG_TRACE) {
+    GDI_CUDA(s->trace.alloc(R * S * sizeof(DevTrace)));
+    GDI_CUDA(s->stamps.alloc(R * (S + 1) * sizeof(unsigned long long)));
+  }
+  if (p->flags & GDI_FLAG_SNAPSHOTS) GDI_CUDA(s->snaps.alloc(R * (S + 1) * n));
+  GDI_CUDA(cudaMemcpyAsync(s->thr_d.p, s->thr.data(), S * sizeof(long long),
+                           cudaMemcpyHostToDevice, s->stream));
+  GDI_CUDA(cudaStreamSynchronize(s->stream));
+  *out = s.release();
+  return GDI_OK;
+}
+
+int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
+  if (!s || !seeds) return fail(GDI_ERR_CONFIG, "NULL argument");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(cudaMemcpyAsync(s->seeds.p, seeds, s->replicas * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, s->stream));
+  return GDI_OK;
+}
+
+int gdi_session_launch(gdi_session* s) {
+  if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  ExactArgs a{};
+  a.g = s->g->csr();
+  a.n_pad = s->plan.n_pad;
+  a.sweeps = s->p.sweeps;
+  a.replicas = s->replicas;
+  a.seeds = s->seeds.as<uint64_t>();
+  a.thr = s->thr_d.as<long long>();
+  a.a4 = 4 * s->p.a_num;
+  a.b = s->p.b_num;
+  a.spins_out = s->spins.as<int8_t>();
+  a.trace = s->trace.as<DevTrace>();
+  a.stamps = s->stamps.as<unsigned long long>();
+  a.snaps = s->snaps.as<int8_t>();
+  a.final_out = s->final_out.as<DevTrace>();
+  GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
+  GDI_CUDA(exact_launch(s->plan, a, s->stream));
+  GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
+  s->launched = true;
+  return GDI_OK;
+}
+
+int gdi_session_sync(gdi_session* s) {
+  if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(cudaStreamSynchronize(s->stream));
+  return GDI_OK;
+}
+
+int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
+  if (!s || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
+  if (!s->launched) return fail(GDI_ERR_CONFIG, "session has not been launched");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(cudaStreamSynchronize(s->stream));
+  const size_t R = s->replicas, n = s->g->st.n, S = s->p.sweeps;
+  const long long A = s->p.a_num, B = s->p.b_num;
+  const double denom = static_cast<double>(s->p.denom);
+  float ms = 0.f;
+  GDI_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  out->seconds = ms * 1e-3;
+  if (out->spins)
+    GDI_CUDA(cudaMemcpy(out->spins, s->spins.p, R * n, cudaMemcpyDeviceToHost));
+  if (out->scores) {
+    std::vector<DevTrace> fin(R);
+    GDI_CUDA(cudaMemcpy(fin.data(), s->final_out.p, R * sizeof(DevTrace), cudaMemcpyDeviceToHost));
+    for (size_t r = 0; r < R; r++) {
+      const long long sum = fin[r].sum, cut = fin[r].cut;
+      gdi_score& sc = out->scores[r];
+      sc.cut = cut;
+      sc.imbalance = sum < 0 ? -sum : sum;
+      sc.hamiltonian_scaled = A * sum * sum + B * cut;
+      sc.hamiltonian = static_cast<double>(sc.hamiltonian_scaled) / denom;
+      sc.balance_counter = fin[r].counter;
+    }
+  }
+  if (out->trace || out->counters) {
+    if (!(s->p.flags & GDI_FLAG_TRACE))
+      return fail(GDI_ERR_CONFIG, "trace requested but the session was created without GDI_FLAG_TRACE");
+    std::vector<DevTrace> tr(R * S);
+    std::vector<unsigned long long> st(R * (S + 1));
+    GDI_CUDA(cudaMemcpy(tr.data(), s->trace.p, tr.size() * sizeof(DevTrace), cudaMemcpyDeviceToHost));
+    GDI_CUDA(cudaMemcpy(st.data(), s->stamps.p, st.size() * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+    for (size_t r = 0; r < R; r++)
+      for (size_t k = 0; k < S; k++) {
+        const DevTrace& d = tr[r * S + k];
+        if (out->counters) out->counters[r * S + k] = d.counter;
+        if (out->trace) {
+          gdi_trace_rec& t = out->trace[r * S + k];
+          t.cut = d.cut;
+          t.imbalance = d.sum < 0 ? -d.sum : d.sum;
+          t.hamiltonian_scaled = A * d.sum * d.sum + B * d.cut;
+          t.hamiltonian = static_cast<double>(t.hamiltonian_scaled) / denom;
+          t.flip_probability = s->pf[k];
+          t.seconds = static_cast<double>(st[r * (S + 1) + k + 1] - st[r * (S + 1) + k]) * 1e-9;
+        }
+      }
+  }
+  if (out->snapshots) {
+    if (!(s->p.flags & GDI_FLAG_SNAPSHOTS))
+      return fail(GDI_ERR_CONFIG, "snapshots requested but the session was created without GDI_FLAG_SNAPSHOTS");
+    GDI_CUDA(cudaMemcpy(out->snapshots, s->snaps.p, R * (S + 1) * n, cudaMemcpyDeviceToHost));
+  }
+  return GDI_OK;
+}
+
+int gdi_session_launch_count(const gdi_session* s, int32_t* count) {
+  if (!s || !count) return fail(GDI_ERR_CONFIG, "NULL argument");
+  *count = 1;
+  return GDI_OK;
+}
+
+const char* gdi_session_kernel(const gdi_session* s) { return s ? s->plan.name : ""; }
+
+int gdi_session_destroy(gdi_session* s) {
+  if (s) {
+    cudaSetDevice(s->g->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    delete s;
+  }
+  return GDI_OK;
+}
+
+int gdi_anneal_batch(const gdi_graph* g, const gdi_params* p, const uint64_t* seeds,
+                     int32_t replicas, gdi_outputs* out) {
+  if (!seeds || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
+  gdi_params q = *p;
+  if (out->trace || out->counters) q.flags |= GDI_FLAG_TRACE;
+  if (out->snapshots) q.flags |= GDI_FLAG_SNAPSHOTS;
+  gdi_session* s = nullptr;
+  int rc = gdi_session_create(g, &q, replicas, nullptr, &s);
+  if (rc) return rc;
+  std::unique_ptr<gdi_session, int (*)(gdi_session*)> guard(s, gdi_session_destroy);
+  if ((rc = gdi_session_set_seeds(s, seeds))) return rc;
+  if ((rc = gdi_session_launch(s))) return rc;
+  if ((rc = gdi_session_sync(s))) return rc;
+  return gdi_session_fetch(s, out);
+}
+
+int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,
+                       int64_t b_num, int64_t denom, gdi_score* scores) {
+  if (!g || !spins || !scores) return fail(GDI_ERR_CONFIG, "NULL argument");
+  if (replicas < 1) return fail(GDI_ERR_CONFIG, "replicas must be >= 1");
+  if (denom <= 0) return fail(GDI_ERR_CONFIG, "denom must be positive");
+  int rc = use_device(g->device);
+  if (rc) return rc;
+  const size_t R = replicas, n = g->st.n;
+  for (size_t i = 0; i < R * n; i++)
+    if (spins[i] != 1 && spins[i] != -1) return fail(GDI_ERR_DOMAIN, "spin must be -1 or +1");
+  DevBuf d_s, d_out;
+  GDI_CUDA(d_s.alloc(R * n));
+  GDI_CUDA(d_out.alloc(R * 2 * sizeof(unsigned long long)));
+  GDI_CUDA(cudaMemcpy(d_s.p, spins, R * n, cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemset(d_out.p, 0, d_out.bytes));
+  EvalArgs a{g->csr(), d_s.as<int8_t>(), replicas, d_out.as<unsigned long long>()};
+  GDI_CUDA(eval_launch(a, !g->st.unit, nullptr));
+  std::vector<long long> res(R * 2);
+  GDI_CUDA(cudaMemcpy(res.data(), d_out.p, res.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  for (size_t r = 0; r < R; r++) {
+    const long long cut = res[2 * r], sum = res[2 * r + 1];
+    scores[r].cut = cut;
+    scores[r].imbalance = sum < 0 ? -sum : sum;
+    scores[r].hamiltonian_scaled = a_num * sum * sum + b_num * cut;
+    scores[r].hamiltonian = static_cast<double>(scores[r].hamiltonian_scaled) / static_cast<double>(denom);
+    scores[r].balance_counter = sum;
+  }
+  return GDI_OK;
+}
+
+}  // extern "C"
