@@ -240,7 +240,10 @@ def main():
     params.sweeps, params.deterministic = sweeps, True
     seeds = np.arange(1 + rank * R, 1 + (rank + 1) * R, dtype=np.uint64)
 
-    stream = torch.cuda.current_stream(dev)
+    # a real (non-legacy) stream: the session launches on it and the torch
+    # events below are recorded on the same stream
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sess = pi.Session(prob, params, R, stream=stream.cuda_stream, trace=True, device=local)
     sess.set_seeds(seeds)
     # L2 flush buffer (> 126 MB L2) rewritten between timed steps

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -78,6 +79,8 @@ struct gdi_graph {
   int device = 0;
   GraphStats st;
   DevBuf off, col, w;
+  DevBuf far_col, far_meta, win_pos, win_neg;  // k1_pipe preprocessing
+  PipeGraph pipe;
   int64_t bytes = 0;
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), w.as<int32_t>(), st.n}; }
 };
@@ -89,9 +92,12 @@ struct gdi_session {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ExactPlan plan;
+  PipePlan pplan;
+  bool use_pipe = false;
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
-  DevBuf seeds, thr_d, spins, trace, stamps, snaps, final_out;
+  std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
+  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
   ~gdi_session() {
@@ -124,15 +130,77 @@ int check_params(const gdi_params* p) {
 // pf_k by the reference's iterated product (anneal.cpp:183, :39-45) and the
 // exactly equivalent integer threshold on the 53-bit draw:
 //   (x>>11) * 2^-53 <= pf  <=>  (x>>11) <= floor(pf * 2^53)   (pf > 0)
-void schedule(const gdi_params& p, std::vector<double>& pf, std::vector<long long>& thr) {
+// The pipe kernel tests the raw draw directly: (x >> 11) <= T  <=>
+// x <= T*2^11 + 2047, with T clamped to 2^53 - 1 (x >> 11 never exceeds it).
+void schedule(const gdi_params& p, std::vector<double>& pf, std::vector<long long>& thr,
+              std::vector<unsigned long long>& tmask) {
   pf.resize(p.sweeps);
   thr.resize(p.sweeps);
+  tmask.resize(p.sweeps);
   double v = p.flip_fraction0;
   for (int k = 0; k < p.sweeps; k++) {
     pf[k] = v;
     thr[k] = v > 0.0 ? static_cast<long long>(std::floor(std::ldexp(v, 53))) : -1LL;
+    const unsigned long long t = thr[k] < 0 ? 0ull : std::min<unsigned long long>(thr[k], (1ull << 53) - 1);
+    tmask[k] = (t << 11) | 2047ull;
     v *= p.decay_rate;
   }
+}
+
+// Spin-independent split of every row into far entries and the window mask
+// of the L vertices visited just before it (see k1_pipe.cu).
+int build_pipe(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const int32_t* weights) {
+  const int32_t n = g->st.n;
+  const int L = pipe_window();
+  if (n < 2 * L) return GDI_OK;  // not eligible: k1_exact only
+  for (int64_t e = 0; e < offsets[n]; e++)
+    if (weights && weights[e] != 1 && weights[e] != -1) return GDI_OK;
+  std::vector<int4> cols, meta(n);
+  std::vector<uint32_t> wp(n, 0u), wn(n, 0u);
+  std::vector<int32_t> pos, neg;
+  for (int32_t i = 0; i < n; i++) {
+    pos.clear();
+    neg.clear();
+    for (int64_t e = offsets[i]; e < offsets[i + 1]; e++) {
+      const int32_t j = nbr[e];
+      const bool minus = weights && weights[e] < 0;
+      const int32_t k = static_cast<int32_t>(((static_cast<int64_t>(i) - j) % n + n) % n);  // 1..n-1
+      if (k >= 1 && k <= L)
+        (minus ? wn[i] : wp[i]) |= 1u << (k - 1);
+      else
+        (minus ? neg : pos).push_back(j);
+    }
+    const int dp = static_cast<int>(pos.size()), dn = static_cast<int>(neg.size());
+    while (pos.size() % 4) pos.push_back(n);
+    while (neg.size() % 4) neg.push_back(n);
+    const int off4 = static_cast<int>(cols.size());
+    for (size_t q = 0; q < pos.size(); q += 4) cols.push_back(make_int4(pos[q], pos[q + 1], pos[q + 2], pos[q + 3]));
+    for (size_t q = 0; q < neg.size(); q += 4) cols.push_back(make_int4(neg[q], neg[q + 1], neg[q + 2], neg[q + 3]));
+    const int fconst = (dp - dn) + __builtin_popcount(wp[i]) - __builtin_popcount(wn[i]);
+    meta[i] = make_int4(off4, static_cast<int>(pos.size() / 4), static_cast<int>(neg.size() / 4), fconst);
+  }
+  if (cols.empty()) cols.push_back(make_int4(n, n, n, n));
+  GDI_CUDA(g->far_col.alloc(cols.size() * sizeof(int4)));
+  GDI_CUDA(g->far_meta.alloc(meta.size() * sizeof(int4)));
+  GDI_CUDA(g->win_pos.alloc(n * sizeof(uint32_t)));
+  GDI_CUDA(g->win_neg.alloc(n * sizeof(uint32_t)));
+  GDI_CUDA(cudaMemcpy(g->far_col.p, cols.data(), cols.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemcpy(g->far_meta.p, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemcpy(g->win_pos.p, wp.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemcpy(g->win_neg.p, wn.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  g->pipe.ok = true;
+  g->pipe.n_words = (n + 1 + 3) & ~3;
+  g->pipe.far_col = g->far_col.as<int4>();
+  g->pipe.far_meta = g->far_meta.as<int4>();
+  g->pipe.win_pos = g->win_pos.as<uint32_t>();
+  g->pipe.win_neg = g->win_neg.as<uint32_t>();
+  return GDI_OK;
+}
+
+// GDI_FORCE_KERNEL=exact|pipe pins the exact-mode variant (tests run both).
+const char* forced_kernel() {
+  const char* e = std::getenv("GDI_FORCE_KERNEL");
+  return e ? e : "";
 }
 
 }  // namespace
@@ -206,7 +274,9 @@ int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_
     GDI_CUDA(g->w.alloc(nnz * sizeof(int32_t)));
     GDI_CUDA(cudaMemcpy(g->w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
-  g->bytes = static_cast<int64_t>(g->off.bytes + g->col.bytes + g->w.bytes);
+  if ((rc = build_pipe(g.get(), offsets, nbr, weights))) return rc;
+  g->bytes = static_cast<int64_t>(g->off.bytes + g->col.bytes + g->w.bytes + g->far_col.bytes +
+                                  g->far_meta.bytes + g->win_pos.bytes + g->win_neg.bytes);
   *out = g.release();
   return GDI_OK;
 }
@@ -244,10 +314,15 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   s->g = g;
   s->p = *p;
   s->replicas = replicas;
-  schedule(s->p, s->pf, s->thr);
+  schedule(s->p, s->pf, s->thr, s->tmask);
   // Both strategies coincide in the exact mode (reference acceptance.cpp
-  // criterion 8); the throughput kernel is selected in gdi_abi_k2.cu.
-  if (exact_plan(g->st, replicas, &s->plan))
+  // criterion 8). Prefer the warp-specialised pipe kernel when it applies.
+  const std::string force = forced_kernel();
+  const bool pipe_ok =
+      force != "exact" && pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
+  if (force == "pipe" && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
+  s->use_pipe = pipe_ok;
+  if (!pipe_ok && exact_plan(g->st, replicas, &s->plan))
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
 
   if (stream) {
@@ -261,6 +336,7 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   const size_t R = replicas, n = g->st.n, S = p->sweeps;
   GDI_CUDA(s->seeds.alloc(R * sizeof(uint64_t)));
   GDI_CUDA(s->thr_d.alloc(S * sizeof(long long)));
+  GDI_CUDA(s->tmask_d.alloc(S * sizeof(unsigned long long)));
   GDI_CUDA(s->spins.alloc(R * n));
   GDI_CUDA(s->final_out.alloc(R * sizeof(DevTrace)));
   if (p->flags & GDI_FLAG_TRACE) {
@@ -269,6 +345,8 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   }
   if (p->flags & GDI_FLAG_SNAPSHOTS) GDI_CUDA(s->snaps.alloc(R * (S + 1) * n));
   GDI_CUDA(cudaMemcpyAsync(s->thr_d.p, s->thr.data(), S * sizeof(long long),
+                           cudaMemcpyHostToDevice, s->stream));
+  GDI_CUDA(cudaMemcpyAsync(s->tmask_d.p, s->tmask.data(), S * sizeof(unsigned long long),
                            cudaMemcpyHostToDevice, s->stream));
   GDI_CUDA(cudaStreamSynchronize(s->stream));
   *out = s.release();
@@ -286,6 +364,32 @@ int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
 int gdi_session_launch(gdi_session* s) {
   if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
   GDI_CUDA(cudaSetDevice(s->g->device));
+  if (s->use_pipe) {
+    PipeArgs a{};
+    a.g = s->g->csr();
+    a.far_col = s->g->pipe.far_col;
+    a.far_meta = s->g->pipe.far_meta;
+    a.win_pos = s->g->pipe.win_pos;
+    a.win_neg = s->g->pipe.win_neg;
+    a.n_words = s->g->pipe.n_words;
+    a.sweeps = s->p.sweeps;
+    a.replicas = s->replicas;
+    a.seeds = s->seeds.as<uint64_t>();
+    a.thr = s->thr_d.as<long long>();
+    a.tmask = s->tmask_d.as<unsigned long long>();
+    a.a4 = static_cast<int32_t>(4 * s->p.a_num);
+    a.b = static_cast<int32_t>(s->p.b_num);
+    a.spins_out = s->spins.as<int8_t>();
+    a.trace = s->trace.as<DevTrace>();
+    a.stamps = s->stamps.as<unsigned long long>();
+    a.snaps = s->snaps.as<int8_t>();
+    a.final_out = s->final_out.as<DevTrace>();
+    GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
+    GDI_CUDA(pipe_launch(s->pplan, a, s->stream));
+    GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
+    s->launched = true;
+    return GDI_OK;
+  }
   ExactArgs a{};
   a.g = s->g->csr();
   a.n_pad = s->plan.n_pad;
@@ -377,7 +481,10 @@ int gdi_session_launch_count(const gdi_session* s, int32_t* count) {
   return GDI_OK;
 }
 
-const char* gdi_session_kernel(const gdi_session* s) { return s ? s->plan.name : ""; }
+const char* gdi_session_kernel(const gdi_session* s) {
+  if (!s) return "";
+  return s->use_pipe ? s->pplan.name : s->plan.name;
+}
 
 int gdi_session_destroy(gdi_session* s) {
   if (s) {

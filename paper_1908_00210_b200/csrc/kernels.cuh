@@ -41,6 +41,33 @@ struct ExactArgs {
   DevTrace* final_out;    // [R]
 };
 
+// k1_pipe (warp-specialised exact kernel). Far CSR: per vertex i,
+// far_meta[i] = {first int4 index, #int4 of +1 neighbours, #int4 of -1
+// neighbours, fconst}; entries padded with index n (a word that reads 0).
+// win_pos/win_neg[i]: bit k-1 set when vertex (i-k) mod n is a +1 / -1
+// neighbour, k = 1..32.
+struct PipeArgs {
+  DevCsr g;                        // full CSR (initial cut only)
+  const int4* far_col;
+  const int4* far_meta;
+  const uint32_t* win_pos;
+  const uint32_t* win_neg;
+  int32_t n_words;                 // words in shared memory (>= n + 1)
+  int32_t sweeps;
+  int32_t replicas;
+  int32_t rc;                      // replicas (lanes) per CTA
+  const uint64_t* seeds;
+  const long long* thr;            // [sweeps] floor(pf*2^53), -1 = never
+  const unsigned long long* tmask; // [sweeps] thr*2^11 + 2047 (saturated)
+  int32_t a4;                      // 4*a_num (narrow)
+  int32_t b;                       // b_num (narrow)
+  int8_t* spins_out;
+  DevTrace* trace;
+  unsigned long long* stamps;
+  int8_t* snaps;
+  DevTrace* final_out;
+};
+
 struct EvalArgs {
   DevCsr g;
   const int8_t* spins;    // [R][n]

@@ -31,6 +31,32 @@ struct ExactPlan {
 int exact_plan(const GraphStats& st, int32_t replicas, ExactPlan* plan);
 cudaError_t exact_launch(const ExactPlan& plan, const ExactArgs& args, cudaStream_t stream);
 
+// Spin-independent preprocessing of a graph for k1_pipe (built once in
+// gdi_graph_create when every |w| == 1 and n >= 64).
+struct PipeGraph {
+  bool ok = false;
+  int32_t n_words = 0;
+  int4* far_col = nullptr;   // device
+  int4* far_meta = nullptr;  // device
+  uint32_t* win_pos = nullptr;
+  uint32_t* win_neg = nullptr;
+};
+
+struct PipePlan {
+  const void* fn = nullptr;
+  int rc = 8;
+  int block = 256;
+  int grid = 1;
+  int smem = 0;
+  const char* name = "";
+};
+
+int pipe_window();
+size_t pipe_smem_bytes(int n_words, int nwarps);
+int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b,
+              int32_t sweeps, PipePlan* plan);
+cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);
+
 // K3 fused exact evaluation: {cut, sum} per replica into a zeroed buffer.
 cudaError_t eval_launch(const EvalArgs& args, bool weighted, cudaStream_t stream);
 

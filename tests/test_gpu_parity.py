@@ -16,6 +16,14 @@ from tests.helpers import fnv_rows, golden_configs, product_graph, small_cases
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["auto", "exact"])
+def kernel_variant(request, monkeypatch):
+    """Run every parity test on both exact-mode kernels: the warp-specialised
+    pipe kernel (chosen automatically where it applies) and k1_exact."""
+    monkeypatch.setenv("GDI_FORCE_KERNEL", request.param)
+    return request.param
+
+
 def det_params(sweeps=1000, pf0=0.04, decay=0.99, seed=1, strategy=pi.Strategy.gdi):
     p = pi.AnnealParams()
     p.sweeps, p.flip_fraction0, p.decay_rate = sweeps, pf0, decay
@@ -152,7 +160,7 @@ def test_evaluate_batch_k3_matches_oracle():
             assert sc["hamiltonian_scaled"][r] == bal * bal + 4 * cut
 
 
-def test_session_device_resident_matches_batch():
+def test_session_device_resident_matches_batch(kernel_variant):
     g = pi.random_graph(2000, 19990, 22)
     prob = pi.MinCutProblem.with_default_coefficients(g)
     seeds = np.arange(1, 65, dtype=np.uint64)
@@ -165,3 +173,26 @@ def test_session_device_resident_matches_batch():
     assert np.array_equal(got["spins"], ref["spins"])
     assert np.array_equal(got["trace"], ref["trace"])
     assert s.launch_count >= 1 and s.kernel
+    assert ("pipe" in s.kernel) == (kernel_variant == "auto")
+
+
+def test_pipe_window_edge_cases_match_oracle():
+    # n just above 2L, dense rows (window masks heavily populated), +-1 weights
+    rng = np.random.default_rng(11)
+    for n, m, signed in ((64, 300, False), (65, 2000, True), (97, 4000, False), (130, 260, True)):
+        seen, edges = set(), []
+        while len(edges) < m:
+            u, v = sorted(int(x) for x in rng.integers(0, n, 2))
+            if u == v or (u, v) in seen:
+                continue
+            seen.add((u, v))
+            edges.append((u, v, int(rng.choice([-1, 1])) if signed else 1))
+        e = np.array(edges, dtype=np.int64)
+        og = o.csr_from_edges(n, e[:, 0], e[:, 1], e[:, 2])
+        prob = pi.MinCutProblem.with_default_coefficients(pi.Graph.from_edges(n, edges))
+        seeds = np.arange(1, 41, dtype=np.uint64)
+        out = pi.anneal_batch(prob, det_params(30, 0.3, 0.9), seeds, trace=True)
+        for i, s in enumerate(seeds.tolist()):
+            ref = o.anneal(og, s, 30, 0.3, 0.9)
+            assert out["spins"][i].tolist() == ref["spins"].tolist(), (n, m, s)
+            assert out["trace"][i].tolist() == ref["trace"].tolist(), (n, m, s)
