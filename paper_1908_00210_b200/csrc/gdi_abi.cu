@@ -97,7 +97,7 @@ struct gdi_session {
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
-  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out;
+  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
   ~gdi_session() {
@@ -148,16 +148,20 @@ void schedule(const gdi_params& p, std::vector<double>& pf, std::vector<long lon
 }
 
 // Spin-independent split of every row into far entries and the window mask
-// of the L vertices visited just before it (see k1_pipe.cu).
+// of the L vertices visited just before it (see k1_pipe.cu). far list per
+// vertex: +1 neighbours, then -1 neighbours; meta = {offset, #pos, #neg,
+// fconst} with fconst = (#pos - #neg) + popc(mask+) - popc(mask-).
 int build_pipe(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const int32_t* weights) {
   const int32_t n = g->st.n;
   const int L = pipe_window();
   if (n < 2 * L) return GDI_OK;  // not eligible: k1_exact only
   for (int64_t e = 0; e < offsets[n]; e++)
     if (weights && weights[e] != 1 && weights[e] != -1) return GDI_OK;
-  std::vector<int4> cols, meta(n);
+  std::vector<int32_t> cols;
+  std::vector<int4> meta(n);
   std::vector<uint32_t> wp(n, 0u), wn(n, 0u);
   std::vector<int32_t> pos, neg;
+  cols.reserve(static_cast<size_t>(offsets[n]));
   for (int32_t i = 0; i < n; i++) {
     pos.clear();
     neg.clear();
@@ -170,27 +174,25 @@ int build_pipe(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const i
       else
         (minus ? neg : pos).push_back(j);
     }
+    const int off = static_cast<int>(cols.size());
+    cols.insert(cols.end(), pos.begin(), pos.end());
+    cols.insert(cols.end(), neg.begin(), neg.end());
     const int dp = static_cast<int>(pos.size()), dn = static_cast<int>(neg.size());
-    while (pos.size() % 4) pos.push_back(n);
-    while (neg.size() % 4) neg.push_back(n);
-    const int off4 = static_cast<int>(cols.size());
-    for (size_t q = 0; q < pos.size(); q += 4) cols.push_back(make_int4(pos[q], pos[q + 1], pos[q + 2], pos[q + 3]));
-    for (size_t q = 0; q < neg.size(); q += 4) cols.push_back(make_int4(neg[q], neg[q + 1], neg[q + 2], neg[q + 3]));
     const int fconst = (dp - dn) + __builtin_popcount(wp[i]) - __builtin_popcount(wn[i]);
-    meta[i] = make_int4(off4, static_cast<int>(pos.size() / 4), static_cast<int>(neg.size() / 4), fconst);
+    meta[i] = make_int4(off, dp, dn, fconst);
   }
-  if (cols.empty()) cols.push_back(make_int4(n, n, n, n));
-  GDI_CUDA(g->far_col.alloc(cols.size() * sizeof(int4)));
+  cols.push_back(n);  // never empty
+  GDI_CUDA(g->far_col.alloc(cols.size() * sizeof(int32_t)));
   GDI_CUDA(g->far_meta.alloc(meta.size() * sizeof(int4)));
   GDI_CUDA(g->win_pos.alloc(n * sizeof(uint32_t)));
   GDI_CUDA(g->win_neg.alloc(n * sizeof(uint32_t)));
-  GDI_CUDA(cudaMemcpy(g->far_col.p, cols.data(), cols.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemcpy(g->far_col.p, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   GDI_CUDA(cudaMemcpy(g->far_meta.p, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice));
   GDI_CUDA(cudaMemcpy(g->win_pos.p, wp.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
   GDI_CUDA(cudaMemcpy(g->win_neg.p, wn.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
   g->pipe.ok = true;
   g->pipe.n_words = (n + 1 + 3) & ~3;
-  g->pipe.far_col = g->far_col.as<int4>();
+  g->pipe.far_col = g->far_col.as<int32_t>();
   g->pipe.far_meta = g->far_meta.as<int4>();
   g->pipe.win_pos = g->win_pos.as<uint32_t>();
   g->pipe.win_neg = g->win_neg.as<uint32_t>();
@@ -339,6 +341,8 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   GDI_CUDA(s->tmask_d.alloc(S * sizeof(unsigned long long)));
   GDI_CUDA(s->spins.alloc(R * n));
   GDI_CUDA(s->final_out.alloc(R * sizeof(DevTrace)));
+  GDI_CUDA(s->watchdog.alloc(8 * sizeof(int)));
+  GDI_CUDA(s->prof.alloc(16 * sizeof(unsigned long long)));
   if (p->flags & GDI_FLAG_TRACE) {
     GDI_CUDA(s->trace.alloc(R * S * sizeof(DevTrace)));
     GDI_CUDA(s->stamps.alloc(R * (S + 1) * sizeof(unsigned long long)));
@@ -384,6 +388,10 @@ int gdi_session_launch(gdi_session* s) {
     a.stamps = s->stamps.as<unsigned long long>();
     a.snaps = s->snaps.as<int8_t>();
     a.final_out = s->final_out.as<DevTrace>();
+    a.watchdog = s->watchdog.as<int>();
+    a.prof = s->prof.as<unsigned long long>();
+    GDI_CUDA(cudaMemsetAsync(s->watchdog.p, 0, s->watchdog.bytes, s->stream));
+    if (s->pplan.prof) GDI_CUDA(cudaMemsetAsync(s->prof.p, 0, s->prof.bytes, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
     GDI_CUDA(pipe_launch(s->pplan, a, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
@@ -411,11 +419,33 @@ int gdi_session_launch(gdi_session* s) {
   return GDI_OK;
 }
 
+// A stalled k1_pipe pipeline aborts itself (watchdog) instead of hanging;
+// surface that as a runtime error rather than returning wrong results.
+static int check_watchdog(gdi_session* s) {
+  if (!s->use_pipe) return GDI_OK;
+  if (s->pplan.prof) {
+    unsigned long long c[16] = {0};
+    GDI_CUDA(cudaMemcpy(c, s->prof.p, sizeof c, cudaMemcpyDeviceToHost));
+    const double nb = c[4] ? static_cast<double>(c[4]) : 1.0;
+    std::fprintf(stderr,
+                 "[k1_pipe prof] per batch (cycles): decider total %.1f wait_ready %.1f wait_draws %.1f "
+                 "replays %.4f | producer total %.1f wait %.1f | gatherers(sum) total %.1f wait %.1f\n",
+                 c[0] / nb, c[1] / nb, c[2] / nb, c[3] / nb, c[5] / nb, c[6] / nb, c[7] / nb, c[8] / nb);
+  }
+  int w[8] = {0};
+  GDI_CUDA(cudaMemcpy(w, s->watchdog.p, sizeof w, cudaMemcpyDeviceToHost));
+  if (w[0] != 0)
+    return fail(GDI_ERR_RUNTIME, "k1_pipe watchdog fired: stage " + std::to_string(w[0]) + " block " +
+                                     std::to_string(w[1]) + " thread " + std::to_string(w[2]) + " (" +
+                                     std::to_string(w[3]) + ", " + std::to_string(w[4]) + ")");
+  return GDI_OK;
+}
+
 int gdi_session_sync(gdi_session* s) {
   if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
   GDI_CUDA(cudaSetDevice(s->g->device));
   GDI_CUDA(cudaStreamSynchronize(s->stream));
-  return GDI_OK;
+  return check_watchdog(s);
 }
 
 int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
@@ -423,6 +453,7 @@ int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
   if (!s->launched) return fail(GDI_ERR_CONFIG, "session has not been launched");
   GDI_CUDA(cudaSetDevice(s->g->device));
   GDI_CUDA(cudaStreamSynchronize(s->stream));
+  if (int rc = check_watchdog(s)) return rc;
   const size_t R = s->replicas, n = s->g->st.n, S = s->p.sweeps;
   const long long A = s->p.a_num, B = s->p.b_num;
   const double denom = static_cast<double>(s->p.denom);

@@ -2,35 +2,54 @@
 //
 // Same contract as k1_exact.cu (bit-identical to the reference's
 // single-worker anneal, reference proj/src/anneal.cpp:132-231), restructured
-// so the serial per-replica chain carries only ALU work:
+// so the serial per-replica chain carries only a few ALU ops per visit.
 //
-//  * lane = replica. A CTA owns RC <= 32 replicas; their spins of vertex v
-//    are one 32-bit word words[v] (bit l = replica l is +1) in shared memory,
+// Warp roles inside one CTA (RC <= 32 replicas, lane = replica):
+//  * spin words: words[v] (bit l = replica l is +1) in shared memory,
 //    written by the decider with one __ballot_sync per visit.
-//  * gatherer warps (1..NG) run ahead of the decider. For global visit
-//    U = sweep*n + i they compute, for all lanes at once, the neighbour field
-//    of vertex i EXCLUDING the L=32 vertices visited immediately before U
-//    ((i-1)..(i-L) mod n). Every other neighbour's latest visit is <= U-L-1,
-//    so its word is final once the decider has published progress P >= U-L,
-//    and no later write can happen before U. The spin-independent split of
-//    each adjacency row into "far" entries and a 32-bit "window" mask is
-//    precomputed once per graph on the host (gdi_graph_create).
-//  * the decider warp (0) adds the window part exactly from a 32-bit history
-//    of its own last 32 decisions: field = f_far + 2*popc(hist & mask+) -
-//    2*popc(hist & mask-) (constants folded into f_far), then runs the
-//    reference decision (anneal.cpp:94-127) in 32-bit arithmetic (selected
-//    only when |4A|(n+1) + |B| max_i sum_j |w_ij| < 2^31, so it equals the
-//    int64 reference), the xoshiro256++ stream-1 draws (coin only on exact
-//    ties) and the flip test x <= floor(pf*2^53)*2^11 + 2047.
-//  * gatherer -> decider: queue of QB batches x B visits of {f_far, own} per
-//    lane + the window masks; release/acquire on per-batch sequence numbers.
-//    decider -> gatherers: progress counter P (release per batch).
+//  * gatherers (NG warps): for global visit U = sweep*n + i they compute the
+//    neighbour field of vertex i for every replica EXCLUDING the L=32
+//    vertices visited immediately before U ((i-1)..(i-L) mod n). Every other
+//    neighbour's latest visit is <= U-L-1, so its word is final once the
+//    decider has published progress P >= U-L, and no later write can happen
+//    before U. The spin-independent split of each adjacency row into "far"
+//    entries and a 32-bit "window" mask is precomputed once per graph
+//    (gdi_graph_create). A gatherer puts one far neighbour per lane (one
+//    coalesced index load, one shared-memory word load per lane), then one
+//    ballot + popc per replica turns the words into per-replica counts.
+//  * producer (1 warp): runs each replica's xoshiro256++ stream 1
+//    (rng.hpp:23-33) ahead of the decider into a per-lane shared-memory ring.
+//  * decider (warp 0): adds the window part exactly from a 32-bit history H
+//    of its own last decisions (field = f_far + 2 popc(H & mask+) -
+//    2 popc(H & mask-), constants folded into f_far) and applies the
+//    reference decision (anneal.cpp:94-127) in 32-bit arithmetic on
+//    (4A, B) / gcd(4A, B) (same sign, same ties; selected only when the
+//    reduced |4A|(n+3) + |B|(max_i sum_j |w_ij| + 2) < 2^31). Splitting off
+//    the newest history bit gives
+//        diff_t = W_t + fin_{t-1} * V_t,   fin_t = ((diff_t < 0) ^ flip_t) ? +1 : -1
+//    with W_t, V_t, flip_t independent of fin_{t-1}.
+//  * draws: a visit consumes one draw, preceded by a coin draw on an exact
+//    tie (anneal.cpp:106-121). Within a chunk of visits each lane may absorb
+//    one tie (its later visits shift by one draw, handled with selects); a
+//    second tie of the same (active) lane in a chunk is rare and triggers an
+//    exact out-of-line replay of the batch. The flip test is the exact
+//    integer form x <= floor(pf*2^53)*2^11 + 2047.
+//  * sync: gatherer -> decider per-batch sequence numbers; decider ->
+//    gatherers progress P; producer <-> decider per-lane ring positions; all
+//    release/acquire at CTA scope on shared memory. Every polling loop has a
+//    watchdog that aborts the CTA (reported as an error) instead of hanging.
+//
+// The hot loops are kept small on purpose: warp specialisation runs three
+// different loops on one SM, and a first version with fully unrolled
+// gatherers spent 40% of the decider's stall samples on instruction-cache
+// misses (profiles/).
 //
 // Restricted to |w| == 1 graphs (unit or +-1), n >= 2L, sweeps*n < 2^31;
-// everything else runs k1_exact.cu. Incremental exact cut for the trace as
-// in k1_exact.cu.
-#include <cuda/atomic>
+// everything else runs k1_exact.cu. Exact incremental cut for the trace as
+// in k1_exact.cu (per-sweep int32 delta: |delta| <= 2m < 2^31).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "device_rng.cuh"
 #include "kernels.cuh"
@@ -40,223 +59,506 @@ namespace gdi {
 
 namespace {
 
-constexpr int kWin = 32;   // window L (history bits)
-constexpr int kBatch = 4;  // visits per queue batch (B)
-constexpr int kQB = 16;    // queue depth in batches (QB*B > L + 1)
+constexpr int kWin = 32;      // window L (history bits)
+constexpr int kBatch = 8;     // visits per queue batch (B)
+constexpr int kChunk = 4;     // decider visits unrolled per inner iteration
+constexpr int kQB = 8;        // queue depth in batches (QB*B > L + B)
+constexpr int kNW = 8;        // warps per CTA
+constexpr int kProducer = 4;  // warp id of the producer (shares SMSP 0 with the decider)
+constexpr int kNG = kNW - 2;  // gatherer warps
+constexpr int kRing = 64;     // draws buffered per lane (power of two, >= 4B)
+constexpr long long kWatchdog = 1LL << 26;
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  cuda::atomic_ref<const int, cuda::thread_scope_block> r(*p);
-  return r.load(cuda::memory_order_acquire);
+__device__ __forceinline__ unsigned saddr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-  cuda::atomic_ref<int, cuda::thread_scope_block> r(*p);
-  r.store(v, cuda::memory_order_release);
+__device__ __forceinline__ int ld_acquire(unsigned a) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned a, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-struct PipeSmem {
-  uint32_t* words;  // [n_pad] (+1 zero word at index n for padding entries)
-  int2* q;          // [QB][B][32] {f_far, own}
-  uint2* qm;        // [QB][B] {mask+, mask-}
-  int* ready;       // [QB]
-  int* progress;    // [1]
-  long long* part;  // [NW][32] initial-cut partials
+// Shared-memory layout (byte offsets from the dynamic smem base).
+struct Layout {
+  int ring, q, qm, part, ready, genpos, cons, progress, done, abort, total;
+  __host__ __device__ static Layout make(int n_words) {
+    Layout L;
+    L.ring = ((n_words * 4) + 15) & ~15;
+    L.q = L.ring + 8 * kRing * 32;
+    L.qm = L.q + 8 * kQB * kBatch * 32;
+    L.part = L.qm + 8 * kQB * kBatch;
+    L.ready = L.part + 8 * kNW * 32;
+    L.genpos = L.ready + 4 * kQB;
+    L.cons = L.genpos + 4 * 32;
+    L.progress = L.cons + 4 * 32;
+    L.done = L.progress + 4;
+    L.abort = L.done + 4;
+    L.total = L.abort + 8;
+    return L;
+  }
 };
 
-__device__ __forceinline__ PipeSmem carve(unsigned char* base, int n_words, int nwarps) {
-  PipeSmem s;
-  s.words = reinterpret_cast<uint32_t*>(base);
-  unsigned char* p = base + static_cast<size_t>(n_words) * 4;
-  s.q = reinterpret_cast<int2*>(p);
-  p += sizeof(int2) * kQB * kBatch * 32;
-  s.qm = reinterpret_cast<uint2*>(p);
-  p += sizeof(uint2) * kQB * kBatch;
-  s.part = reinterpret_cast<long long*>(p);
-  p += sizeof(long long) * nwarps * 32;
-  s.ready = reinterpret_cast<int*>(p);
-  p += sizeof(int) * kQB;
-  s.progress = reinterpret_cast<int*>(p);
-  return s;
+// Decider state between visits. H = history used by the previous visit
+// (bit k-1 = spin of the visit k before it), fin/own = that visit's final and
+// prior spin, AG = a*G before that visit's change was applied (a = reduced
+// 4A), pos = first unconsumed draw.
+struct DState {
+  uint32_t H;
+  int fin, own, AG, dcut, pos;
+};
+
+struct Sweep {  // per-sweep bookkeeping handled at a barrier
+  long long cut;
+  int sweep, i;
+  unsigned long long tm;
+  bool en;
+};
+
+struct ReplayIO {
+  DState st;
+  Sweep sw;
+};
+
+// Safety net: record why a polling loop gave up and raise the abort flag.
+__device__ __noinline__ void watchdog(const PipeArgs& a, unsigned abort_s, int where, long long x, long long y) {
+  st_release(abort_s, 1);
+  if (a.watchdog != nullptr && atomicCAS(a.watchdog, 0, where) == 0) {
+    a.watchdog[1] = static_cast<int>(blockIdx.x);
+    a.watchdog[2] = static_cast<int>(threadIdx.x);
+    a.watchdog[3] = static_cast<int>(x);
+    a.watchdog[4] = static_cast<int>(y);
+  }
 }
 
-template <bool SIGNED, int NG>
-__global__ void __launch_bounds__(32 * (NG + 1), 1) k1_pipe(const PipeArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int NW = NG + 1;
+__device__ __forceinline__ uint64_t ring_at(const uint64_t* ring, int pos, int lane) {
+  return ring[(pos & (kRing - 1)) * 32 + lane];
+}
+
+// record_barrier (anneal.cpp:165-187): exact cut, spin sum, counter.
+__device__ __noinline__ void record_barrier(const PipeArgs& a, const uint32_t* words, Sweep& sw, int dcut, int G,
+                                            int lane, bool active, size_t rs) {
+  const int n = a.g.n;
+  sw.cut += dcut;
+  if (active) {
+    if (a.trace != nullptr) a.trace[rs * a.sweeps + sw.sweep] = DevTrace{sw.cut, G, G};
+    if (a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1) + sw.sweep + 1] = globaltimer_ns();
+  }
+  if (a.snaps != nullptr) {
+    __syncwarp();
+    if (active) {
+      int8_t* dst = a.snaps + (rs * (a.sweeps + 1) + sw.sweep + 1) * n;
+      for (int v = 0; v < n; v++) dst[v] = ((words[v] >> lane) & 1u) ? 1 : -1;
+    }
+  }
+  if (++sw.sweep < a.sweeps) {
+    sw.tm = a.tmask[sw.sweep];
+    sw.en = a.thr[sw.sweep] >= 0;
+  }
+}
+
+// Exact replay of one batch (rare): per-visit draw accounting straight from
+// the ring, queue entries re-read from the (still valid) slot.
+template <bool SIGNED>
+__device__ __noinline__ void replay_batch(const PipeArgs& a, uint32_t* words, const uint64_t* ring, const int2* qs,
+                                          const uint2* ms, ReplayIO& io, int nv, int lane, bool active, size_t rs) {
+  const int n = a.g.n, a4 = a.a4, bb = a.b;
+  DState& st = io.st;
+  Sweep& sw = io.sw;
+  uint32_t hist = (st.H << 1) | static_cast<uint32_t>(st.fin > 0);
+  int AG = st.AG + a4 * (st.fin - st.own);
+  int pos = st.pos, fin = st.fin, own = st.own;
+  for (int t = 0; t < nv; t++) {
+    const int2 fo = qs[t * 32];
+    const uint2 mw = ms[t];
+    int p = __popc(hist & mw.x);
+    if (SIGNED) p -= __popc(hist & mw.y);
+    const int f = fo.x + 2 * p;
+    own = fo.y;
+    const int diff = AG - a4 * own - bb * f;
+    int c;
+    if (diff == 0) {
+      c = (static_cast<long long>(ring_at(ring, pos, lane)) < 0) ? 1 : -1;
+      pos++;
+    } else {
+      c = diff < 0 ? 1 : -1;
+    }
+    fin = (sw.en && ring_at(ring, pos, lane) <= sw.tm) ? -c : c;
+    pos++;
+    const int d = fin - own;
+    AG += a4 * d;
+    st.dcut -= (d >> 1) * f;
+    const unsigned w = __ballot_sync(0xffffffffu, fin > 0);
+    if (lane == 0) words[sw.i] = w;
+    if (t + 1 < nv) hist = (hist << 1) | static_cast<uint32_t>(fin > 0);
+    if (++sw.i == n) {
+      sw.i = 0;
+      record_barrier(a, words, sw, st.dcut, AG / a4, lane, active, rs);
+      st.dcut = 0;
+    }
+  }
+  st.H = hist;
+  st.fin = fin;
+  st.own = own;
+  st.AG = AG - a4 * (fin - own);
+  st.pos = pos;
+}
+
+// PROF: accumulate clock64 wait/work counters per role into a.prof
+// (profiling builds only, GDI_PIPE_PROFILE=1; see gdi_abi.cu).
+template <bool SIGNED, bool UNITAB, bool PROF>
+__global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.g.n;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int replica = blockIdx.x * a.rc + lane;
-  const bool active = lane < a.rc && replica < a.replicas;
-  PipeSmem sm = carve(smem_raw, a.n_words, NW);
+  const int rc = a.rc;
+  const int replica = blockIdx.x * rc + lane;
+  const bool active = lane < rc && replica < a.replicas;
+  const Layout lay = Layout::make(a.n_words);
+  uint32_t* words = reinterpret_cast<uint32_t*>(smem);
+  uint64_t* ring = reinterpret_cast<uint64_t*>(smem + lay.ring);
+  int2* q = reinterpret_cast<int2*>(smem + lay.q);
+  uint2* qm = reinterpret_cast<uint2*>(smem + lay.qm);
+  long long* part = reinterpret_cast<long long*>(smem + lay.part);
+  int* ready = reinterpret_cast<int*>(smem + lay.ready);
+  int* genpos = reinterpret_cast<int*>(smem + lay.genpos);
+  int* cons = reinterpret_cast<int*>(smem + lay.cons);
+  int* progress = reinterpret_cast<int*>(smem + lay.progress);
+  int* done = reinterpret_cast<int*>(smem + lay.done);
+  const unsigned abort_s = saddr(smem + lay.abort);
   const long long total = static_cast<long long>(a.sweeps) * n;
   const int nbatches = static_cast<int>((total + kBatch - 1) / kBatch);
+  const uint64_t seed = active ? a.seeds[replica] : 0ull;
 
   // ---------------- init (anneal.cpp:148-155): lane = replica, stream 0
   int G = 0;  // meaningful in warp 0 (the decider) only
   if (warp == 0) {
-    const uint64_t seed = active ? a.seeds[replica] : 0ull;
     Xoshiro r0 = Xoshiro::stream(seed, 0);
     for (int i = 0; i < n; i++) {
       const bool up = (r0.next() >> 63) != 0;
       G += up ? 1 : -1;
       const unsigned w = __ballot_sync(0xffffffffu, up);
-      if (lane == 0) sm.words[i] = w;
+      if (lane == 0) words[i] = w;
     }
     if (lane == 0) {
-      for (int i = n; i < a.n_words; i++) sm.words[i] = 0u;  // padding entries read 0
-      *sm.progress = 0;
+      for (int i = n; i < a.n_words; i++) words[i] = 0u;  // index n reads 0
+      *progress = 0;
+      *done = 0;
+      *reinterpret_cast<int*>(smem + lay.abort) = 0;
     }
-    if (lane < kQB) sm.ready[lane] = -1;
+    if (lane < kQB) ready[lane] = -1;
+    genpos[lane] = 0;
+    cons[lane] = 0;
   }
   __syncthreads();
 
   // exact initial cut, all warps (evaluate.cpp:10-18), per lane = replica
   long long cut = 0;
-  for (int u = warp; u < n; u += NW) {
-    const unsigned su = (sm.words[u] >> lane) & 1u;
+  for (int u = warp; u < n; u += kNW) {
+    const unsigned su = (words[u] >> lane) & 1u;
     const int e1 = __ldg(a.g.off + u + 1);
     for (int e = __ldg(a.g.off + u); e < e1; e++) {
       const int v = __ldg(a.g.col + e);
-      if (v > u && ((sm.words[v] >> lane) & 1u) != su) cut += SIGNED ? __ldg(a.g.w + e) : 1;
+      if (v > u && ((words[v] >> lane) & 1u) != su) cut += SIGNED ? __ldg(a.g.w + e) : 1;
     }
   }
-  sm.part[warp * 32 + lane] = cut;
+  part[warp * 32 + lane] = cut;
   __syncthreads();
 
   if (warp == 0) {
     // ============================ decider ============================
-    for (int w = 1; w < NW; w++) cut += sm.part[w * 32 + lane];
+    for (int w = 1; w < kNW; w++) cut += part[w * 32 + lane];
     const size_t rs = static_cast<size_t>(replica);
     const int sweeps = a.sweeps;
     if (active && a.stamps != nullptr) a.stamps[rs * (sweeps + 1)] = globaltimer_ns();
     if (active && a.snaps != nullptr)
-      for (int i = 0; i < n; i++) a.snaps[rs * (sweeps + 1) * n + i] = ((sm.words[i] >> lane) & 1u) ? 1 : -1;
-    // history: bit k-1 = spin of vertex (0 - k) mod n, k = 1..L
-    uint32_t hist = 0;
-    for (int k = kWin; k >= 1; k--) hist = (hist << 1) | ((sm.words[n - k] >> lane) & 1u);
+      for (int i = 0; i < n; i++) a.snaps[rs * (sweeps + 1) * n + i] = ((words[i] >> lane) & 1u) ? 1 : -1;
+    uint32_t hist0 = 0;  // bit k-1 = spin of vertex (0 - k) mod n
+    for (int k = kWin; k >= 1; k--) hist0 = (hist0 << 1) | ((words[n - k] >> lane) & 1u);
 
-    const uint64_t seed = active ? a.seeds[replica] : 0ull;
-    Xoshiro rng = Xoshiro::stream(seed, 1);
     const int a4 = a.a4, bb = a.b;
-    int AG = a4 * G;
-    int sweep = 0, i = 0;
-    unsigned long long tm = a.tmask[0];
-    bool en = a.thr[0] >= 0;
+    DState st;  // "previous visit" = vertex n-1's initial spin, no change applied
+    st.H = hist0 >> 1;
+    st.fin = (hist0 & 1u) ? 1 : -1;
+    st.own = st.fin;
+    st.AG = a4 * G;
+    st.dcut = 0;
+    st.pos = 0;
+    Sweep sw{cut, 0, 0, a.tmask[0], a.thr[0] >= 0};
+    const unsigned ready_s = saddr(ready), progress_s = saddr(progress);
+    const unsigned genpos_s = saddr(genpos + lane), cons_s = saddr(cons + lane);
+    int ready_next = -2;
+    long long p_t0 = PROF ? clock64() : 0, p_ready = 0, p_gen = 0, p_replay = 0;
 
+#pragma unroll 1
     for (int b = 0; b < nbatches; b++) {
       const int slot = b % kQB;
-      while (ld_acquire(sm.ready + slot) != b) {
-      }
-      const int2* qs = sm.q + slot * kBatch * 32;
-      const uint2* ms = sm.qm + slot * kBatch;
-      const int nv = static_cast<int>(min(static_cast<long long>(kBatch), total - static_cast<long long>(b) * kBatch));
-#pragma unroll
-      for (int t = 0; t < kBatch; t++) {
-        if (t < nv) {
-          const int2 fo = qs[t * 32 + lane];
-          const uint2 mw = ms[t];
-          int f = fo.x + 2 * __popc(hist & mw.x);
-          if (SIGNED) f -= 2 * __popc(hist & mw.y);
-          const int own = fo.y;
-          const int diff = AG - a4 * own - bb * f;
-          uint64_t x = rng.next();
-          int c;
-          if (diff == 0) {  // exact tie: coin, then the unit draw (anneal.cpp:106-121)
-            c = (static_cast<long long>(x) < 0) ? 1 : -1;
-            x = rng.next();
-          } else {
-            c = diff < 0 ? 1 : -1;
+      bool aborted = false;
+      const long long p_a = PROF ? clock64() : 0;
+      if (ready_next != b)
+        for (long long k = 0; ld_acquire(ready_s + 4 * slot) != b; k++)
+          if (k > kWatchdog || ld_acquire(abort_s)) {
+            watchdog(a, abort_s, 1, b, ld_acquire(ready_s + 4 * slot));
+            aborted = true;
+            break;
           }
-          const int fin = (en && x <= tm) ? -c : c;
-          const int d = fin - own;
-          AG += a4 * d;
-          G += d;
-          cut -= static_cast<long long>(d >> 1) * f;
-          hist = (hist << 1) | static_cast<uint32_t>(fin > 0);
-          const unsigned w = __ballot_sync(0xffffffffu, fin > 0);
-          if (lane == 0) sm.words[i] = w;
-          if (++i == n) {  // record_barrier (anneal.cpp:165-187)
-            if (active) {
-              if (a.trace != nullptr) a.trace[rs * sweeps + sweep] = DevTrace{cut, G, G};
-              if (a.stamps != nullptr) a.stamps[rs * (sweeps + 1) + sweep + 1] = globaltimer_ns();
+      const long long p_b = PROF ? clock64() : 0;
+      // draws: pos .. pos+2B-1 must be available (the replay may use all)
+      for (long long k = 0; !__all_sync(0xffffffffu, ld_acquire(genpos_s) >= st.pos + 2 * kBatch); k++)
+        if (k > kWatchdog || ld_acquire(abort_s)) {
+          watchdog(a, abort_s, 2, b, st.pos);
+          aborted = true;
+          break;
+        }
+      if (PROF) {
+        const long long p_c = clock64();
+        p_ready += p_b - p_a;
+        p_gen += p_c - p_b;
+      }
+      if (aborted) break;
+      ready_next = ld_acquire(ready_s + 4 * ((b + 1) % kQB));
+      const int2* qs = q + slot * kBatch * 32 + lane;
+      const uint2* ms = qm + slot * kBatch;
+      const long long left = total - static_cast<long long>(b) * kBatch;
+      bool replay = true;  // boundary/tail batches always take the exact path
+      if (left >= kBatch && sw.i + kBatch <= n) {
+        uint32_t H = st.H;
+        int fin = st.fin, own = st.own, AG = st.AG, dcut = st.dcut;
+        int pos = st.pos;
+        bool dbl = false;
+#pragma unroll 1
+        for (int h = 0; h < kBatch; h += kChunk) {
+          int2 fo[kChunk];
+          uint2 mw[kChunk];
+          bool fl[kChunk + 1], cn[kChunk];
+#pragma unroll
+          for (int t = 0; t < kChunk; t++) {
+            fo[t] = qs[(h + t) * 32];
+            mw[t] = ms[h + t];
+          }
+#pragma unroll
+          for (int k = 0; k <= kChunk; k++) {  // unit draws, flip / coin predicates
+            const uint64_t d = ring_at(ring, pos + k, lane);
+            fl[k] = sw.en && d <= sw.tm;
+            if (k < kChunk) cn[k] = static_cast<long long>(d) < 0;
+          }
+          bool s = false;  // this lane already consumed one coin in this chunk
+#pragma unroll
+          for (int t = 0; t < kChunk; t++) {
+            int S = __popc((H << 1) & mw[t].x);
+            int e = static_cast<int>(mw[t].x & 1u);
+            if (SIGNED) {
+              S -= __popc((H << 1) & mw[t].y);
+              e -= static_cast<int>(mw[t].y & 1u);
             }
-            if (a.snaps != nullptr) {
-              __syncwarp();
-              if (active) {
-                int8_t* dst = a.snaps + (rs * (sweeps + 1) + sweep + 1) * n;
-                for (int v = 0; v < n; v++) dst[v] = ((sm.words[v] >> lane) & 1u) ? 1 : -1;
-              }
+            const int ownt = fo[t].y;
+            int W, V;
+            if (UNITAB) {
+              W = AG - ownt - (fo[t].x + 2 * S) - own - e;
+              V = 1 - e;
+            } else {
+              W = AG - a4 * ownt - bb * (fo[t].x + 2 * S) - a4 * own - bb * e;
+              V = a4 - bb * e;
             }
-            i = 0;
-            if (++sweep < sweeps) {
-              tm = a.tmask[sweep];
-              en = a.thr[sweep] >= 0;
-            }
+            const bool flip = s ? fl[t + 1] : fl[t];
+            const bool up_tie = cn[t] != fl[t + 1];  // coin draw t, unit draw t+1
+            // serial chain: diff_t = W + fin_{t-1} V
+            const int diff = W + fin * V;
+            const bool tie = diff == 0;
+            const bool up = tie ? up_tie : ((diff < 0) != flip);
+            dbl |= tie && s;
+            s |= tie;
+            const int fnew = up ? 1 : -1;
+            const int bprev = fin > 0 ? 1 : 0;
+            const int f = fo[t].x + 2 * S + 2 * e * bprev;
+            AG += UNITAB ? (fin - own) : a4 * (fin - own);
+            H = (H << 1) | static_cast<uint32_t>(bprev);
+            dcut -= ((fnew - ownt) >> 1) * f;
+            fin = fnew;
+            own = ownt;
+            const unsigned w = __ballot_sync(0xffffffffu, up);
+            if (lane == 0) words[sw.i + h + t] = w;
+          }
+          pos += kChunk + (s ? 1 : 0);
+        }
+        replay = __any_sync(0xffffffffu, dbl && active);
+        if (!replay) {
+          st.H = H;
+          st.fin = fin;
+          st.own = own;
+          st.AG = AG;
+          st.dcut = dcut;
+          st.pos = pos;
+          sw.i += kBatch;
+          if (sw.i == n) {  // batch ended exactly on the barrier
+            sw.i = 0;
+            record_barrier(a, words, sw, st.dcut, (st.AG + a4 * (st.fin - st.own)) / a4, lane, active, rs);
+            st.dcut = 0;
           }
         }
       }
+      if (replay) {  // rare: exact replay of the batch from the saved state
+        if (PROF) p_replay++;
+        ReplayIO io{st, sw};
+        replay_batch<SIGNED>(a, words, ring, qs, ms, io, left < kBatch ? static_cast<int>(left) : kBatch, lane,
+                             active, rs);
+        st = io.st;
+        sw = io.sw;
+      }
       __syncwarp();
-      if (lane == 0) st_release(sm.progress, (b + 1) * kBatch);
+      st_release(cons_s, st.pos);  // draws before pos are no longer needed
+      if (lane == 0) st_release(progress_s, (b + 1) * kBatch);
     }
-    if (active) a.final_out[rs] = DevTrace{cut, G, G};
+    if (lane == 0) st_release(saddr(done), 1);
+    if (PROF && lane == 0 && a.prof != nullptr) {
+      atomicAdd(a.prof + 0, static_cast<unsigned long long>(clock64() - p_t0));
+      atomicAdd(a.prof + 1, static_cast<unsigned long long>(p_ready));
+      atomicAdd(a.prof + 2, static_cast<unsigned long long>(p_gen));
+      atomicAdd(a.prof + 3, static_cast<unsigned long long>(p_replay));
+      atomicAdd(a.prof + 4, static_cast<unsigned long long>(nbatches));
+    }
+    const int Gf = (st.AG + a4 * (st.fin - st.own)) / a4;
+    if (active) a.final_out[rs] = DevTrace{sw.cut + st.dcut, Gf, Gf};
+  } else if (warp == kProducer) {
+    // ============================ producer ============================
+    // Each lane runs its own replica's stream as far as its own consumer
+    // allows: lanes drift apart by their individual tie counts.
+    Xoshiro rng = Xoshiro::stream(seed, 1);  // anneal.cpp:191
+    const unsigned genpos_s = saddr(genpos + lane), cons_s = saddr(cons + lane), done_s = saddr(done);
+    int gen = 0;
+    long long p_t0 = PROF ? clock64() : 0, p_wait = 0;
+#pragma unroll 1
+    for (long long spins = 0;; spins++) {
+      const int c = ld_acquire(cons_s);
+      const bool can = gen + 8 <= c + kRing;
+      if (can) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) ring[((gen + k) & (kRing - 1)) * 32 + lane] = rng.next();
+        gen += 8;
+        st_release(genpos_s, gen);
+      }
+      if (!__any_sync(0xffffffffu, can)) {
+        if (ld_acquire(done_s) || ld_acquire(abort_s)) break;
+        const long long p_a = PROF ? clock64() : 0;
+        __nanosleep(64);
+        if (PROF) p_wait += clock64() - p_a;
+        if (spins > kWatchdog) {
+          watchdog(a, abort_s, 3, gen, c);
+          break;
+        }
+      }
+    }
+    if (PROF && lane == 0 && a.prof != nullptr) {
+      atomicAdd(a.prof + 5, static_cast<unsigned long long>(clock64() - p_t0));
+      atomicAdd(a.prof + 6, static_cast<unsigned long long>(p_wait));
+    }
   } else {
     // ============================ gatherers ============================
-    const int g = warp - 1;
-    const int4* __restrict__ fcol = a.far_col;
+    // lane = far neighbour of the row; per replica r: popc of a ballot.
+    const int g = warp < kProducer ? warp - 1 : warp - 2;
+    const int* __restrict__ fcol = a.far_col;
     const int4* __restrict__ meta = a.far_meta;
-    for (int b = g; b < nbatches; b += NG) {
+    const unsigned progress_s = saddr(progress), ready_s = saddr(ready);
+    int i0 = static_cast<int>((static_cast<long long>(g) * kBatch) % n);
+    const int stride = static_cast<int>((static_cast<long long>(kNG) * kBatch) % n);
+    long long p_t0 = PROF ? clock64() : 0, p_wait = 0;
+#pragma unroll 1
+    for (int b = g; b < nbatches; b += kNG) {
       const long long U0 = static_cast<long long>(b) * kBatch;
-      const int need = static_cast<int>(U0) + kBatch - 1 - kWin;
-      if (need > 0)
-        while (ld_acquire(sm.progress) < need) __nanosleep(32);
-      const int slot = b % kQB;
-      int i = static_cast<int>(U0 % n);
       const int nv = static_cast<int>(min(static_cast<long long>(kBatch), total - U0));
-      for (int t = 0; t < nv; t++) {
-        const int4 md = __ldg(meta + i);  // {off4, pos4, neg4, fconst}
-        int cp = 0, cn = 0;
-        const int e_pos = md.x + md.y;
-        for (int e = md.x; e < e_pos; e++) {
-          const int4 c = __ldg(fcol + e);
-          cp += ((sm.words[c.x] >> lane) & 1u) + ((sm.words[c.y] >> lane) & 1u) +
-                ((sm.words[c.z] >> lane) & 1u) + ((sm.words[c.w] >> lane) & 1u);
+      const int slot = b % kQB;
+      // spin-independent prefetch: lane t < B holds row t's metadata, every
+      // lane the first far entry of row 0
+      int vt = i0 + (lane & (kBatch - 1));
+      vt = vt >= n ? vt - n : vt;
+      const int4 mine = __ldg(meta + vt);
+      int4 m = make_int4(__shfl_sync(0xffffffffu, mine.x, 0), __shfl_sync(0xffffffffu, mine.y, 0),
+                         __shfl_sync(0xffffffffu, mine.z, 0), __shfl_sync(0xffffffffu, mine.w, 0));
+      int jn = lane < m.y + m.z ? __ldg(fcol + m.x + lane) : n;
+      const int need = static_cast<int>(U0) + kBatch - 1 - kWin;
+      const long long p_a = PROF ? clock64() : 0;
+      bool aborted = false;
+      if (need > 0)
+        for (long long k = 0; ld_acquire(progress_s) < need; k++) {
+          if (k > kWatchdog || ld_acquire(abort_s)) {
+            watchdog(a, abort_s, 4, b, need);
+            aborted = true;
+            break;
+          }
+          __nanosleep(20);
         }
-        if (SIGNED) {
-          const int e_neg = e_pos + md.z;
-          for (int e = e_pos; e < e_neg; e++) {
-            const int4 c = __ldg(fcol + e);
-            cn += ((sm.words[c.x] >> lane) & 1u) + ((sm.words[c.y] >> lane) & 1u) +
-                  ((sm.words[c.z] >> lane) & 1u) + ((sm.words[c.w] >> lane) & 1u);
+      if (PROF) p_wait += clock64() - p_a;
+      if (aborted) break;
+#pragma unroll 1
+      for (int t = 0; t < nv; t++) {
+        const int deg = m.y + m.z;
+        int cnt = 0;  // lane r < rc: count for replica r
+        for (int e0 = 0; e0 < deg; e0 += 32) {
+          const int j = e0 == 0 ? jn : (e0 + lane < deg ? __ldg(fcol + m.x + e0 + lane) : n);
+          const uint32_t wj = words[j];
+          const bool neg = SIGNED && (e0 + lane >= m.y) && (e0 + lane < deg);
+          const unsigned nmask = SIGNED ? __ballot_sync(0xffffffffu, neg) : 0u;
+#pragma unroll 1
+          for (int r = 0; r < rc; r++) {
+            const unsigned bm = __ballot_sync(0xffffffffu, (wj >> r) & 1u);
+            int v = __popc(bm);
+            if (SIGNED) v -= 2 * __popc(bm & nmask);
+            cnt += lane == r ? v : 0;
           }
         }
-        const int own = ((sm.words[i] >> lane) & 1u) ? 1 : -1;
-        sm.q[(slot * kBatch + t) * 32 + lane] = make_int2(2 * (cp - cn) - md.w, own);
-        if (lane == 0) sm.qm[slot * kBatch + t] = make_uint2(__ldg(a.win_pos + i), SIGNED ? __ldg(a.win_neg + i) : 0u);
-        if (++i == n) i = 0;
+        int v = i0 + t;
+        v = v >= n ? v - n : v;
+        const int own = ((words[v] >> lane) & 1u) ? 1 : -1;
+        q[(slot * kBatch + t) * 32 + lane] = make_int2(2 * cnt - m.w, own);
+        if (lane == 0) qm[slot * kBatch + t] = make_uint2(__ldg(a.win_pos + v), SIGNED ? __ldg(a.win_neg + v) : 0u);
+        if (t + 1 < nv) {  // next row: metadata from lane t+1, first entries
+          m = make_int4(__shfl_sync(0xffffffffu, mine.x, t + 1), __shfl_sync(0xffffffffu, mine.y, t + 1),
+                        __shfl_sync(0xffffffffu, mine.z, t + 1), __shfl_sync(0xffffffffu, mine.w, t + 1));
+          jn = lane < m.y + m.z ? __ldg(fcol + m.x + lane) : n;
+        }
       }
       __syncwarp();
-      if (lane == 0) st_release(sm.ready + slot, b);
+      if (lane == 0) st_release(ready_s + 4 * slot, b);
+      if (ld_acquire(abort_s)) break;
+      i0 += stride;
+      i0 = i0 >= n ? i0 - n : i0;
+    }
+    if (PROF && lane == 0 && a.prof != nullptr) {
+      atomicAdd(a.prof + 7, static_cast<unsigned long long>(clock64() - p_t0));
+      atomicAdd(a.prof + 8, static_cast<unsigned long long>(p_wait));
     }
   }
 
   __syncthreads();
   // final spins, all warps: spins_out[r][v] (lane = replica)
   if (active)
-    for (int v = warp; v < n; v += NW)
-      a.spins_out[static_cast<size_t>(replica) * n + v] = ((sm.words[v] >> lane) & 1u) ? 1 : -1;
+    for (int v = warp; v < n; v += kNW)
+      a.spins_out[static_cast<size_t>(replica) * n + v] = ((words[v] >> lane) & 1u) ? 1 : -1;
 }
 
-template <bool S, int NG>
-const void* pipe_fn() {
-  return reinterpret_cast<const void*>(&k1_pipe<S, NG>);
+template <bool S, bool U>
+const void* pipe_fn(bool prof) {
+  return prof ? reinterpret_cast<const void*>(&k1_pipe<S, U, true>)
+              : reinterpret_cast<const void*>(&k1_pipe<S, U, false>);
+}
+
+long long gcd64(long long x, long long y) {
+  x = x < 0 ? -x : x;
+  y = y < 0 ? -y : y;
+  while (y) {
+    const long long t = x % y;
+    x = y;
+    y = t;
+  }
+  return x;
 }
 
 }  // namespace
 
-size_t pipe_smem_bytes(int n_words, int nwarps) {
-  return static_cast<size_t>(n_words) * 4 + sizeof(int2) * kQB * kBatch * 32 + sizeof(uint2) * kQB * kBatch +
-         sizeof(long long) * nwarps * 32 + sizeof(int) * (kQB + 1);
-}
+size_t pipe_smem_bytes(int n_words, int) { return Layout::make(n_words).total; }
 
 int pipe_window() { return kWin; }
 
@@ -264,25 +566,34 @@ int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64
               int32_t sweeps, PipePlan* plan) {
   if (!pg.ok) return -1;
   if (static_cast<long long>(sweeps) * st.n >= (1LL << 31) - 64) return -1;
-  const long long absa4 = a4 < 0 ? -a4 : a4, absb = b < 0 ? -b : b;
-  // narrow arithmetic must be exact: |AG - a4*own - b*f| < 2^31 always
-  const double bound = static_cast<double>(absa4) * (st.n + 1) + static_cast<double>(absb) * st.max_abs_field;
+  if (2 * st.m >= (1LL << 31)) return -1;
+  // diff = 4A (G - own) - B f: dividing both coefficients by their gcd keeps
+  // the sign and the exact ties
+  const long long g = gcd64(a4, b);
+  const long long ra = a4 / g, rb = b / g;
+  const double bound = static_cast<double>(ra) * (st.n + 3) + static_cast<double>(rb) * (st.max_abs_field + 2);
   if (bound >= 2147483647.0) return -1;
-  constexpr int NG = 7;
-  const int nw = NG + 1;
-  const int n_words = pg.n_words;
-  const size_t smem = pipe_smem_bytes(n_words, nw);
+  const size_t smem = pipe_smem_bytes(pg.n_words, kNW);
   if (smem > 200 * 1024) return -1;
   // replicas per CTA: spread R over the SMs (the per-replica chain is the
   // bound, so fewer lanes per CTA only adds parallel CTAs)
   int rc = (replicas + 147) / 148;
   rc = rc < 1 ? 1 : rc > 32 ? 32 : rc;
-  plan->fn = st.unit ? pipe_fn<false, NG>() : pipe_fn<true, NG>();
+  const bool unitab = ra == 1 && rb == 1;
+  const bool prof = std::getenv("GDI_PIPE_PROFILE") != nullptr;
+  if (st.unit)
+    plan->fn = unitab ? pipe_fn<false, true>(prof) : pipe_fn<false, false>(prof);
+  else
+    plan->fn = unitab ? pipe_fn<true, true>(prof) : pipe_fn<true, false>(prof);
+  plan->prof = prof;
   plan->rc = rc;
-  plan->block = 32 * nw;
+  plan->block = 32 * kNW;
   plan->grid = (replicas + rc - 1) / rc;
   plan->smem = static_cast<int>(smem);
-  plan->name = st.unit ? "k1_pipe<unit>" : "k1_pipe<signed>";
+  plan->a4 = static_cast<int32_t>(ra);
+  plan->b = static_cast<int32_t>(rb);
+  plan->name = st.unit ? (unitab ? "k1_pipe<unit,ab=1>" : "k1_pipe<unit>")
+                       : (unitab ? "k1_pipe<signed,ab=1>" : "k1_pipe<signed>");
   return 0;
 }
 
@@ -291,6 +602,8 @@ cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t
   if (err != cudaSuccess) return err;
   PipeArgs a = args;
   a.rc = plan.rc;
+  a.a4 = plan.a4;
+  a.b = plan.b;
   void* params[] = {&a};
   return cudaLaunchKernel(plan.fn, dim3(plan.grid), dim3(plan.block), params, plan.smem, stream);
 }

@@ -41,14 +41,14 @@ struct ExactArgs {
   DevTrace* final_out;    // [R]
 };
 
-// k1_pipe (warp-specialised exact kernel). Far CSR: per vertex i,
-// far_meta[i] = {first int4 index, #int4 of +1 neighbours, #int4 of -1
-// neighbours, fconst}; entries padded with index n (a word that reads 0).
+// k1_pipe (warp-specialised exact kernel). Far lists: for vertex i,
+// far_meta[i] = {offset into far_col, #(+1 neighbours), #(-1 neighbours),
+// fconst}; far_col holds the +1 far neighbours then the -1 far neighbours.
 // win_pos/win_neg[i]: bit k-1 set when vertex (i-k) mod n is a +1 / -1
 // neighbour, k = 1..32.
 struct PipeArgs {
   DevCsr g;                        // full CSR (initial cut only)
-  const int4* far_col;
+  const int32_t* far_col;
   const int4* far_meta;
   const uint32_t* win_pos;
   const uint32_t* win_neg;
@@ -66,6 +66,8 @@ struct PipeArgs {
   unsigned long long* stamps;
   int8_t* snaps;
   DevTrace* final_out;
+  int* watchdog;                   // [8] zeroed; non-zero [0] = pipeline stalled
+  unsigned long long* prof;        // [16] profiling counters (PROF builds)
 };
 
 struct EvalArgs {

@@ -36,7 +36,7 @@ cudaError_t exact_launch(const ExactPlan& plan, const ExactArgs& args, cudaStrea
 struct PipeGraph {
   bool ok = false;
   int32_t n_words = 0;
-  int4* far_col = nullptr;   // device
+  int32_t* far_col = nullptr;  // device
   int4* far_meta = nullptr;  // device
   uint32_t* win_pos = nullptr;
   uint32_t* win_neg = nullptr;
@@ -44,10 +44,12 @@ struct PipeGraph {
 
 struct PipePlan {
   const void* fn = nullptr;
+  int32_t a4 = 4, b = 4;  // coefficients reduced by gcd(4A, B)
   int rc = 8;
   int block = 256;
   int grid = 1;
   int smem = 0;
+  bool prof = false;
   const char* name = "";
 };
 

@@ -18,6 +18,7 @@ def run(name, R, sweeps, reps=3):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(st); s.launch(); e1.record(st); torch.cuda.synchronize()
         if i: ts.append(e0.elapsed_time(e1))
+    s.sync()
     ms = min(ts)
     ups = R * g.num_nodes * sweeps / (ms * 1e-3)
     print(json.dumps({"config": name, "R": R, "sweeps": sweeps, "ms": ms, "updates_per_s": ups,
