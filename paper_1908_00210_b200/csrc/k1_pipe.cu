@@ -64,8 +64,13 @@ constexpr int kBatch = 8;     // visits per queue batch (B)
 constexpr int kChunk = 4;     // decider visits unrolled per inner iteration
 constexpr int kQB = 8;        // queue depth in batches (QB*B > L + B)
 constexpr int kNW = 8;        // warps per CTA
-constexpr int kProducer = 4;  // warp id of the producer (shares SMSP 0 with the decider)
-constexpr int kNG = kNW - 2;  // gatherer warps
+// Warp w runs on SM sub-partition w % 4. The decider is bound by its own
+// SMSP's ALU/FMA issue rate (measured: a busy co-resident warp slows it by
+// half), so warp 4 - its SMSP partner - only helps with the prologue and
+// then retires; the producer and the gatherers share SMSPs 1-3.
+constexpr int kIdle = 4;      // SMSP 0 partner of the decider: retires after init
+constexpr int kProducer = 1;  // RNG producer
+constexpr int kNG = kNW - 3;  // gatherer warps (2, 3, 5, 6, 7)
 constexpr int kRing = 64;     // draws buffered per lane (power of two, >= 4B)
 constexpr long long kWatchdog = 1LL << 26;
 
@@ -79,6 +84,10 @@ __device__ __forceinline__ int ld_acquire(unsigned a) {
 }
 __device__ __forceinline__ void st_release(unsigned a, int v) {
   asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// Relaxed store; callers order it after a preceding __threadfence_block().
+__device__ __forceinline__ void st_relaxed(unsigned a, int v) {
+  asm volatile("st.relaxed.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 // Shared-memory layout (byte offsets from the dynamic smem base).
@@ -280,25 +289,27 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
     for (int k = kWin; k >= 1; k--) hist0 = (hist0 << 1) | ((words[n - k] >> lane) & 1u);
 
     const int a4 = a.a4, bb = a.b;
-    DState st;  // "previous visit" = vertex n-1's initial spin, no change applied
-    st.H = hist0 >> 1;
-    st.fin = (hist0 & 1u) ? 1 : -1;
-    st.own = st.fin;
-    st.AG = a4 * G;
-    st.dcut = 0;
-    st.pos = 0;
-    Sweep sw{cut, 0, 0, a.tmask[0], a.thr[0] >= 0};
+    // Decider state, all in registers (only the rare replay path copies it
+    // into a local struct): see DState / Sweep for the meaning.
+    uint32_t H = hist0 >> 1;  // "previous visit" = vertex n-1's initial spin, no change applied
+    int fin = (hist0 & 1u) ? 1 : -1, own = fin, AG = a4 * G, dcut = 0, pos = 0;
+    long long cutv = cut;
+    int sweep = 0, vi = 0;
+    unsigned long long tm = a.tmask[0];
+    bool en = a.thr[0] >= 0;
     const unsigned ready_s = saddr(ready), progress_s = saddr(progress);
     const unsigned genpos_s = saddr(genpos + lane), cons_s = saddr(cons + lane);
-    int ready_next = -2;
+    int rdy = ld_acquire(ready_s);  // prefetched ready flag of the current batch
+    int gp = ld_acquire(genpos_s);  // prefetched generated-draw count
     long long p_t0 = PROF ? clock64() : 0, p_ready = 0, p_gen = 0, p_replay = 0;
+    auto gsum = [&](int agv) { return UNITAB ? agv : agv / a4; };
 
 #pragma unroll 1
     for (int b = 0; b < nbatches; b++) {
       const int slot = b % kQB;
       bool aborted = false;
       const long long p_a = PROF ? clock64() : 0;
-      if (ready_next != b)
+      if (rdy != b)
         for (long long k = 0; ld_acquire(ready_s + 4 * slot) != b; k++)
           if (k > kWatchdog || ld_acquire(abort_s)) {
             watchdog(a, abort_s, 1, b, ld_acquire(ready_s + 4 * slot));
@@ -306,28 +317,30 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
             break;
           }
       const long long p_b = PROF ? clock64() : 0;
-      // draws: pos .. pos+2B-1 must be available (the replay may use all)
-      for (long long k = 0; !__all_sync(0xffffffffu, ld_acquire(genpos_s) >= st.pos + 2 * kBatch); k++)
-        if (k > kWatchdog || ld_acquire(abort_s)) {
-          watchdog(a, abort_s, 2, b, st.pos);
-          aborted = true;
-          break;
-        }
+      // draws pos .. pos+2B-1 must be available (the replay may use all)
+      if (!__all_sync(0xffffffffu, gp >= pos + 2 * kBatch))
+        for (long long k = 0; !__all_sync(0xffffffffu, (gp = ld_acquire(genpos_s)) >= pos + 2 * kBatch); k++)
+          if (k > kWatchdog || ld_acquire(abort_s)) {
+            watchdog(a, abort_s, 2, b, pos);
+            aborted = true;
+            break;
+          }
       if (PROF) {
         const long long p_c = clock64();
         p_ready += p_b - p_a;
         p_gen += p_c - p_b;
       }
       if (aborted) break;
-      ready_next = ld_acquire(ready_s + 4 * ((b + 1) % kQB));
+      // prefetch next batch's flags now; their latency hides under the chunks
+      rdy = ld_acquire(ready_s + 4 * ((b + 1) % kQB));
+      gp = ld_acquire(genpos_s);
       const int2* qs = q + slot * kBatch * 32 + lane;
       const uint2* ms = qm + slot * kBatch;
       const long long left = total - static_cast<long long>(b) * kBatch;
       bool replay = true;  // boundary/tail batches always take the exact path
-      if (left >= kBatch && sw.i + kBatch <= n) {
-        uint32_t H = st.H;
-        int fin = st.fin, own = st.own, AG = st.AG, dcut = st.dcut;
-        int pos = st.pos;
+      if (left >= kBatch && vi + kBatch <= n) {
+        uint32_t H1 = H;
+        int fin1 = fin, own1 = own, AG1 = AG, dcut1 = dcut, pos1 = pos;
         bool dbl = false;
 #pragma unroll 1
         for (int h = 0; h < kBatch; h += kChunk) {
@@ -341,76 +354,93 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
           }
 #pragma unroll
           for (int k = 0; k <= kChunk; k++) {  // unit draws, flip / coin predicates
-            const uint64_t d = ring_at(ring, pos + k, lane);
-            fl[k] = sw.en && d <= sw.tm;
+            const uint64_t d = ring_at(ring, pos1 + k, lane);
+            fl[k] = en && d <= tm;
             if (k < kChunk) cn[k] = static_cast<long long>(d) < 0;
           }
           bool s = false;  // this lane already consumed one coin in this chunk
 #pragma unroll
           for (int t = 0; t < kChunk; t++) {
-            int S = __popc((H << 1) & mw[t].x);
+            int S = __popc((H1 << 1) & mw[t].x);
             int e = static_cast<int>(mw[t].x & 1u);
             if (SIGNED) {
-              S -= __popc((H << 1) & mw[t].y);
+              S -= __popc((H1 << 1) & mw[t].y);
               e -= static_cast<int>(mw[t].y & 1u);
             }
             const int ownt = fo[t].y;
             int W, V;
             if (UNITAB) {
-              W = AG - ownt - (fo[t].x + 2 * S) - own - e;
+              W = AG1 - ownt - (fo[t].x + 2 * S) - own1 - e;
               V = 1 - e;
             } else {
-              W = AG - a4 * ownt - bb * (fo[t].x + 2 * S) - a4 * own - bb * e;
+              W = AG1 - a4 * ownt - bb * (fo[t].x + 2 * S) - a4 * own1 - bb * e;
               V = a4 - bb * e;
             }
             const bool flip = s ? fl[t + 1] : fl[t];
             const bool up_tie = cn[t] != fl[t + 1];  // coin draw t, unit draw t+1
             // serial chain: diff_t = W + fin_{t-1} V
-            const int diff = W + fin * V;
+            const int diff = W + fin1 * V;
             const bool tie = diff == 0;
             const bool up = tie ? up_tie : ((diff < 0) != flip);
             dbl |= tie && s;
             s |= tie;
             const int fnew = up ? 1 : -1;
-            const int bprev = fin > 0 ? 1 : 0;
+            const int bprev = fin1 > 0 ? 1 : 0;
             const int f = fo[t].x + 2 * S + 2 * e * bprev;
-            AG += UNITAB ? (fin - own) : a4 * (fin - own);
-            H = (H << 1) | static_cast<uint32_t>(bprev);
-            dcut -= ((fnew - ownt) >> 1) * f;
-            fin = fnew;
-            own = ownt;
+            AG1 += UNITAB ? (fin1 - own1) : a4 * (fin1 - own1);
+            H1 = (H1 << 1) | static_cast<uint32_t>(bprev);
+            dcut1 -= ((fnew - ownt) >> 1) * f;
+            fin1 = fnew;
+            own1 = ownt;
             const unsigned w = __ballot_sync(0xffffffffu, up);
-            if (lane == 0) words[sw.i + h + t] = w;
+            if (lane == 0) words[vi + h + t] = w;
           }
-          pos += kChunk + (s ? 1 : 0);
+          pos1 += kChunk + (s ? 1 : 0);
         }
         replay = __any_sync(0xffffffffu, dbl && active);
         if (!replay) {
-          st.H = H;
-          st.fin = fin;
-          st.own = own;
-          st.AG = AG;
-          st.dcut = dcut;
-          st.pos = pos;
-          sw.i += kBatch;
-          if (sw.i == n) {  // batch ended exactly on the barrier
-            sw.i = 0;
-            record_barrier(a, words, sw, st.dcut, (st.AG + a4 * (st.fin - st.own)) / a4, lane, active, rs);
-            st.dcut = 0;
+          H = H1;
+          fin = fin1;
+          own = own1;
+          AG = AG1;
+          dcut = dcut1;
+          pos = pos1;
+          vi += kBatch;
+          if (vi == n) {  // batch ended exactly on the barrier
+            vi = 0;
+            Sweep sw{cutv, sweep, vi, tm, en};
+            record_barrier(a, words, sw, dcut, gsum(AG + (UNITAB ? 1 : a4) * (fin - own)), lane, active, rs);
+            cutv = sw.cut;
+            sweep = sw.sweep;
+            tm = sw.tm;
+            en = sw.en;
+            dcut = 0;
           }
         }
       }
       if (replay) {  // rare: exact replay of the batch from the saved state
         if (PROF) p_replay++;
-        ReplayIO io{st, sw};
+        ReplayIO io{DState{H, fin, own, AG, dcut, pos}, Sweep{cutv, sweep, vi, tm, en}};
         replay_batch<SIGNED>(a, words, ring, qs, ms, io, left < kBatch ? static_cast<int>(left) : kBatch, lane,
                              active, rs);
-        st = io.st;
-        sw = io.sw;
+        H = io.st.H;
+        fin = io.st.fin;
+        own = io.st.own;
+        AG = io.st.AG;
+        dcut = io.st.dcut;
+        pos = io.st.pos;
+        cutv = io.sw.cut;
+        sweep = io.sw.sweep;
+        vi = io.sw.i;
+        tm = io.sw.tm;
+        en = io.sw.en;
       }
+      // publish: the batch's spin words are final (gatherers, release) and
+      // draws before pos are no longer needed (producer; the ring loads were
+      // consumed by this batch's decisions, so a relaxed store suffices)
       __syncwarp();
-      st_release(cons_s, st.pos);  // draws before pos are no longer needed
       if (lane == 0) st_release(progress_s, (b + 1) * kBatch);
+      st_relaxed(cons_s, pos);
     }
     if (lane == 0) st_release(saddr(done), 1);
     if (PROF && lane == 0 && a.prof != nullptr) {
@@ -420,8 +450,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
       atomicAdd(a.prof + 3, static_cast<unsigned long long>(p_replay));
       atomicAdd(a.prof + 4, static_cast<unsigned long long>(nbatches));
     }
-    const int Gf = (st.AG + a4 * (st.fin - st.own)) / a4;
-    if (active) a.final_out[rs] = DevTrace{sw.cut + st.dcut, Gf, Gf};
+    const int Gf = gsum(AG + (UNITAB ? 1 : a4) * (fin - own));
+    if (active) a.final_out[rs] = DevTrace{cutv + dcut, Gf, Gf};
+  } else if (warp == kIdle) {
+    // nothing: keep SMSP 0 for the decider
   } else if (warp == kProducer) {
     // ============================ producer ============================
     // Each lane runs its own replica's stream as far as its own consumer
@@ -458,7 +490,8 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
   } else {
     // ============================ gatherers ============================
     // lane = far neighbour of the row; per replica r: popc of a ballot.
-    const int g = warp < kProducer ? warp - 1 : warp - 2;
+    // All index loads of a batch are issued before waiting on progress.
+    const int g = warp < kIdle ? warp - 2 : warp - 3;
     const int* __restrict__ fcol = a.far_col;
     const int4* __restrict__ meta = a.far_meta;
     const unsigned progress_s = saddr(progress), ready_s = saddr(ready);
@@ -470,14 +503,20 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
       const long long U0 = static_cast<long long>(b) * kBatch;
       const int nv = static_cast<int>(min(static_cast<long long>(kBatch), total - U0));
       const int slot = b % kQB;
-      // spin-independent prefetch: lane t < B holds row t's metadata, every
-      // lane the first far entry of row 0
+      // spin-independent prefetch: lane t < B holds row t's metadata and
+      // window masks; jn[t] = far entry `lane` of row t (or n -> zero word)
       int vt = i0 + (lane & (kBatch - 1));
       vt = vt >= n ? vt - n : vt;
       const int4 mine = __ldg(meta + vt);
-      int4 m = make_int4(__shfl_sync(0xffffffffu, mine.x, 0), __shfl_sync(0xffffffffu, mine.y, 0),
-                         __shfl_sync(0xffffffffu, mine.z, 0), __shfl_sync(0xffffffffu, mine.w, 0));
-      int jn = lane < m.y + m.z ? __ldg(fcol + m.x + lane) : n;
+      const uint32_t wpos = __ldg(a.win_pos + vt);
+      const uint32_t wneg = SIGNED ? __ldg(a.win_neg + vt) : 0u;
+      int jn[kBatch];
+#pragma unroll
+      for (int t = 0; t < kBatch; t++) {
+        const int off = __shfl_sync(0xffffffffu, mine.x, t);
+        const int deg = __shfl_sync(0xffffffffu, mine.y + mine.z, t);
+        jn[t] = lane < deg ? __ldg(fcol + off + lane) : n;
+      }
       const int need = static_cast<int>(U0) + kBatch - 1 - kWin;
       const long long p_a = PROF ? clock64() : 0;
       bool aborted = false;
@@ -492,32 +531,46 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
         }
       if (PROF) p_wait += clock64() - p_a;
       if (aborted) break;
+#pragma unroll
+      for (int t = 0; t < kBatch; t++) {
+        if (t < nv && (a.debug & 1)) {  // timing experiment: no field work
+          q[(slot * kBatch + t) * 32 + lane] = make_int2(0, 1);
+          if (lane == 0) qm[slot * kBatch + t] = make_uint2(0u, 0u);
+        } else if (t < nv) {
+          const int4 m = make_int4(__shfl_sync(0xffffffffu, mine.x, t), __shfl_sync(0xffffffffu, mine.y, t),
+                                   __shfl_sync(0xffffffffu, mine.z, t), __shfl_sync(0xffffffffu, mine.w, t));
+          const int deg = m.y + m.z;
+          int cnt = 0;  // lane r < rc: count for replica r
+          for (int e0 = 0; e0 < deg; e0 += 32) {
+            const int j = e0 == 0 ? jn[t] : (e0 + lane < deg ? __ldg(fcol + m.x + e0 + lane) : n);
+            const uint32_t wj = words[j];
+            const bool neg = SIGNED && (e0 + lane >= m.y) && (e0 + lane < deg);
+            const unsigned nmask = SIGNED ? __ballot_sync(0xffffffffu, neg) : 0u;
+            if (rc <= 8) {
+#pragma unroll
+              for (int r = 0; r < 8; r++) {
+                const unsigned bm = __ballot_sync(0xffffffffu, (wj >> r) & 1u);
+                int v = __popc(bm);
+                if (SIGNED) v -= 2 * __popc(bm & nmask);
+                cnt += lane == r ? v : 0;
+              }
+            } else {
 #pragma unroll 1
-      for (int t = 0; t < nv; t++) {
-        const int deg = m.y + m.z;
-        int cnt = 0;  // lane r < rc: count for replica r
-        for (int e0 = 0; e0 < deg; e0 += 32) {
-          const int j = e0 == 0 ? jn : (e0 + lane < deg ? __ldg(fcol + m.x + e0 + lane) : n);
-          const uint32_t wj = words[j];
-          const bool neg = SIGNED && (e0 + lane >= m.y) && (e0 + lane < deg);
-          const unsigned nmask = SIGNED ? __ballot_sync(0xffffffffu, neg) : 0u;
-#pragma unroll 1
-          for (int r = 0; r < rc; r++) {
-            const unsigned bm = __ballot_sync(0xffffffffu, (wj >> r) & 1u);
-            int v = __popc(bm);
-            if (SIGNED) v -= 2 * __popc(bm & nmask);
-            cnt += lane == r ? v : 0;
+              for (int r = 0; r < rc; r++) {
+                const unsigned bm = __ballot_sync(0xffffffffu, (wj >> r) & 1u);
+                int v = __popc(bm);
+                if (SIGNED) v -= 2 * __popc(bm & nmask);
+                cnt += lane == r ? v : 0;
+              }
+            }
           }
-        }
-        int v = i0 + t;
-        v = v >= n ? v - n : v;
-        const int own = ((words[v] >> lane) & 1u) ? 1 : -1;
-        q[(slot * kBatch + t) * 32 + lane] = make_int2(2 * cnt - m.w, own);
-        if (lane == 0) qm[slot * kBatch + t] = make_uint2(__ldg(a.win_pos + v), SIGNED ? __ldg(a.win_neg + v) : 0u);
-        if (t + 1 < nv) {  // next row: metadata from lane t+1, first entries
-          m = make_int4(__shfl_sync(0xffffffffu, mine.x, t + 1), __shfl_sync(0xffffffffu, mine.y, t + 1),
-                        __shfl_sync(0xffffffffu, mine.z, t + 1), __shfl_sync(0xffffffffu, mine.w, t + 1));
-          jn = lane < m.y + m.z ? __ldg(fcol + m.x + lane) : n;
+          int v = i0 + t;
+          v = v >= n ? v - n : v;
+          const int own = ((words[v] >> lane) & 1u) ? 1 : -1;
+          q[(slot * kBatch + t) * 32 + lane] = make_int2(2 * cnt - m.w, own);
+          const uint32_t mp = __shfl_sync(0xffffffffu, wpos, t);
+          const uint32_t mn = __shfl_sync(0xffffffffu, wneg, t);
+          if (lane == 0) qm[slot * kBatch + t] = make_uint2(mp, mn);
         }
       }
       __syncwarp();
@@ -602,6 +655,8 @@ cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t
   if (err != cudaSuccess) return err;
   PipeArgs a = args;
   a.rc = plan.rc;
+  const char* dbg = std::getenv("GDI_PIPE_DEBUG");
+  a.debug = dbg ? std::atoi(dbg) : 0;
   a.a4 = plan.a4;
   a.b = plan.b;
   void* params[] = {&a};

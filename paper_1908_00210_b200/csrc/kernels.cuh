@@ -68,6 +68,7 @@ struct PipeArgs {
   DevTrace* final_out;
   int* watchdog;                   // [8] zeroed; non-zero [0] = pipeline stalled
   unsigned long long* prof;        // [16] profiling counters (PROF builds)
+  int32_t debug;                   // timing experiments only (GDI_PIPE_DEBUG); 0 in production
 };
 
 struct EvalArgs {
