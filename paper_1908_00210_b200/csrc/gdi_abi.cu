@@ -80,6 +80,9 @@ struct gdi_graph {
   GraphStats st;
   DevBuf off, col, w;
   DevBuf far_col, far_meta, win_pos, win_neg;  // k1_pipe preprocessing
+  DevBuf order;                                // k2 degree-binned visit order
+  DevBuf sell, sell_off, sell_w, edges, edge_w;  // k2 SELL-32 rows + edge list
+  int wkind = 0;                               // 0 unit, 1 +-1 (sign bit), 2 general
   PipeGraph pipe;
   int64_t bytes = 0;
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), w.as<int32_t>(), st.n}; }
@@ -93,7 +96,9 @@ struct gdi_session {
   bool own_stream = false;
   ExactPlan plan;
   PipePlan pplan;
+  ThruPlan tplan;
   bool use_pipe = false;
+  bool use_thru = false;
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
@@ -199,6 +204,75 @@ int build_pipe(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const i
   return GDI_OK;
 }
 
+// Throughput-kernel layout: degree-binned order, SELL-32 rows over it and
+// the canonical edge list for the per-sweep exact cut (see k2_throughput.cu).
+int build_thru(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const int32_t* weights) {
+  const int32_t n = g->st.n;
+  bool pm1 = true;
+  for (int64_t e = 0; weights && e < offsets[n]; e++)
+    if (weights[e] != 1 && weights[e] != -1) pm1 = false;
+  g->wkind = !weights || g->st.unit ? 0 : (pm1 ? 1 : 2);
+  std::vector<int32_t> ord(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; i++) ord[i] = i;
+  // descending degree, ties by index: a chunk's 32 rows have nearly equal length
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+    return offsets[x + 1] - offsets[x] > offsets[y + 1] - offsets[y];
+  });
+  const int32_t chunks = (n + 31) / 32;
+  std::vector<int32_t> soff(static_cast<size_t>(chunks) + 1, 0);
+  for (int32_t c = 0; c < chunks; c++) {
+    int64_t kmax = 0;
+    for (int32_t l = 0; l < 32 && 32 * c + l < n; l++) {
+      const int32_t v = ord[32 * c + l];
+      kmax = std::max<int64_t>(kmax, offsets[v + 1] - offsets[v]);
+    }
+    const int64_t next = soff[c] + ((kmax + 3) / 4) * 32;
+    if (next > 0x7fffffffLL) return fail(GDI_ERR_CAPACITY, "SELL layout exceeds 2^31 entries");
+    soff[c + 1] = static_cast<int32_t>(next);
+  }
+  std::vector<int4> sell(std::max<size_t>(1, static_cast<size_t>(soff[chunks])), make_int4(n, n, n, n));
+  std::vector<int4> sellw(g->wkind == 2 ? sell.size() : 0, make_int4(0, 0, 0, 0));
+  for (int32_t c = 0; c < chunks; c++)
+    for (int32_t l = 0; l < 32 && 32 * c + l < n; l++) {
+      const int32_t v = ord[32 * c + l];
+      for (int64_t e = offsets[v]; e < offsets[v + 1]; e++) {
+        const int64_t k = e - offsets[v];
+        const size_t slot = static_cast<size_t>(soff[c]) + static_cast<size_t>(k / 4) * 32 + l;
+        int32_t idx = nbr[e];
+        if (g->wkind == 1 && weights[e] < 0) idx |= static_cast<int32_t>(0x80000000u);
+        (&sell[slot].x)[k % 4] = idx;
+        if (g->wkind == 2) (&sellw[slot].x)[k % 4] = weights[e];
+      }
+    }
+  std::vector<int2> edges;
+  std::vector<int32_t> ew;
+  edges.reserve(static_cast<size_t>(g->st.m));
+  for (int32_t u = 0; u < n; u++)
+    for (int64_t e = offsets[u]; e < offsets[u + 1]; e++)
+      if (nbr[e] > u) {
+        edges.push_back(make_int2(u, nbr[e]));
+        if (g->wkind != 0) ew.push_back(weights[e]);
+      }
+  if (edges.empty()) edges.push_back(make_int2(0, 0));
+  GDI_CUDA(g->order.alloc(ord.size() * sizeof(int32_t)));
+  GDI_CUDA(cudaMemcpy(g->order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  GDI_CUDA(g->sell.alloc(sell.size() * sizeof(int4)));
+  GDI_CUDA(cudaMemcpy(g->sell.p, sell.data(), sell.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  GDI_CUDA(g->sell_off.alloc(soff.size() * sizeof(int32_t)));
+  GDI_CUDA(cudaMemcpy(g->sell_off.p, soff.data(), soff.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (!sellw.empty()) {
+    GDI_CUDA(g->sell_w.alloc(sellw.size() * sizeof(int4)));
+    GDI_CUDA(cudaMemcpy(g->sell_w.p, sellw.data(), sellw.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  }
+  GDI_CUDA(g->edges.alloc(edges.size() * sizeof(int2)));
+  GDI_CUDA(cudaMemcpy(g->edges.p, edges.data(), edges.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  if (!ew.empty()) {
+    GDI_CUDA(g->edge_w.alloc(ew.size() * sizeof(int32_t)));
+    GDI_CUDA(cudaMemcpy(g->edge_w.p, ew.data(), ew.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  return GDI_OK;
+}
+
 // GDI_FORCE_KERNEL=exact|pipe pins the exact-mode variant (tests run both).
 const char* forced_kernel() {
   const char* e = std::getenv("GDI_FORCE_KERNEL");
@@ -277,6 +351,7 @@ int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_
     GDI_CUDA(cudaMemcpy(g->w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   if ((rc = build_pipe(g.get(), offsets, nbr, weights))) return rc;
+  if ((rc = build_thru(g.get(), offsets, nbr, weights))) return rc;
   g->bytes = static_cast<int64_t>(g->off.bytes + g->col.bytes + g->w.bytes + g->far_col.bytes +
                                   g->far_meta.bytes + g->win_pos.bytes + g->win_neg.bytes);
   *out = g.release();
@@ -320,11 +395,17 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   // Both strategies coincide in the exact mode (reference acceptance.cpp
   // criterion 8). Prefer the warp-specialised pipe kernel when it applies.
   const std::string force = forced_kernel();
-  const bool pipe_ok =
-      force != "exact" && pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
+  // THROUGHPUT: the racy pooled-mode kernel. Any exact-mode result is also a
+  // legal outcome of the racy contract (one worker claiming every chunk), so
+  // the exact kernels serve as its fallback when k2 does not apply.
+  if (p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" &&
+      thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
+    s->use_thru = true;
+  const bool pipe_ok = !s->use_thru && force != "exact" &&
+                       pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
   if (force == "pipe" && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
   s->use_pipe = pipe_ok;
-  if (!pipe_ok && exact_plan(g->st, replicas, &s->plan))
+  if (!s->use_thru && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
 
   if (stream) {
@@ -368,6 +449,32 @@ int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
 int gdi_session_launch(gdi_session* s) {
   if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
   GDI_CUDA(cudaSetDevice(s->g->device));
+  if (s->use_thru) {
+    ThruArgs a{};
+    a.g = s->g->csr();
+    a.order = s->g->order.as<int32_t>();
+    a.sell = s->g->sell.as<int4>();
+    a.sell_off = s->g->sell_off.as<int32_t>();
+    a.sell_w = s->g->sell_w.as<int4>();
+    a.edges = s->g->edges.as<int2>();
+    a.edge_w = s->g->edge_w.as<int32_t>();
+    a.m = s->g->st.m;
+    a.sweeps = s->p.sweeps;
+    a.replicas = s->replicas;
+    a.seeds = s->seeds.as<uint64_t>();
+    a.thr = s->thr_d.as<long long>();
+    a.tmask = s->tmask_d.as<unsigned long long>();
+    a.spins_out = s->spins.as<int8_t>();
+    a.trace = s->trace.as<DevTrace>();
+    a.stamps = s->stamps.as<unsigned long long>();
+    a.snaps = s->snaps.as<int8_t>();
+    a.final_out = s->final_out.as<DevTrace>();
+    GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
+    GDI_CUDA(thru_launch(s->tplan, a, s->stream));
+    GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
+    s->launched = true;
+    return GDI_OK;
+  }
   if (s->use_pipe) {
     PipeArgs a{};
     a.g = s->g->csr();
@@ -514,6 +621,7 @@ int gdi_session_launch_count(const gdi_session* s, int32_t* count) {
 
 const char* gdi_session_kernel(const gdi_session* s) {
   if (!s) return "";
+  if (s->use_thru) return s->tplan.name;
   return s->use_pipe ? s->pplan.name : s->plan.name;
 }
 

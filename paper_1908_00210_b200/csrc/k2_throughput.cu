@@ -1,0 +1,256 @@
+// K2 — throughput GDI sweep for the reference's pooled (racy) mode (sm_100a).
+//
+// Contract: reference proj/src/anneal.cpp:203-225 with workers > 1 and
+// SPEC.md "annealer / Concurrency Model": within a sweep every vertex is
+// visited exactly once, concurrently and in any interleaving, reading the
+// current (possibly not yet updated) neighbour spins; every spin change is
+// folded into the shared balance counter G which each visit reads live
+// (visit_node, anneal.cpp:86-128); a barrier ends the sweep, records the
+// exact trace (cut, balance, counter; anneal.cpp:165-187) and decays pf.
+// Results are not bit-reproducible (neither are the reference's); quality is
+// checked statistically against the exact mode (tests/test_gpu_throughput.py).
+//
+// Why one warp per replica. A first version let 128 threads of a CTA visit
+// concurrently against one shared counter: every thread saw nearly the same
+// stale G, all over-corrected together and the balance oscillated (the
+// paper's "biphasic oscillation"; imbalance ~240 on G22).
+// Here a warp owns a replica and visits its vertices in chunks of 32 (one
+// per lane): the 32 decisions are made as if the lanes ran in order, i.e.
+// lane l sees G plus the spin changes of lanes < l. That sequential
+// counter is obtained by a fixed-point iteration on an exclusive warp prefix
+// sum of the deltas (lane 0 is right after one round, lanes <= k after k+1;
+// spin changes are rare, so it converges in 1-3 rounds). Only the
+// neighbour-spin reads inside a chunk stay racy, as the contract allows.
+//
+// Layout: spins int8 in shared memory (n bytes per replica, 4 replicas per
+// CTA). Vertices are visited in a degree-binned order (sorted by degree,
+// built once per graph) and their rows are stored SELL-32 over that order:
+// chunk c holds the rows of order[32c..32c+31] interleaved so that the k-th
+// int4 (4 neighbour indices) of all 32 lanes is one contiguous 512-byte,
+// fully coalesced load, and degree binning keeps the zero-padding small.
+// +-1 weights ride in the sign bit of the index. The layout is shared by all
+// replicas through L1/L2. Draws: Philox4x32-10 keyed by the replica seed with
+// counter (sweep, vertex): out[0..1] = 64-bit unit draw, bit 31 of out[2] =
+// tie coin. Barrier: exact cut over the canonical edge list (coalesced) +
+// spin sum for the trace and the counter-integrity value.
+#include <cuda_runtime.h>
+
+#include "device_rng.cuh"
+#include "kernels.cuh"
+#include "launch.hpp"
+
+namespace gdi {
+
+namespace {
+
+constexpr int kWarps = 4;  // replicas per CTA (one warp each)
+
+__device__ __forceinline__ int decide(int diff, bool coin, bool flip) {
+  const int c = diff < 0 ? 1 : diff > 0 ? -1 : (coin ? 1 : -1);
+  return flip ? -c : c;
+}
+
+// WK: 0 unit weights, 1 +-1 weights (sign bit of the SELL index), 2 general.
+template <int WK>
+__device__ __forceinline__ int contrib(const int8_t* s, int idx, int w) {
+  if (WK == 1) return idx < 0 ? -s[idx & 0x7fffffff] : s[idx];
+  if (WK == 2) return w * s[idx];
+  return s[idx];
+}
+
+// One chunk's spin-independent inputs plus its racy field: gathered one
+// chunk ahead of its decision (see k2_sweep).
+struct ChunkIn {
+  int v, own, f;
+  bool live, coin, flip;
+};
+
+template <int WK, int KMAX>
+__device__ __forceinline__ ChunkIn gather_chunk(const ThruArgs& a, const int8_t* s, int base, int sweep, uint32_t k0,
+                                                uint32_t k1, unsigned long long tm, bool en, int lane) {
+  ChunkIn c{0, 0, 0, false, false, false};
+  const int idx = base + lane;
+  c.live = idx < a.g.n;
+  if (!c.live) return c;
+  c.v = __ldg(a.order + idx);
+  const int c0 = __ldg(a.sell_off + (base >> 5)), c1 = __ldg(a.sell_off + (base >> 5) + 1);
+  const int groups = (c1 - c0) >> 5;
+  // issue every row load first (one coalesced 512 B warp load per group)
+  int4 g4[KMAX], w4[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; k++) {
+    if (k < groups) {
+      g4[k] = __ldg(a.sell + c0 + k * 32 + lane);
+      if (WK == 2) w4[k] = __ldg(a.sell_w + c0 + k * 32 + lane);
+    }
+  }
+  const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(c.v), 0u, 0u, k0, k1);
+  c.coin = (x.z >> 31) != 0;
+  c.flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
+  c.own = s[c.v];
+  int f = 0;
+#pragma unroll
+  for (int k = 0; k < KMAX; k++) {
+    if (k < groups) {
+      const int4 q = g4[k];
+      const int4 w = WK == 2 ? w4[k] : make_int4(1, 1, 1, 1);
+      f += contrib<WK>(s, q.x, w.x) + contrib<WK>(s, q.y, w.y) + contrib<WK>(s, q.z, w.z) + contrib<WK>(s, q.w, w.w);
+    }
+  }
+  for (int k = KMAX; k < groups; k++) {  // rows longer than the bucket
+    const int4 q = __ldg(a.sell + c0 + k * 32 + lane);
+    const int4 w = WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
+    f += contrib<WK>(s, q.x, w.x) + contrib<WK>(s, q.y, w.y) + contrib<WK>(s, q.z, w.z) + contrib<WK>(s, q.w, w.w);
+  }
+  c.f = f;
+  return c;
+}
+
+template <int WK, int KMAX>
+__global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
+  extern __shared__ __align__(16) int8_t smem[];
+  const int n = a.g.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * kWarps + warp;
+  if (r >= a.replicas) return;  // whole warp exits; no block-level sync below
+  int8_t* s = smem + static_cast<size_t>(warp) * a.n_pad;
+  const uint64_t seed = a.seeds[r];
+  const size_t rs = static_cast<size_t>(r);
+  const int2* __restrict__ edges = a.edges;
+  const int32_t* __restrict__ ew = a.edge_w;
+
+  // init (anneal.cpp:148-155): stream-0 coins; the serial stream is walked
+  // by every lane, lane i%32 stores spin i
+  int G = 0;
+  {
+    Xoshiro r0 = Xoshiro::stream(seed, 0);
+    for (int i = 0; i < n; i++) {
+      const int v = (r0.next() >> 63) ? 1 : -1;
+      G += v;
+      if ((i & 31) == lane) s[i] = static_cast<int8_t>(v);
+    }
+    for (int i = n + lane; i < a.n_pad; i += 32) s[i] = 0;  // SELL padding index n reads 0
+  }
+  __syncwarp();
+  if (a.snaps != nullptr)
+    for (int i = lane; i < n; i += 32) a.snaps[rs * (a.sweeps + 1) * n + i] = s[i];
+  if (lane == 0 && a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1)] = globaltimer_ns();
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  const int a4 = a.a4, bb = a.b;
+
+  for (int sweep = 0; sweep < a.sweeps; sweep++) {
+    const unsigned long long tm = a.tmask[sweep];
+    const bool en = a.thr[sweep] >= 0;
+    // Software pipeline over chunks: chunk c+1 is gathered (row loads, spin
+    // reads, draws) before chunk c's spins are written. Those reads are racy
+    // exactly as the contract allows (another worker may read a neighbour
+    // before this one's write lands); the counter stays sequential.
+    ChunkIn cur = gather_chunk<WK, KMAX>(a, s, 0, sweep, k0, k1, tm, en, lane);
+    for (int base = 0; base < n; base += 32) {
+      ChunkIn nxt{0, 0, 0, false, false, false};
+      if (base + 32 < n) nxt = gather_chunk<WK, KMAX>(a, s, base + 32, sweep, k0, k1, tm, en, lane);
+      // sequentially consistent counter inside the chunk (see header)
+      const int base_diff = -a4 * cur.own - bb * cur.f;  // diff = a4 (G + excl) + base_diff
+      int fin = cur.live ? decide(a4 * G + base_diff, cur.coin, cur.flip) : 0;
+      int d = cur.live ? fin - cur.own : 0;
+      if (__any_sync(0xffffffffu, d != 0)) {
+        for (int round = 0; round < 33; round++) {
+          int incl = d;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const int excl = incl - d;
+          const int fin2 = cur.live ? decide(a4 * (G + excl) + base_diff, cur.coin, cur.flip) : 0;
+          if (__all_sync(0xffffffffu, fin2 == fin)) break;
+          fin = fin2;
+          d = cur.live ? fin - cur.own : 0;
+        }
+      }
+      if (cur.live && d != 0) s[cur.v] = static_cast<int8_t>(fin);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      G += d;
+      cur = nxt;
+    }
+    __syncwarp();
+    // record_barrier: exact cut (each edge once, coalesced over the
+    // canonical edge list) + spin sum
+    long long cut = 0;
+    int sum = 0;
+    for (int u = lane; u < n; u += 32) sum += s[u];
+    for (long long e = lane; e < a.m; e += 32) {
+      const int2 uv = __ldg(edges + e);
+      if (s[uv.x] != s[uv.y]) cut += WK == 0 ? 1 : __ldg(ew + e);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cut += __shfl_xor_sync(0xffffffffu, cut, o);
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    }
+    if (lane == 0) {
+      if (a.trace != nullptr) a.trace[rs * a.sweeps + sweep] = DevTrace{cut, sum, G};
+      if (a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1) + sweep + 1] = globaltimer_ns();
+      if (sweep + 1 == a.sweeps) a.final_out[rs] = DevTrace{cut, sum, G};
+    }
+    if (a.snaps != nullptr)
+      for (int i = lane; i < n; i += 32) a.snaps[(rs * (a.sweeps + 1) + sweep + 1) * n + i] = s[i];
+  }
+  for (int i = lane; i < n; i += 32) a.spins_out[rs * n + i] = s[i];
+}
+
+template <int WK>
+const void* k2_fn(int kmax) {
+  switch (kmax) {
+    case 1: return reinterpret_cast<const void*>(&k2_sweep<WK, 1>);
+    case 2: return reinterpret_cast<const void*>(&k2_sweep<WK, 2>);
+    case 4: return reinterpret_cast<const void*>(&k2_sweep<WK, 4>);
+    case 8: return reinterpret_cast<const void*>(&k2_sweep<WK, 8>);
+    default: return reinterpret_cast<const void*>(&k2_sweep<WK, 16>);
+  }
+}
+
+}  // namespace
+
+int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, ThruPlan* plan) {
+  // 32-bit decision arithmetic must be exact (same bound as k1_pipe)
+  long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
+  while (y) {
+    const long long t = x % y;
+    x = y;
+    y = t;
+  }
+  const long long ra = a4 / x, rb = b / x;
+  const double bound = static_cast<double>(ra) * (2.0 * st.n + 1) + static_cast<double>(rb) * (st.max_abs_field + 1);
+  if (bound >= 2147483647.0) return -1;
+  const int n_pad = (st.n + 1 + 15) & ~15;  // + pad entry n
+  const long long smem = static_cast<long long>(n_pad) * kWarps;
+  if (smem > 200 * 1024) return -1;
+  // register-resident row bucket: smallest of 1/2/4/8/16 int4 groups that
+  // holds the longest row (longer rows loop over the remainder)
+  const int groups = (st.max_degree + 3) / 4;
+  const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : groups <= 4 ? 4 : groups <= 8 ? 8 : 16;
+  plan->fn = wkind == 0 ? k2_fn<0>(kmax) : wkind == 1 ? k2_fn<1>(kmax) : k2_fn<2>(kmax);
+  plan->block = 32 * kWarps;
+  plan->grid = (replicas + kWarps - 1) / kWarps;
+  plan->smem = static_cast<int>(smem);
+  plan->n_pad = n_pad;
+  plan->a4 = static_cast<int32_t>(ra);
+  plan->b = static_cast<int32_t>(rb);
+  plan->name = wkind == 0 ? "k2_sweep<unit>" : wkind == 1 ? "k2_sweep<pm1>" : "k2_sweep<weighted>";
+  return 0;
+}
+
+cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t stream) {
+  cudaError_t err = cudaFuncSetAttribute(plan.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+  if (err != cudaSuccess) return err;
+  ThruArgs a = args;
+  a.a4 = plan.a4;
+  a.b = plan.b;
+  a.n_pad = plan.n_pad;
+  void* params[] = {&a};
+  return cudaLaunchKernel(plan.fn, dim3(plan.grid), dim3(plan.block), params, plan.smem, stream);
+}
+
+}  // namespace gdi

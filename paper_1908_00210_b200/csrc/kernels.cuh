@@ -71,6 +71,33 @@ struct PipeArgs {
   int32_t debug;                   // timing experiments only (GDI_PIPE_DEBUG); 0 in production
 };
 
+// k2_sweep (throughput / pooled mode): one CTA per replica.
+struct ThruArgs {
+  DevCsr g;
+  const int32_t* order;            // [n] degree-binned visit order
+  // SELL-32 over `order`: chunk c = order[32c .. 32c+31]; sell[sell_off[c] +
+  // k*32 + lane] = neighbours 4k..4k+3 of the lane's vertex (index n = pad,
+  // bit 31 set = weight -1 on +-1 graphs); sell_w likewise for general weights
+  const int4* sell;
+  const int32_t* sell_off;         // [chunks+1] in int4 units
+  const int4* sell_w;              // nullptr unless general weights
+  const int2* edges;               // [m] canonical (u < v) edge list
+  const int32_t* edge_w;           // [m] or nullptr (unit)
+  int64_t m;
+  int32_t n_pad;                   // per-replica spin stride in shared memory
+  int32_t sweeps;
+  int32_t replicas;
+  const uint64_t* seeds;
+  const long long* thr;
+  const unsigned long long* tmask;
+  int32_t a4, b;                   // reduced by gcd (narrow)
+  int8_t* spins_out;
+  DevTrace* trace;
+  unsigned long long* stamps;
+  int8_t* snaps;
+  DevTrace* final_out;
+};
+
 struct EvalArgs {
   DevCsr g;
   const int8_t* spins;    // [R][n]

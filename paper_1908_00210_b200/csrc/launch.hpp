@@ -59,6 +59,15 @@ int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64
               int32_t sweeps, PipePlan* plan);
 cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);
 
+struct ThruPlan {
+  const void* fn = nullptr;
+  int32_t a4 = 4, b = 4;
+  int block = 128, grid = 1, smem = 0, n_pad = 0;
+  const char* name = "";
+};
+int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, ThruPlan* plan);
+cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t stream);
+
 // K3 fused exact evaluation: {cut, sum} per replica into a zeroed buffer.
 cudaError_t eval_launch(const EvalArgs& args, bool weighted, cudaStream_t stream);
 
