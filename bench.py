@@ -106,20 +106,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def l2_probe_gbs(torch, device) -> float:
-    """Measured L2-resident read bandwidth: sum a 32 MB buffer repeatedly."""
-    x = torch.ones(8 * 1024 * 1024, dtype=torch.float32, device=device)
-    for _ in range(3):
-        x.sum()
-    torch.cuda.synchronize(device)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 50
-    e0.record()
-    for _ in range(reps):
-        x.sum()
-    e1.record()
-    torch.cuda.synchronize(device)
-    return reps * x.numel() * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+def l2_probe_gbs(pi) -> float:
+    """Measured L2-resident read bandwidth (library probe, 48 MB buffer)."""
+    return pi.probe_l2_bandwidth(48 << 20, 50)
 
 
 def ref_tool_path():
@@ -212,6 +201,7 @@ def main():
     ap.add_argument("--replicas", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-throughput", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -249,14 +239,17 @@ def main():
     # L2 flush buffer (> 126 MB L2) rewritten between timed steps
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    def one_step():
+    def step_on(session):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        sess.launch()
+        session.launch()
         e1.record(stream)
         return e0, e1
+
+    def one_step():
+        return step_on(sess)
 
     for _ in range(args.warmup):
         one_step()
@@ -306,7 +299,7 @@ def main():
         except OSError:
             pass
         hbm = peaks.get("hbm_gbs", 6650.0)
-        l2 = l2_probe_gbs(torch, dev)
+        l2 = l2_probe_gbs(pi)
         line = {
             "metric": METRIC, "value": value, "unit": "spin-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
@@ -321,14 +314,51 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                         "bytes_per_update": bpu, "l2_probe_gbs": l2, "frac_of_l2_probe": achieved / l2,
-                         "note": "K1 is latency-bound (serial per replica); working set is L2/smem resident"},
+                         "bytes_per_update": bpu, "l2_peak_gbs": l2, "frac_of_l2": achieved / l2,
+                         "note": "exact mode is bound by the serial per-replica decision chain, not bandwidth; "
+                                 "logical bytes per SURVEY 8(d); CSR and spins are L1/L2/smem resident"},
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * sess.launch_count,
             "wall_s_timed": t_wall,
             "result": best,
         }
+    sess.sync()
     del sess
+
+    # Throughput mode (K2, the reference's pooled racy mode) on the same
+    # workload and seeds: reported beside the exact-mode headline.
+    if not args.no_throughput:
+        tparams = pi.AnnealParams()
+        tparams.sweeps, tparams.workers = sweeps, 8
+        tsess = pi.Session(prob, tparams, R, stream=stream.cuda_stream, trace=True, device=local)
+        tsess.set_seeds(seeds)
+        for _ in range(args.warmup):
+            step_on(tsess)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        tev = [step_on(tsess) for _ in range(args.steps)]
+        torch.cuda.synchronize(dev)
+        t_ms = sum(a.elapsed_time(b) for a, b in tev) / len(tev)
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tsess.sync()
+        tres = tsess.fetch(spins=False, trace=False)
+        if rank == 0:
+            tbal = tres["imbalance"] <= n % 2
+            t_ach = bpu * R * n * sweeps / (t_ms * 1e-3) / 1e9
+            line["throughput_mode"] = {
+                "value": updates_per_step / (float(tt.item()) * 1e-3), "unit": "spin-updates/s",
+                "ms_per_step": float(tt.item()), "kernel": tsess.kernel,
+                "mode": "racy pooled mode (reference workers>1), Philox4x32-10, statistically equivalent",
+                "best_balanced_cut": int(tres["cut"][tbal].min()) if tbal.any() else None,
+                "mean_cut": float(tres["cut"].mean()), "frac_balanced": float(tbal.mean()),
+                "gpu_launches": args.steps * tsess.launch_count,
+                "roofline": {"bound": "hbm", "achieved": t_ach, "peak": hbm, "unit": "GB/s", "frac": t_ach / hbm,
+                             "l2_peak_gbs": l2, "frac_of_l2": t_ach / l2, "bytes_per_update": bpu,
+                             "note": "logical bytes (SURVEY 8(d)); CSR and spins are L1/L2/smem resident"}}
+        del tsess
 
     # e2e: the public batched call with host buffers (fresh CSR upload, seeds
     # H2D, full spins + trace + scores D2H) every step

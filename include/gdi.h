@@ -150,6 +150,11 @@ int gdi_session_launch_count(const gdi_session* s, int32_t* count);
 const char* gdi_session_kernel(const gdi_session* s);
 int gdi_session_destroy(gdi_session* s);
 
+/* Measurement utility (not a reference interface): sustained read bandwidth
+ * in GB/s of an L2-resident buffer of `bytes` bytes re-read `iters` times on
+ * `device`; the roofline denominator for cache-resident graphs. */
+int gdi_probe_l2_bandwidth(int device, int64_t bytes, int32_t iters, double* gbs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -680,4 +680,12 @@ int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas
   return GDI_OK;
 }
 
+int gdi_probe_l2_bandwidth(int device, int64_t bytes, int32_t iters, double* gbs) {
+  if (!gbs || bytes < (1 << 20) || iters < 1) return fail(GDI_ERR_CONFIG, "bad probe arguments");
+  int rc = use_device(device);
+  if (rc) return rc;
+  GDI_CUDA(probe_l2_read(static_cast<size_t>(bytes), iters, gbs));
+  return GDI_OK;
+}
+
 }  // extern "C"

@@ -68,6 +68,9 @@ struct ThruPlan {
 int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, ThruPlan* plan);
 cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t stream);
 
+// L2-resident read bandwidth (GB/s) for roofline denominators.
+cudaError_t probe_l2_read(size_t bytes, int iters, double* gbs);
+
 // K3 fused exact evaluation: {cut, sum} per replica into a zeroed buffer.
 cudaError_t eval_launch(const EvalArgs& args, bool weighted, cudaStream_t stream);
 

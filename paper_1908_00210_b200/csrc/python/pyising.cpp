@@ -456,6 +456,15 @@ PYBIND11_MODULE(pyising, m) {
       .def_property_readonly("launch_count", &Session::launch_count)
       .def_property_readonly("kernel", &Session::kernel);
 
+  m.def(
+      "probe_l2_bandwidth",
+      [](std::int64_t bytes, int iters) {
+        double gbs = 0.0;
+        check_abi(gdi_probe_l2_bandwidth(device(), bytes, iters, &gbs));
+        return gbs;
+      },
+      py::arg("bytes") = 48LL << 20, py::arg("iters") = 50,
+      "Sustained read GB/s of an L2-resident buffer on the current device (roofline denominator).");
   m.def("set_device", &set_device, py::arg("device"));
   m.def("device", &device);
   m.def("device_count", []() {
