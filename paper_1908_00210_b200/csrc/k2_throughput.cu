@@ -154,14 +154,11 @@ __global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
       int fin = cur.live ? decide(a4 * G + base_diff, cur.coin, cur.flip) : 0;
       int d = cur.live ? fin - cur.own : 0;
       if (__any_sync(0xffffffffu, d != 0)) {
+        const unsigned below = (1u << lane) - 1u;  // lanes < this lane
         for (int round = 0; round < 33; round++) {
-          int incl = d;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-          }
-          const int excl = incl - d;
+          // d is -2, 0 or +2: the exclusive prefix is two masked popcounts
+          const unsigned up = __ballot_sync(0xffffffffu, d > 0), dn = __ballot_sync(0xffffffffu, d < 0);
+          const int excl = 2 * (__popc(up & below) - __popc(dn & below));
           const int fin2 = cur.live ? decide(a4 * (G + excl) + base_diff, cur.coin, cur.flip) : 0;
           if (__all_sync(0xffffffffu, fin2 == fin)) break;
           fin = fin2;
@@ -227,9 +224,12 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const int n_pad = (st.n + 1 + 15) & ~15;  // + pad entry n
   const long long smem = static_cast<long long>(n_pad) * kWarps;
   if (smem > 200 * 1024) return -1;
-  // register-resident row bucket: smallest of 1/2/4/8/16 int4 groups that
-  // holds the longest row (longer rows loop over the remainder)
-  const int groups = (st.max_degree + 3) / 4;
+  // register-resident row bucket: the int4 groups of a typical row (mean
+  // degree, rounded up to 1/2/4/8/16); unused slots of the bucket are still
+  // issued (predicated), so it is sized by the mean, not the longest row,
+  // and longer rows loop over the remainder
+  const double mean_deg = st.n > 0 ? 2.0 * static_cast<double>(st.m) / st.n : 0.0;
+  const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : groups <= 4 ? 4 : groups <= 8 ? 8 : 16;
   plan->fn = wkind == 0 ? k2_fn<0>(kmax) : wkind == 1 ? k2_fn<1>(kmax) : k2_fn<2>(kmax);
   plan->block = 32 * kWarps;
