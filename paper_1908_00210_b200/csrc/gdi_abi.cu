@@ -102,7 +102,7 @@ struct gdi_session {
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
-  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof;
+  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
   ~gdi_session() {
@@ -398,12 +398,12 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   // THROUGHPUT: the racy pooled-mode kernel. Any exact-mode result is also a
   // legal outcome of the racy contract (one worker claiming every chunk), so
   // the exact kernels serve as its fallback when k2 does not apply.
-  if (p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" &&
+  if (p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" && force != "pipe_gmem" &&
       thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
     s->use_thru = true;
   const bool pipe_ok = !s->use_thru && force != "exact" &&
                        pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
-  if (force == "pipe" && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
+  if ((force == "pipe" || force == "pipe_gmem") && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
   s->use_pipe = pipe_ok;
   if (!s->use_thru && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
@@ -424,6 +424,8 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   GDI_CUDA(s->final_out.alloc(R * sizeof(DevTrace)));
   GDI_CUDA(s->watchdog.alloc(8 * sizeof(int)));
   GDI_CUDA(s->prof.alloc(16 * sizeof(unsigned long long)));
+  if (s->use_pipe && s->pplan.gw)
+    GDI_CUDA(s->gwords.alloc(static_cast<size_t>(s->pplan.grid) * g->pipe.n_words * sizeof(uint32_t)));
   if (p->flags & GDI_FLAG_TRACE) {
     GDI_CUDA(s->trace.alloc(R * S * sizeof(DevTrace)));
     GDI_CUDA(s->stamps.alloc(R * (S + 1) * sizeof(unsigned long long)));
@@ -483,6 +485,7 @@ int gdi_session_launch(gdi_session* s) {
     a.win_pos = s->g->pipe.win_pos;
     a.win_neg = s->g->pipe.win_neg;
     a.n_words = s->g->pipe.n_words;
+    a.gwords = s->pplan.gw ? s->gwords.as<uint32_t>() : nullptr;
     a.sweeps = s->p.sweeps;
     a.replicas = s->replicas;
     a.seeds = s->seeds.as<uint64_t>();

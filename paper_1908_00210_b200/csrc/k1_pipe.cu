@@ -50,6 +50,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <string>
 
 #include "device_rng.cuh"
 #include "kernels.cuh"
@@ -217,7 +218,12 @@ __device__ __noinline__ void replay_batch(const PipeArgs& a, uint32_t* words, co
 
 // PROF: accumulate clock64 wait/work counters per role into a.prof
 // (profiling builds only, GDI_PIPE_PROFILE=1; see gdi_abi.cu).
-template <bool SIGNED, bool UNITAB, bool PROF>
+// GW: spin words in global memory (one n_words slice per CTA; graphs whose
+// words do not fit in shared memory, e.g. the 1M-vertex config). Only this
+// CTA reads and writes its slice, so the CTA-scope release/acquire on the
+// shared-memory progress counter orders them exactly as in the smem variant
+// (plain loads: no non-coherent __ldg on data written during the kernel).
+template <bool SIGNED, bool UNITAB, bool PROF, bool GW>
 __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.g.n;
@@ -226,8 +232,8 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
   const int rc = a.rc;
   const int replica = blockIdx.x * rc + lane;
   const bool active = lane < rc && replica < a.replicas;
-  const Layout lay = Layout::make(a.n_words);
-  uint32_t* words = reinterpret_cast<uint32_t*>(smem);
+  const Layout lay = Layout::make(GW ? 0 : a.n_words);
+  uint32_t* words = GW ? a.gwords + static_cast<size_t>(blockIdx.x) * a.n_words : reinterpret_cast<uint32_t*>(smem);
   uint64_t* ring = reinterpret_cast<uint64_t*>(smem + lay.ring);
   int2* q = reinterpret_cast<int2*>(smem + lay.q);
   uint2* qm = reinterpret_cast<uint2*>(smem + lay.qm);
@@ -266,12 +272,41 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
 
   // exact initial cut, all warps (evaluate.cpp:10-18), per lane = replica
   long long cut = 0;
-  for (int u = warp; u < n; u += kNW) {
-    const unsigned su = (words[u] >> lane) & 1u;
-    const int e1 = __ldg(a.g.off + u + 1);
-    for (int e = __ldg(a.g.off + u); e < e1; e++) {
-      const int v = __ldg(a.g.col + e);
-      if (v > u && ((words[v] >> lane) & 1u) != su) cut += SIGNED ? __ldg(a.g.w + e) : 1;
+  if (!GW) {
+    for (int u = warp; u < n; u += kNW) {
+      const unsigned su = (words[u] >> lane) & 1u;
+      const int e1 = __ldg(a.g.off + u + 1);
+      for (int e = __ldg(a.g.off + u); e < e1; e++) {
+        const int v = __ldg(a.g.col + e);
+        if (v > u && ((words[v] >> lane) & 1u) != su) cut += SIGNED ? __ldg(a.g.w + e) : 1;
+      }
+    }
+  } else {
+    // large graphs: lane = vertex (independent loads in flight), per-replica
+    // counts bit-sliced in registers, then one warp reduction per replica
+    int c[32];
+#pragma unroll
+    for (int r = 0; r < 32; r++) c[r] = 0;
+    for (int u = warp * 32 + lane; u < n; u += 32 * kNW) {
+      const uint32_t wu = words[u];
+      const int e1 = __ldg(a.g.off + u + 1);
+      for (int e = __ldg(a.g.off + u); e < e1; e++) {
+        const int v = __ldg(a.g.col + e);
+        if (v <= u) continue;
+        const uint32_t x = wu ^ words[v];
+        const int w = SIGNED ? __ldg(a.g.w + e) : 1;
+#pragma unroll
+        for (int r = 0; r < 32; r++)
+          if (r < rc) c[r] += ((x >> r) & 1u) ? w : 0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+      if (r >= rc) break;
+      int t = c[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == r) cut = t;
     }
   }
   part[warp * 32 + lane] = cut;
@@ -593,9 +628,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
 }
 
 template <bool S, bool U>
-const void* pipe_fn(bool prof) {
-  return prof ? reinterpret_cast<const void*>(&k1_pipe<S, U, true>)
-              : reinterpret_cast<const void*>(&k1_pipe<S, U, false>);
+const void* pipe_fn(bool prof, bool gw) {
+  if (gw) return reinterpret_cast<const void*>(&k1_pipe<S, U, false, true>);
+  return prof ? reinterpret_cast<const void*>(&k1_pipe<S, U, true, false>)
+              : reinterpret_cast<const void*>(&k1_pipe<S, U, false, false>);
 }
 
 long long gcd64(long long x, long long y) {
@@ -626,8 +662,11 @@ int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64
   const long long ra = a4 / g, rb = b / g;
   const double bound = static_cast<double>(ra) * (st.n + 3) + static_cast<double>(rb) * (st.max_abs_field + 2);
   if (bound >= 2147483647.0) return -1;
-  const size_t smem = pipe_smem_bytes(pg.n_words, kNW);
-  if (smem > 200 * 1024) return -1;
+  // spin words in shared memory when they fit, else in global memory
+  // (GDI_FORCE_KERNEL=pipe_gmem forces the global variant: parity tests)
+  const char* force = std::getenv("GDI_FORCE_KERNEL");
+  const bool gw = pipe_smem_bytes(pg.n_words, kNW) > 200 * 1024 || (force && std::string(force) == "pipe_gmem");
+  const size_t smem = pipe_smem_bytes(gw ? 0 : pg.n_words, kNW);
   // replicas per CTA: spread R over the SMs (the per-replica chain is the
   // bound, so fewer lanes per CTA only adds parallel CTAs)
   int rc = (replicas + 147) / 148;
@@ -635,18 +674,21 @@ int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64
   const bool unitab = ra == 1 && rb == 1;
   const bool prof = std::getenv("GDI_PIPE_PROFILE") != nullptr;
   if (st.unit)
-    plan->fn = unitab ? pipe_fn<false, true>(prof) : pipe_fn<false, false>(prof);
+    plan->fn = unitab ? pipe_fn<false, true>(prof, gw) : pipe_fn<false, false>(prof, gw);
   else
-    plan->fn = unitab ? pipe_fn<true, true>(prof) : pipe_fn<true, false>(prof);
-  plan->prof = prof;
+    plan->fn = unitab ? pipe_fn<true, true>(prof, gw) : pipe_fn<true, false>(prof, gw);
+  plan->prof = prof && !gw;
+  plan->gw = gw;
   plan->rc = rc;
   plan->block = 32 * kNW;
   plan->grid = (replicas + rc - 1) / rc;
   plan->smem = static_cast<int>(smem);
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
-  plan->name = st.unit ? (unitab ? "k1_pipe<unit,ab=1>" : "k1_pipe<unit>")
-                       : (unitab ? "k1_pipe<signed,ab=1>" : "k1_pipe<signed>");
+  static const char* names[2][2][2] = {
+      {{"k1_pipe<signed>", "k1_pipe<signed,ab=1>"}, {"k1_pipe<signed,gmem>", "k1_pipe<signed,ab=1,gmem>"}},
+      {{"k1_pipe<unit>", "k1_pipe<unit,ab=1>"}, {"k1_pipe<unit,gmem>", "k1_pipe<unit,ab=1,gmem>"}}};
+  plan->name = names[st.unit ? 1 : 0][gw ? 1 : 0][unitab ? 1 : 0];
   return 0;
 }
 

@@ -52,7 +52,8 @@ struct PipeArgs {
   const int4* far_meta;
   const uint32_t* win_pos;
   const uint32_t* win_neg;
-  int32_t n_words;                 // words in shared memory (>= n + 1)
+  int32_t n_words;                 // spin words per CTA (>= n + 1)
+  uint32_t* gwords;                // [grid][n_words] global spin words, or nullptr (shared memory)
   int32_t sweeps;
   int32_t replicas;
   int32_t rc;                      // replicas (lanes) per CTA

@@ -50,6 +50,7 @@ struct PipePlan {
   int grid = 1;
   int smem = 0;
   bool prof = false;
+  bool gw = false;  // spin words in global memory (graph too large for shared memory)
   const char* name = "";
 };
 

@@ -196,3 +196,25 @@ def test_pipe_window_edge_cases_match_oracle():
             ref = o.anneal(og, s, 30, 0.3, 0.9)
             assert out["spins"][i].tolist() == ref["spins"].tolist(), (n, m, s)
             assert out["trace"][i].tolist() == ref["trace"].tolist(), (n, m, s)
+
+
+# ---- global-memory spin words (k1_pipe<...,gmem>): graphs whose words do not
+# fit in shared memory, e.g. the 1M-vertex config (BASELINE configs[4])
+
+
+@pytest.mark.parametrize("name,count", [("G1", 16), ("G22", 256), ("G81pm1", 16)])
+def test_gmem_pipe_variant_bit_exact(name, count, kernel_variant, monkeypatch):
+    if kernel_variant != "auto":
+        pytest.skip("one forced variant is enough")
+    monkeypatch.setenv("GDI_FORCE_KERNEL", "pipe_gmem")
+    s = pi.Session(pi.MinCutProblem.with_default_coefficients(product_graph(golden_configs()[name]["recipe"])),
+                   det_params(), 1)
+    assert s.kernel.endswith("gmem>"), s.kernel
+    check_batch_against_golden(name, count=count)
+
+
+def test_m1_million_vertices_bit_exact(kernel_variant):
+    if kernel_variant != "auto":
+        pytest.skip("k1_exact keeps spins in shared memory: 1M does not fit (capacity)")
+    out = check_batch_against_golden("M1")
+    assert out["cut"][0] == 1252631 and out["imbalance"][0] == 0
