@@ -97,15 +97,20 @@ struct gdi_session {
   ExactPlan plan;
   PipePlan pplan;
   ThruPlan tplan;
+  PartPlan kplan;
   bool use_pipe = false;
   bool use_thru = false;
+  bool use_part = false;
+  cudaGraphExec_t part_exec = nullptr;  // k4: 1 + 3M launches replayed as one graph
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
   DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords;
+  DevBuf live, gsum, gdelta, acc, done, finished, bits;  // k4 state
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
   ~gdi_session() {
+    if (part_exec) cudaGraphExecDestroy(part_exec);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -398,8 +403,21 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   // THROUGHPUT: the racy pooled-mode kernel. Any exact-mode result is also a
   // legal outcome of the racy contract (one worker claiming every chunk), so
   // the exact kernels serve as its fallback when k2 does not apply.
-  if (p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" && force != "pipe_gmem" &&
+  // K2 (one warp per replica, spins in shared memory) when it fits and either
+  // the replicas fill the GPU or the graph is small; else K4 (vertex-
+  // partitioned chains, spins in L2/HBM). K4 keeps ~P*32 vertices in flight
+  // at once: harmless on large graphs (1M: cut within 0.3% of the sequential
+  // run) but a large fraction of a small one, where lattices (torus) then
+  // degrade as under Jacobi updates.
+  const bool thru_ok = p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" &&
+                       force != "pipe_gmem";
+  if (thru_ok && force != "part" && (replicas >= 148 || g->st.n <= 32768) &&
       thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
+    s->use_thru = true;
+  else if (thru_ok && part_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->kplan) == 0)
+    s->use_part = s->use_thru = true;
+  else if (thru_ok && force != "part" &&
+           thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
     s->use_thru = true;
   const bool pipe_ok = !s->use_thru && force != "exact" &&
                        pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
@@ -431,6 +449,15 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
     GDI_CUDA(s->stamps.alloc(R * (S + 1) * sizeof(unsigned long long)));
   }
   if (p->flags & GDI_FLAG_SNAPSHOTS) GDI_CUDA(s->snaps.alloc(R * (S + 1) * n));
+  if (s->use_part) {
+    GDI_CUDA(s->live.alloc(R * part_stride(g->st.n)));
+    GDI_CUDA(s->gsum.alloc(R * sizeof(long long)));
+    GDI_CUDA(s->gdelta.alloc(R * sizeof(long long)));
+    GDI_CUDA(s->acc.alloc(2 * R * sizeof(unsigned long long)));
+    GDI_CUDA(s->done.alloc(R * sizeof(unsigned int)));
+    GDI_CUDA(s->finished.alloc(R * sizeof(unsigned int)));
+    GDI_CUDA(s->bits.alloc(R * ((n + 31) / 32) * sizeof(uint32_t)));
+  }
   GDI_CUDA(cudaMemcpyAsync(s->thr_d.p, s->thr.data(), S * sizeof(long long),
                            cudaMemcpyHostToDevice, s->stream));
   GDI_CUDA(cudaMemcpyAsync(s->tmask_d.p, s->tmask.data(), S * sizeof(unsigned long long),
@@ -451,6 +478,58 @@ int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
 int gdi_session_launch(gdi_session* s) {
   if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
   GDI_CUDA(cudaSetDevice(s->g->device));
+  if (s->use_part) {
+    if (!s->part_exec) {
+      PartArgs a{};
+      a.g = s->g->csr();
+      a.order = s->g->order.as<int32_t>();
+      a.sell = s->g->sell.as<int4>();
+      a.sell_off = s->g->sell_off.as<int32_t>();
+      a.sell_w = s->g->sell_w.as<int4>();
+      a.edges = s->g->edges.as<int2>();
+      a.edge_w = s->g->edge_w.as<int32_t>();
+      a.e_begin = 0;
+      a.e_end = s->g->st.m;
+      a.chains = s->kplan.chains;
+      a.world_chains = s->kplan.chains;
+      a.chain0 = 0;
+      a.sweeps = s->p.sweeps;
+      a.replicas = s->replicas;
+      a.seeds = s->seeds.as<uint64_t>();
+      a.thr = s->thr_d.as<long long>();
+      a.tmask = s->tmask_d.as<unsigned long long>();
+      a.spins = s->live.as<int8_t>();
+      a.gsum = s->gsum.as<long long>();
+      a.gdelta = s->gdelta.as<long long>();
+      a.acc = s->acc.as<unsigned long long>();
+      a.done = s->done.as<unsigned int>();
+      a.finished = s->finished.as<unsigned int>();
+      a.bits = s->bits.as<uint32_t>();
+      a.trace = s->trace.as<DevTrace>();
+      a.stamps = s->stamps.as<unsigned long long>();
+      a.snaps = s->snaps.as<int8_t>();
+      a.final_out = s->final_out.as<DevTrace>();
+      a.watchdog = s->watchdog.as<int>();
+      cudaGraph_t graph = nullptr;
+      GDI_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+      const cudaError_t le = part_launch(s->kplan, a, s->spins.as<int8_t>(), s->stream);
+      const cudaError_t ce = cudaStreamEndCapture(s->stream, &graph);
+      if (le != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return cuda_fail(le, "part_launch (capture)");
+      }
+      GDI_CUDA(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&s->part_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      GDI_CUDA(ie);
+    }
+    GDI_CUDA(cudaMemsetAsync(s->watchdog.p, 0, s->watchdog.bytes, s->stream));
+    GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
+    GDI_CUDA(cudaGraphLaunch(s->part_exec, s->stream));
+    GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
+    s->launched = true;
+    return GDI_OK;
+  }
   if (s->use_thru) {
     ThruArgs a{};
     a.g = s->g->csr();
@@ -532,6 +611,18 @@ int gdi_session_launch(gdi_session* s) {
 // A stalled k1_pipe pipeline aborts itself (watchdog) instead of hanging;
 // surface that as a runtime error rather than returning wrong results.
 static int check_watchdog(gdi_session* s) {
+  if (s->use_part) {
+    int w = 0;
+    GDI_CUDA(cudaMemcpy(&w, s->watchdog.p, sizeof w, cudaMemcpyDeviceToHost));
+    if (w != 0) return fail(GDI_ERR_RUNTIME, "k4_sweep chain token watchdog fired (warp " + std::to_string(w - 40) + ")");
+    if (std::getenv("GDI_K4_DEBUG")) {
+      int d[8] = {0};
+      GDI_CUDA(cudaMemcpy(d, s->watchdog.p, sizeof d, cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[k4 debug] tail g0 %d -> %d, T %d nmain %d | CTAs with residual %d, sum|Gc0| %d sum|Gc| %d\n",
+                   d[2], d[3], d[4], d[5], d[6], d[7], d[1]);
+    }
+    return GDI_OK;
+  }
   if (!s->use_pipe) return GDI_OK;
   if (s->pplan.prof) {
     unsigned long long c[16] = {0};
@@ -618,12 +709,13 @@ int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
 
 int gdi_session_launch_count(const gdi_session* s, int32_t* count) {
   if (!s || !count) return fail(GDI_ERR_CONFIG, "NULL argument");
-  *count = 1;
+  *count = s->use_part ? part_launch_count(s->kplan, s->p.sweeps) : 1;
   return GDI_OK;
 }
 
 const char* gdi_session_kernel(const gdi_session* s) {
   if (!s) return "";
+  if (s->use_part) return s->kplan.name;
   if (s->use_thru) return s->tplan.name;
   return s->use_pipe ? s->pplan.name : s->plan.name;
 }

@@ -99,6 +99,44 @@ struct ThruArgs {
   DevTrace* final_out;
 };
 
+// k4 (vertex-partitioned throughput sweep for large graphs): the chunks of
+// the SELL order are dealt round-robin to `world_chains` chains (chain J owns
+// chunks J, J + world_chains, ...); this device runs chains chain0 ..
+// chain0 + gridDim.x - 1. Spins live in global memory ([R][n], L2-resident).
+struct PartArgs {
+  DevCsr g;
+  const int32_t* order;
+  const int4* sell;
+  const int32_t* sell_off;
+  const int4* sell_w;
+  const int2* edges;               // canonical edge list slice [e_begin, e_end)
+  const int32_t* edge_w;
+  int64_t e_begin, e_end;
+  int32_t chains;                  // chains per replica on this device
+  int32_t world_chains, chain0;
+  int32_t sweeps;
+  int32_t replicas;
+  int32_t sweep;                   // set per launch
+  const uint64_t* seeds;
+  const long long* thr;
+  const unsigned long long* tmask;
+  int32_t a4, b;
+  int8_t* spins;                   // [R][n] live spins (= the session's output)
+  long long* gsum;                 // [R] balance counter at the last barrier
+  long long* gdelta;               // [R] sum of the chains' counter changes this sweep
+  unsigned long long* acc;         // [R][2] cut / spin-sum accumulators
+  unsigned int* done;              // [R] barrier blocks finished
+  unsigned int* finished;          // [R] CTAs finished (tail ticket)
+  uint32_t* bits;                  // [R][ceil(n/32)] packed spins at the barrier
+  int32_t tail;                    // chunks run by the last chain against the exact counter
+  int32_t debug;                   // timing experiments only (GDI_K4_DEBUG); 0 in production
+  DevTrace* trace;
+  unsigned long long* stamps;
+  int8_t* snaps;
+  DevTrace* final_out;
+  int* watchdog;
+};
+
 struct EvalArgs {
   DevCsr g;
   const int8_t* spins;    // [R][n]

@@ -69,6 +69,24 @@ struct ThruPlan {
 int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, ThruPlan* plan);
 cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t stream);
 
+struct PartPlan {
+  const void* sweep_fn = nullptr;
+  const void* cut_fn = nullptr;
+  int32_t a4 = 4, b = 4;
+  int ctas = 1;        // per replica
+  int chains = 16;     // per replica (one per warp)
+  int tail = 0;        // tail chunks (exact counter) per sweep
+  int block = 512;
+  int pack_grid = 148, cut_grid = 148;
+  const char* name = "";
+};
+int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan);
+// Enqueues init + sweeps x (sweep, pack, cut) kernels: 1 + 3 * sweeps launches.
+// spins_out [R][n] receives the final spins (the live array has stride part_stride(n)).
+cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream);
+int part_launch_count(const PartPlan& plan, int32_t sweeps);
+int part_stride(int n);
+
 // L2-resident read bandwidth (GB/s) for roofline denominators.
 cudaError_t probe_l2_read(size_t bytes, int iters, double* gbs);
 

@@ -93,11 +93,16 @@ public:
     out.spins = spins ? sp.data() : nullptr;
     out.scores = sc.data();
     out.trace = trace ? tr.data() : nullptr;
+    std::vector<std::int64_t> ctr(trace ? R * S : 0);
+    out.counters = trace ? ctr.data() : nullptr;
     {
       py::gil_scoped_release nogil;
       check_abi(gdi_session_fetch(sess_, &out));
     }
-    return pack(std::move(sp), sc, tr, R, n, S, out.seconds, spins, trace);
+    py::dict d = pack(std::move(sp), sc, tr, R, n, S, out.seconds, spins, trace);
+    // signed balance counter at every barrier (acceptance criterion 4 checks)
+    if (trace) d["counters"] = to_numpy(std::move(ctr), {static_cast<py::ssize_t>(R), static_cast<py::ssize_t>(S)});
+    return d;
   }
   int launch_count() const {
     std::int32_t c = 0;
