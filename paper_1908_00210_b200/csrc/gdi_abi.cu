@@ -9,12 +9,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
+#include "devbuf.hpp"
 #include "gdi.h"
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "layout.hpp"
 
 using namespace gdi;
 
@@ -36,26 +39,6 @@ int cuda_fail(cudaError_t e, const char* what) {
     cudaError_t e_ = (call);                           \
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
-
-// RAII device allocation.
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-  cudaError_t alloc(size_t b) {
-    bytes = b;
-    return b ? cudaMalloc(&p, b) : cudaSuccess;
-  }
-  template <typename T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
 
 // Selects the device and checks it is a Blackwell (sm_100) part: the
 // kernels are compiled for sm_100a only and there is no fallback.
@@ -79,13 +62,20 @@ struct gdi_graph {
   int device = 0;
   GraphStats st;
   DevBuf off, col, w;
-  DevBuf far_col, far_meta, win_pos, win_neg;  // k1_pipe preprocessing
-  DevBuf order;                                // k2 degree-binned visit order
-  DevBuf sell, sell_off, sell_w, edges, edge_w;  // k2 SELL-32 rows + edge list
-  int wkind = 0;                               // 0 unit, 1 +-1 (sign bit), 2 general
-  PipeGraph pipe;
-  int64_t bytes = 0;
-  DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), w.as<int32_t>(), st.n}; }
+  int wkind = 0;  // 0 unit, 1 +-1 (sign bit), 2 general
+  // kernel layouts, built on the device the first time a session needs one
+  std::mutex mu;
+  bool thru_built = false, pipe_built = false;
+  ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
+  PipeLayout pipel;  // k1_pipe: far lists + window masks
+  PipeGraph pipe;    // k1_pipe view (ok = eligible; pointers once built)
+  DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
+  int64_t bytes() const {
+    return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
+                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes +
+                                pipel.far_col.bytes + pipel.far_meta.bytes + pipel.win_pos.bytes +
+                                pipel.win_neg.bytes);
+  }
 };
 
 struct gdi_session {
@@ -157,128 +147,36 @@ void schedule(const gdi_params& p, std::vector<double>& pf, std::vector<long lon
   }
 }
 
-// Spin-independent split of every row into far entries and the window mask
-// of the L vertices visited just before it (see k1_pipe.cu). far list per
-// vertex: +1 neighbours, then -1 neighbours; meta = {offset, #pos, #neg,
-// fconst} with fconst = (#pos - #neg) + popc(mask+) - popc(mask-).
-int build_pipe(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const int32_t* weights) {
-  const int32_t n = g->st.n;
-  const int L = pipe_window();
-  if (n < 2 * L) return GDI_OK;  // not eligible: k1_exact only
-  for (int64_t e = 0; e < offsets[n]; e++)
-    if (weights && weights[e] != 1 && weights[e] != -1) return GDI_OK;
-  std::vector<int32_t> cols;
-  std::vector<int4> meta(n);
-  std::vector<uint32_t> wp(n, 0u), wn(n, 0u);
-  std::vector<int32_t> pos, neg;
-  cols.reserve(static_cast<size_t>(offsets[n]));
-  for (int32_t i = 0; i < n; i++) {
-    pos.clear();
-    neg.clear();
-    for (int64_t e = offsets[i]; e < offsets[i + 1]; e++) {
-      const int32_t j = nbr[e];
-      const bool minus = weights && weights[e] < 0;
-      const int32_t k = static_cast<int32_t>(((static_cast<int64_t>(i) - j) % n + n) % n);  // 1..n-1
-      if (k >= 1 && k <= L)
-        (minus ? wn[i] : wp[i]) |= 1u << (k - 1);
-      else
-        (minus ? neg : pos).push_back(j);
-    }
-    const int off = static_cast<int>(cols.size());
-    cols.insert(cols.end(), pos.begin(), pos.end());
-    cols.insert(cols.end(), neg.begin(), neg.end());
-    const int dp = static_cast<int>(pos.size()), dn = static_cast<int>(neg.size());
-    const int fconst = (dp - dn) + __builtin_popcount(wp[i]) - __builtin_popcount(wn[i]);
-    meta[i] = make_int4(off, dp, dn, fconst);
-  }
-  cols.push_back(n);  // never empty
-  GDI_CUDA(g->far_col.alloc(cols.size() * sizeof(int32_t)));
-  GDI_CUDA(g->far_meta.alloc(meta.size() * sizeof(int4)));
-  GDI_CUDA(g->win_pos.alloc(n * sizeof(uint32_t)));
-  GDI_CUDA(g->win_neg.alloc(n * sizeof(uint32_t)));
-  GDI_CUDA(cudaMemcpy(g->far_col.p, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  GDI_CUDA(cudaMemcpy(g->far_meta.p, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  GDI_CUDA(cudaMemcpy(g->win_pos.p, wp.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  GDI_CUDA(cudaMemcpy(g->win_neg.p, wn.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  g->pipe.ok = true;
-  g->pipe.n_words = (n + 1 + 3) & ~3;
-  g->pipe.far_col = g->far_col.as<int32_t>();
-  g->pipe.far_meta = g->far_meta.as<int4>();
-  g->pipe.win_pos = g->win_pos.as<uint32_t>();
-  g->pipe.win_neg = g->win_neg.as<uint32_t>();
+// Lazy layout builders (layout.cu), serialised per graph.
+int ensure_thru(gdi_graph* g) {
+  std::lock_guard<std::mutex> lock(g->mu);
+  if (g->thru_built) return GDI_OK;
+  cudaStream_t st = nullptr;
+  GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const cudaError_t e = build_thru_layout(g->csr(), g->st.m, g->wkind, &g->thru, st);
+  cudaStreamDestroy(st);
+  if (e == cudaErrorInvalidValue) return fail(GDI_ERR_CAPACITY, "SELL layout exceeds 2^31 entries");
+  GDI_CUDA(e);
+  g->thru_built = true;
   return GDI_OK;
 }
 
-// Throughput-kernel layout: degree-binned order, SELL-32 rows over it and
-// the canonical edge list for the per-sweep exact cut (see k2_throughput.cu).
-int build_thru(gdi_graph* g, const int64_t* offsets, const int32_t* nbr, const int32_t* weights) {
-  const int32_t n = g->st.n;
-  bool pm1 = true;
-  for (int64_t e = 0; weights && e < offsets[n]; e++)
-    if (weights[e] != 1 && weights[e] != -1) pm1 = false;
-  g->wkind = !weights || g->st.unit ? 0 : (pm1 ? 1 : 2);
-  std::vector<int32_t> ord(static_cast<size_t>(n));
-  for (int32_t i = 0; i < n; i++) ord[i] = i;
-  // descending degree, ties by index: a chunk's 32 rows have nearly equal length
-  std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
-    return offsets[x + 1] - offsets[x] > offsets[y + 1] - offsets[y];
-  });
-  const int32_t chunks = (n + 31) / 32;
-  std::vector<int32_t> soff(static_cast<size_t>(chunks) + 1, 0);
-  for (int32_t c = 0; c < chunks; c++) {
-    int64_t kmax = 0;
-    for (int32_t l = 0; l < 32 && 32 * c + l < n; l++) {
-      const int32_t v = ord[32 * c + l];
-      kmax = std::max<int64_t>(kmax, offsets[v + 1] - offsets[v]);
-    }
-    const int64_t next = soff[c] + ((kmax + 3) / 4) * 32;
-    if (next > 0x7fffffffLL) return fail(GDI_ERR_CAPACITY, "SELL layout exceeds 2^31 entries");
-    soff[c + 1] = static_cast<int32_t>(next);
-  }
-  std::vector<int4> sell(std::max<size_t>(1, static_cast<size_t>(soff[chunks])), make_int4(n, n, n, n));
-  std::vector<int4> sellw(g->wkind == 2 ? sell.size() : 0, make_int4(0, 0, 0, 0));
-  for (int32_t c = 0; c < chunks; c++)
-    for (int32_t l = 0; l < 32 && 32 * c + l < n; l++) {
-      const int32_t v = ord[32 * c + l];
-      for (int64_t e = offsets[v]; e < offsets[v + 1]; e++) {
-        const int64_t k = e - offsets[v];
-        const size_t slot = static_cast<size_t>(soff[c]) + static_cast<size_t>(k / 4) * 32 + l;
-        int32_t idx = nbr[e];
-        if (g->wkind == 1 && weights[e] < 0) idx |= static_cast<int32_t>(0x80000000u);
-        (&sell[slot].x)[k % 4] = idx;
-        if (g->wkind == 2) (&sellw[slot].x)[k % 4] = weights[e];
-      }
-    }
-  std::vector<int2> edges;
-  std::vector<int32_t> ew;
-  edges.reserve(static_cast<size_t>(g->st.m));
-  for (int32_t u = 0; u < n; u++)
-    for (int64_t e = offsets[u]; e < offsets[u + 1]; e++)
-      if (nbr[e] > u) {
-        edges.push_back(make_int2(u, nbr[e]));
-        if (g->wkind != 0) ew.push_back(weights[e]);
-      }
-  if (edges.empty()) edges.push_back(make_int2(0, 0));
-  GDI_CUDA(g->order.alloc(ord.size() * sizeof(int32_t)));
-  GDI_CUDA(cudaMemcpy(g->order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  GDI_CUDA(g->sell.alloc(sell.size() * sizeof(int4)));
-  GDI_CUDA(cudaMemcpy(g->sell.p, sell.data(), sell.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  GDI_CUDA(g->sell_off.alloc(soff.size() * sizeof(int32_t)));
-  GDI_CUDA(cudaMemcpy(g->sell_off.p, soff.data(), soff.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  if (!sellw.empty()) {
-    GDI_CUDA(g->sell_w.alloc(sellw.size() * sizeof(int4)));
-    GDI_CUDA(cudaMemcpy(g->sell_w.p, sellw.data(), sellw.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  }
-  GDI_CUDA(g->edges.alloc(edges.size() * sizeof(int2)));
-  GDI_CUDA(cudaMemcpy(g->edges.p, edges.data(), edges.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  if (!ew.empty()) {
-    GDI_CUDA(g->edge_w.alloc(ew.size() * sizeof(int32_t)));
-    GDI_CUDA(cudaMemcpy(g->edge_w.p, ew.data(), ew.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  }
+int ensure_pipe(gdi_graph* g) {
+  std::lock_guard<std::mutex> lock(g->mu);
+  if (g->pipe_built) return GDI_OK;
+  cudaStream_t st = nullptr;
+  GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const cudaError_t e = build_pipe_layout(g->csr(), pipe_window(), &g->pipel, st);
+  cudaStreamDestroy(st);
+  GDI_CUDA(e);
+  g->pipe.far_col = g->pipel.far_col.as<int32_t>();
+  g->pipe.far_meta = g->pipel.far_meta.as<int4>();
+  g->pipe.win_pos = g->pipel.win_pos.as<uint32_t>();
+  g->pipe.win_neg = g->pipel.win_neg.as<uint32_t>();
+  g->pipe_built = true;
   return GDI_OK;
 }
 
-// GDI_FORCE_KERNEL=exact|pipe pins the exact-mode variant (tests run both).
 const char* forced_kernel() {
   const char* e = std::getenv("GDI_FORCE_KERNEL");
   return e ? e : "";
@@ -314,51 +212,42 @@ int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_
     return fail(GDI_ERR_DOMAIN, "offsets must start at 0 and hold an even entry count");
   if (nnz > 0x7fffffffLL) return fail(GDI_ERR_CAPACITY, "more than 2^31-1 adjacency entries");
   if (nnz > 0 && !nbr) return fail(GDI_ERR_DOMAIN, "nbr is NULL");
+  // graph.cpp:47-61 invariants, checked before any device work so that a bad
+  // CSR is a domain error on every machine (the statistics come from the
+  // device pass below)
+  for (int32_t i = 0; i < n; i++) {
+    const int64_t o0 = offsets[i], o1 = offsets[i + 1];
+    if (o1 < o0) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
+    for (int64_t e = o0; e < o1; e++) {
+      const int32_t v = nbr[e];
+      if (v < 0 || v >= n) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
+      if (v == i) return fail(GDI_ERR_DOMAIN, "self-loop");
+    }
+  }
 
   auto g = std::make_unique<gdi_graph>();
   g->device = device;
   g->st.n = n;
   g->st.m = nnz / 2;
-  std::vector<int32_t> off32(static_cast<size_t>(n) + 1);
-  for (int32_t i = 0; i <= n; i++) {
-    if (i > 0 && offsets[i] < offsets[i - 1]) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
-    off32[i] = static_cast<int32_t>(offsets[i]);
-  }
-  bool unit = true;
-  long long max_field = 0;
-  int32_t max_deg = 0;
-  for (int32_t i = 0; i < n; i++) {
-    long long row = 0;
-    for (int64_t e = offsets[i]; e < offsets[i + 1]; e++) {
-      const int32_t v = nbr[e];
-      if (v < 0 || v >= n) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
-      if (v == i) return fail(GDI_ERR_DOMAIN, "self-loop");
-      const long long wv = weights ? weights[e] : 1;
-      if (wv != 1) unit = false;
-      row += wv < 0 ? -wv : wv;
-    }
-    max_field = std::max(max_field, row);
-    max_deg = std::max<int32_t>(max_deg, static_cast<int32_t>(offsets[i + 1] - offsets[i]));
-  }
-  g->st.unit = unit;
-  g->st.max_abs_field = max_field;
-  g->st.max_degree = max_deg;
-
   int rc = use_device(device);
   if (rc) return rc;
-  GDI_CUDA(g->off.alloc(off32.size() * sizeof(int32_t)));
-  GDI_CUDA(g->col.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
-  GDI_CUDA(cudaMemcpy(g->off.p, off32.data(), off32.size() * sizeof(int32_t),
-                      cudaMemcpyHostToDevice));
-  if (nnz) GDI_CUDA(cudaMemcpy(g->col.p, nbr, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
-  if (!unit) {
-    GDI_CUDA(g->w.alloc(nnz * sizeof(int32_t)));
-    GDI_CUDA(cudaMemcpy(g->w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
-  }
-  if ((rc = build_pipe(g.get(), offsets, nbr, weights))) return rc;
-  if ((rc = build_thru(g.get(), offsets, nbr, weights))) return rc;
-  g->bytes = static_cast<int64_t>(g->off.bytes + g->col.bytes + g->w.bytes + g->far_col.bytes +
-                                  g->far_meta.bytes + g->win_pos.bytes + g->win_neg.bytes);
+  // upload + validation + statistics on the device (layout.cu)
+  GraphScan scan{};
+  cudaStream_t st = nullptr;
+  GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const cudaError_t ue = upload_and_scan(offsets, nbr, weights, n, nnz, g->off, g->col, g->w, &scan, st);
+  cudaStreamDestroy(st);
+  GDI_CUDA(ue);
+  if (scan.bad & 1u) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
+  if (scan.bad & 2u) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
+  if (scan.bad & 4u) return fail(GDI_ERR_DOMAIN, "self-loop");
+  g->st.unit = !weights || !scan.non_unit;
+  g->st.max_abs_field = static_cast<long long>(scan.max_abs_field);
+  g->st.max_degree = scan.max_degree;
+  g->wkind = g->st.unit ? 0 : (!scan.non_pm1 ? 1 : 2);
+  // k1_pipe eligibility (every |w| == 1, n >= 2L); its layout is built lazily
+  g->pipe.ok = n >= 2 * pipe_window() && (g->st.unit || !scan.non_pm1);
+  g->pipe.n_words = (n + 1 + 3) & ~3;
   *out = g.release();
   return GDI_OK;
 }
@@ -378,7 +267,7 @@ int gdi_graph_query(const gdi_graph* g, gdi_graph_info* info) {
   info->max_degree = g->st.max_degree;
   info->device = g->device;
   info->all_unit_weights = g->st.unit ? 1 : 0;
-  info->device_bytes = g->bytes;
+  info->device_bytes = g->bytes();
   return GDI_OK;
 }
 
@@ -425,6 +314,9 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   s->use_pipe = pipe_ok;
   if (!s->use_thru && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
+  gdi_graph* gm = const_cast<gdi_graph*>(g);  // layouts are a lazily built cache
+  if (s->use_thru && (rc = ensure_thru(gm))) return rc;
+  if (s->use_pipe && (rc = ensure_pipe(gm))) return rc;
 
   if (stream) {
     s->stream = static_cast<cudaStream_t>(stream);
@@ -482,12 +374,12 @@ int gdi_session_launch(gdi_session* s) {
     if (!s->part_exec) {
       PartArgs a{};
       a.g = s->g->csr();
-      a.order = s->g->order.as<int32_t>();
-      a.sell = s->g->sell.as<int4>();
-      a.sell_off = s->g->sell_off.as<int32_t>();
-      a.sell_w = s->g->sell_w.as<int4>();
-      a.edges = s->g->edges.as<int2>();
-      a.edge_w = s->g->edge_w.as<int32_t>();
+      a.order = s->g->thru.order.as<int32_t>();
+      a.sell = s->g->thru.sell.as<int4>();
+      a.sell_off = s->g->thru.sell_off.as<int32_t>();
+      a.sell_w = s->g->thru.sell_w.as<int4>();
+      a.edges = s->g->thru.edges.as<int2>();
+      a.edge_w = s->g->thru.edge_w.as<int32_t>();
       a.e_begin = 0;
       a.e_end = s->g->st.m;
       a.chains = s->kplan.chains;
@@ -533,12 +425,12 @@ int gdi_session_launch(gdi_session* s) {
   if (s->use_thru) {
     ThruArgs a{};
     a.g = s->g->csr();
-    a.order = s->g->order.as<int32_t>();
-    a.sell = s->g->sell.as<int4>();
-    a.sell_off = s->g->sell_off.as<int32_t>();
-    a.sell_w = s->g->sell_w.as<int4>();
-    a.edges = s->g->edges.as<int2>();
-    a.edge_w = s->g->edge_w.as<int32_t>();
+    a.order = s->g->thru.order.as<int32_t>();
+    a.sell = s->g->thru.sell.as<int4>();
+    a.sell_off = s->g->thru.sell_off.as<int32_t>();
+    a.sell_w = s->g->thru.sell_w.as<int4>();
+    a.edges = s->g->thru.edges.as<int2>();
+    a.edge_w = s->g->thru.edge_w.as<int32_t>();
     a.m = s->g->st.m;
     a.sweeps = s->p.sweeps;
     a.replicas = s->replicas;

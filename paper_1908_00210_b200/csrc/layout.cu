@@ -1,0 +1,312 @@
+// Graph loader on the device (SURVEY.md §8(f)3 "loader throughput").
+//
+// gdi_graph_create uploads the reference CSR (graph.hpp:66-67: int64 row
+// offsets, int32 neighbours, int32 weights) once and everything else is
+// derived on the GPU:
+//   * validation + statistics (graph.cpp:47-61 invariants: monotone offsets,
+//     endpoints in range, no self loops; unit / +-1 weights, max degree,
+//     max_i sum_j |w_ij| for the 32-bit decision bound), one thread per row;
+//   * the throughput layout (K2/K4): degree-binned visit order (stable radix
+//     sort, descending degree, ties by index), SELL-32 rows over it, and the
+//     canonical u < v edge list for the barrier cut;
+//   * the exact-pipe layout (k1_pipe): per row the "far" neighbours and the
+//     32-bit window masks of the L vertices visited just before it.
+// The layouts are built lazily, the first time a session needs one. A host
+// version of all this took ~0.4 s for the 1M-vertex graph, more than the
+// whole 20-sweep anneal; here it is a few milliseconds.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include "devbuf.hpp"
+#include "layout.hpp"
+
+namespace gdi {
+
+namespace {
+
+constexpr int kB = 256;
+
+inline unsigned blocks(long long n) { return static_cast<unsigned>((n + kB - 1) / kB < 1 ? 1 : (n + kB - 1) / kB); }
+
+__global__ void k_validate(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                           const int32_t* __restrict__ w, int n, int32_t* off32, GraphScan* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t o0 = off[i], o1 = off[i + 1];
+  off32[i] = static_cast<int32_t>(o0);
+  if (i == n - 1) off32[n] = static_cast<int32_t>(o1);
+  unsigned bad = 0;
+  if (o1 < o0) bad |= 1u;
+  bool unit = true, pm1 = true;
+  long long row = 0;
+  for (int64_t e = o0; e < o1; e++) {
+    const int32_t v = col[e];
+    if (v < 0 || v >= n) bad |= 2u;
+    if (v == i) bad |= 4u;
+    const long long wv = w ? w[e] : 1;
+    unit &= wv == 1;
+    pm1 &= wv == 1 || wv == -1;
+    row += wv < 0 ? -wv : wv;
+  }
+  if (bad) atomicOr(&out->bad, bad);
+  if (!unit) atomicOr(&out->non_unit, 1u);
+  if (!pm1) atomicOr(&out->non_pm1, 1u);
+  atomicMax(&out->max_abs_field, static_cast<unsigned long long>(row));
+  atomicMax(&out->max_degree, static_cast<int>(o1 > o0 ? o1 - o0 : 0));
+}
+
+// ---- throughput layout -------------------------------------------------------
+
+__global__ void k_degree(const int32_t* off, int n, int32_t* deg, int32_t* idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    deg[i] = off[i + 1] - off[i];
+    idx[i] = i;
+  }
+}
+
+// SELL-32 slots of chunk c: the chunk's longest row (its first, the order is
+// degree-descending) rounded up to int4 groups, times 32 lanes
+__global__ void k_chunk_slots(const int32_t* deg_sorted, int n, int chunks, long long* cnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < chunks) cnt[c] = static_cast<long long>((deg_sorted[32 * c] + 3) / 4) * 32;
+  if (c == chunks) cnt[c] = 0;
+}
+
+__global__ void k_to_i32(const long long* a, int count, int32_t* b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) b[i] = static_cast<int32_t>(a[i]);
+}
+
+__global__ void k_fill_i32(int32_t* p, long long count, int32_t v) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+// thread = (chunk, lane): copies its row into the lane's column of the chunk
+template <int WK>
+__global__ void k_sell_fill(const int32_t* off, const int32_t* col, const int32_t* w, const int32_t* ord,
+                            const int32_t* soff, int n, int32_t* sell, int32_t* sellw) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int c = t >> 5, l = t & 31, v = ord[t];
+  const int o0 = off[v], o1 = off[v + 1];
+  for (int e = o0; e < o1; e++) {
+    const int k = e - o0;
+    const long long slot = static_cast<long long>(soff[c]) + (k >> 2) * 32 + l;
+    int32_t idx = col[e];
+    if (WK == 1 && w[e] < 0) idx |= static_cast<int32_t>(0x80000000u);
+    sell[slot * 4 + (k & 3)] = idx;
+    if (WK == 2) sellw[slot * 4 + (k & 3)] = w[e];
+  }
+}
+
+__global__ void k_up_count(const int32_t* off, const int32_t* col, int n, int32_t* cnt) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u > n) return;
+  if (u == n) {
+    cnt[u] = 0;
+    return;
+  }
+  int c = 0;
+  for (int e = off[u]; e < off[u + 1]; e++) c += col[e] > u;
+  cnt[u] = c;
+}
+
+__global__ void k_edges_fill(const int32_t* off, const int32_t* col, const int32_t* w, const int32_t* eoff, int n,
+                             int2* edges, int32_t* ew) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  int p = eoff[u];
+  for (int e = off[u]; e < off[u + 1]; e++)
+    if (col[e] > u) {
+      edges[p] = make_int2(u, col[e]);
+      if (ew) ew[p] = w[e];
+      p++;
+    }
+}
+
+// ---- exact-pipe layout (k1_pipe.cu) -----------------------------------------
+
+// window distance of neighbour j from row i: k = (i - j) mod n in 1..n-1
+__device__ __forceinline__ int wdist(int i, int j, int n) {
+  const int k = i - j;
+  return k < 0 ? k + n : k;
+}
+
+__global__ void k_far_count(const int32_t* off, const int32_t* col, int n, int L, int32_t* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {
+    cnt[i] = 0;
+    return;
+  }
+  int c = 0;
+  for (int e = off[i]; e < off[i + 1]; e++) {
+    const int k = wdist(i, col[e], n);
+    c += !(k >= 1 && k <= L);
+  }
+  cnt[i] = c;
+}
+
+// far list per row: +1 neighbours then -1 neighbours; meta = {offset, #pos,
+// #neg, fconst}, fconst = (#pos - #neg) + popc(mask+) - popc(mask-)
+__global__ void k_far_fill(const int32_t* off, const int32_t* col, const int32_t* w, const int32_t* foff, int n,
+                           int L, int32_t* far_col, int4* meta, uint32_t* wpos, uint32_t* wneg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t mp = 0u, mn = 0u;
+  int dp = 0, dn = 0;
+  for (int e = off[i]; e < off[i + 1]; e++) {
+    const int k = wdist(i, col[e], n);
+    const bool minus = w && w[e] < 0;
+    if (k >= 1 && k <= L)
+      (minus ? mn : mp) |= 1u << (k - 1);
+    else if (minus)
+      dn++;
+    else
+      dp++;
+  }
+  const int base = foff[i];
+  int p = 0, q = 0;
+  for (int e = off[i]; e < off[i + 1]; e++) {
+    const int k = wdist(i, col[e], n);
+    if (k >= 1 && k <= L) continue;
+    if (w && w[e] < 0)
+      far_col[base + dp + q++] = col[e];
+    else
+      far_col[base + p++] = col[e];
+  }
+  meta[i] = make_int4(base, dp, dn, (dp - dn) + __popc(mp) - __popc(mn));
+  wpos[i] = mp;
+  wneg[i] = mn;
+}
+
+template <typename T>
+cudaError_t exclusive_scan(const T* in, T* out, int count, cudaStream_t st) {
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, st);
+  if (e) return e;
+  DevBuf tmp;
+  if ((e = tmp.alloc(bytes))) return e;
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, count, st))) return e;
+  return cudaStreamSynchronize(st);  // tmp is released on return
+}
+
+}  // namespace
+
+cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, int n, int64_t nnz,
+                            DevBuf& off32, DevBuf& col, DevBuf& w, GraphScan* scan, cudaStream_t st) {
+  cudaError_t e;
+  DevBuf off64, d_scan;
+  if ((e = off64.alloc((n + 1) * sizeof(int64_t)))) return e;
+  if ((e = off32.alloc((n + 1) * sizeof(int32_t)))) return e;
+  if ((e = col.alloc((nnz > 0 ? nnz : 1) * sizeof(int32_t)))) return e;
+  if ((e = d_scan.alloc(sizeof(GraphScan)))) return e;
+  if ((e = cudaMemcpyAsync(off64.p, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st))) return e;
+  if (nnz && (e = cudaMemcpyAsync(col.p, nbr, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
+  if (weights) {
+    if ((e = w.alloc(nnz * sizeof(int32_t)))) return e;
+    if (nnz && (e = cudaMemcpyAsync(w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
+  }
+  if ((e = cudaMemsetAsync(d_scan.p, 0, sizeof(GraphScan), st))) return e;
+  k_validate<<<blocks(n), kB, 0, st>>>(off64.as<int64_t>(), col.as<int32_t>(), w.as<int32_t>(), n,
+                                        off32.as<int32_t>(), d_scan.as<GraphScan>());
+  if ((e = cudaGetLastError())) return e;
+  if ((e = cudaMemcpyAsync(scan, d_scan.p, sizeof(GraphScan), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  if (!weights || !scan->non_unit) w.reset();  // unit weights: no weight array downstream
+  return cudaSuccess;
+}
+
+cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout* L, cudaStream_t st) {
+  const int n = g.n, chunks = (n + 31) / 32;
+  cudaError_t e;
+  // degree-binned order: stable radix sort on degree, descending
+  DevBuf deg, deg_s, idx;
+  if ((e = deg.alloc(n * sizeof(int32_t))) || (e = deg_s.alloc(n * sizeof(int32_t))) ||
+      (e = idx.alloc(n * sizeof(int32_t))) || (e = L->order.alloc(n * sizeof(int32_t))))
+    return e;
+  k_degree<<<blocks(n), kB, 0, st>>>(g.off, n, deg.as<int32_t>(), idx.as<int32_t>());
+  {
+    size_t bytes = 0;
+    if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, deg.as<int32_t>(), deg_s.as<int32_t>(),
+                                                       idx.as<int32_t>(), L->order.as<int32_t>(), n, 0, 32, st)))
+      return e;
+    DevBuf tmp;
+    if ((e = tmp.alloc(bytes))) return e;
+    if ((e = cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, deg.as<int32_t>(), deg_s.as<int32_t>(),
+                                                       idx.as<int32_t>(), L->order.as<int32_t>(), n, 0, 32, st)))
+      return e;
+    if ((e = cudaStreamSynchronize(st))) return e;
+  }
+  // chunk offsets (int4 units) by an exclusive scan of the chunk sizes
+  DevBuf cnt, soff64;
+  if ((e = cnt.alloc((chunks + 1) * sizeof(long long))) || (e = soff64.alloc((chunks + 1) * sizeof(long long))))
+    return e;
+  k_chunk_slots<<<blocks(chunks + 1), kB, 0, st>>>(deg_s.as<int32_t>(), n, chunks, cnt.as<long long>());
+  if ((e = exclusive_scan(cnt.as<long long>(), soff64.as<long long>(), chunks + 1, st))) return e;
+  long long total = 0;
+  if ((e = cudaMemcpy(&total, soff64.as<long long>() + chunks, sizeof total, cudaMemcpyDeviceToHost))) return e;
+  if (total > 0x7fffffffLL) return cudaErrorInvalidValue;  // reported as capacity by the caller
+  L->slots = total;
+  if ((e = L->sell_off.alloc((chunks + 1) * sizeof(int32_t)))) return e;
+  k_to_i32<<<blocks(chunks + 1), kB, 0, st>>>(soff64.as<long long>(), chunks + 1, L->sell_off.as<int32_t>());
+  const long long cells = (total > 0 ? total : 1) * 4;
+  if ((e = L->sell.alloc(cells * sizeof(int32_t)))) return e;
+  k_fill_i32<<<1024, kB, 0, st>>>(L->sell.as<int32_t>(), cells, n);  // padding index n reads spin 0
+  if (wkind == 2) {
+    if ((e = L->sell_w.alloc(cells * sizeof(int32_t)))) return e;
+    k_fill_i32<<<1024, kB, 0, st>>>(L->sell_w.as<int32_t>(), cells, 0);
+  } else {
+    L->sell_w.reset();
+  }
+  if (wkind == 0)
+    k_sell_fill<0><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, L->order.as<int32_t>(), L->sell_off.as<int32_t>(), n,
+                                             L->sell.as<int32_t>(), nullptr);
+  else if (wkind == 1)
+    k_sell_fill<1><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, L->order.as<int32_t>(), L->sell_off.as<int32_t>(), n,
+                                             L->sell.as<int32_t>(), nullptr);
+  else
+    k_sell_fill<2><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, L->order.as<int32_t>(), L->sell_off.as<int32_t>(), n,
+                                             L->sell.as<int32_t>(), L->sell_w.as<int32_t>());
+  // canonical edge list (u < v, row order): count, scan, fill
+  DevBuf ucnt, eoff;
+  if ((e = ucnt.alloc((n + 1) * sizeof(int32_t))) || (e = eoff.alloc((n + 1) * sizeof(int32_t)))) return e;
+  k_up_count<<<blocks(n + 1), kB, 0, st>>>(g.off, g.col, n, ucnt.as<int32_t>());
+  if ((e = exclusive_scan(ucnt.as<int32_t>(), eoff.as<int32_t>(), n + 1, st))) return e;
+  if ((e = L->edges.alloc((m > 0 ? m : 1) * sizeof(int2)))) return e;
+  if (m == 0) k_fill_i32<<<1, 32, 0, st>>>(L->edges.as<int32_t>(), 2, 0);
+  if (wkind != 0) {
+    if ((e = L->edge_w.alloc((m > 0 ? m : 1) * sizeof(int32_t)))) return e;
+  } else {
+    L->edge_w.reset();
+  }
+  k_edges_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, wkind != 0 ? g.w : nullptr, eoff.as<int32_t>(), n,
+                                         L->edges.as<int2>(), wkind != 0 ? L->edge_w.as<int32_t>() : nullptr);
+  if ((e = cudaGetLastError())) return e;
+  return cudaStreamSynchronize(st);
+}
+
+cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st) {
+  const int n = g.n;
+  cudaError_t e;
+  DevBuf cnt, foff;
+  if ((e = cnt.alloc((n + 1) * sizeof(int32_t))) || (e = foff.alloc((n + 1) * sizeof(int32_t)))) return e;
+  k_far_count<<<blocks(n + 1), kB, 0, st>>>(g.off, g.col, n, win, cnt.as<int32_t>());
+  if ((e = exclusive_scan(cnt.as<int32_t>(), foff.as<int32_t>(), n + 1, st))) return e;
+  int total = 0;
+  if ((e = cudaMemcpy(&total, foff.as<int32_t>() + n, sizeof total, cudaMemcpyDeviceToHost))) return e;
+  if ((e = L->far_col.alloc((static_cast<size_t>(total) + 1) * sizeof(int32_t))) ||
+      (e = L->far_meta.alloc(n * sizeof(int4))) || (e = L->win_pos.alloc(n * sizeof(uint32_t))) ||
+      (e = L->win_neg.alloc(n * sizeof(uint32_t))))
+    return e;
+  k_fill_i32<<<1, 32, 0, st>>>(L->far_col.as<int32_t>() + total, 1, n);  // never empty; index n = zero word
+  k_far_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, foff.as<int32_t>(), n, win, L->far_col.as<int32_t>(),
+                                       L->far_meta.as<int4>(), L->win_pos.as<uint32_t>(), L->win_neg.as<uint32_t>());
+  if ((e = cudaGetLastError())) return e;
+  return cudaStreamSynchronize(st);
+}
+
+}  // namespace gdi

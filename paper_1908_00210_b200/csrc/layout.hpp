@@ -1,0 +1,45 @@
+// Device-side graph loader (layout.cu): upload + validation, and the kernel
+// layouts derived from the CSR on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "devbuf.hpp"
+#include "kernels.cuh"
+
+namespace gdi {
+
+// Result of the device validation pass (graph.cpp:47-61 invariants + stats).
+struct GraphScan {
+  unsigned bad;       // bit 0: offsets not monotone, 1: endpoint out of range, 2: self loop
+  unsigned non_unit;  // some weight != 1
+  unsigned non_pm1;   // some weight not in {-1, +1}
+  int max_degree;
+  unsigned long long max_abs_field;  // max_i sum_j |w_ij|
+};
+
+struct ThruLayout {
+  DevBuf order, sell, sell_off, sell_w, edges, edge_w;
+  long long slots = 0;  // int4 cells of SELL
+};
+
+struct PipeLayout {
+  DevBuf far_col, far_meta, win_pos, win_neg;
+};
+
+// Uploads the reference CSR (int64 offsets, int32 neighbours, optional int32
+// weights), converts the offsets to int32 and validates on the device.
+// `w` is released when every weight is 1.
+cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, int n, int64_t nnz,
+                            DevBuf& off32, DevBuf& col, DevBuf& w, GraphScan* scan, cudaStream_t st);
+
+// K2/K4 layout. wkind: 0 unit, 1 +-1 (sign bit), 2 general weights.
+// Returns cudaErrorInvalidValue when SELL would exceed 2^31 int4 cells.
+cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout* L, cudaStream_t st);
+
+// k1_pipe layout (every |w| == 1, n >= 2 * win).
+cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st);
+
+}  // namespace gdi
