@@ -150,6 +150,29 @@ int gdi_session_launch_count(const gdi_session* s, int32_t* count);
 const char* gdi_session_kernel(const gdi_session* s);
 int gdi_session_destroy(gdi_session* s);
 
+/* Vertex-partitioned anneal of ONE replica across W ranks (one device each;
+ * SURVEY.md §8(e), the 1M-vertex config). Throughput mode only. Rank r owns
+ * the chunks c = r (mod W) of the degree-binned order and keeps a full spin
+ * copy; remote spins are refreshed once per sweep (racy reads, reference
+ * SPEC.md concurrency contract). Per sweep the caller runs, on `stream`:
+ *   gdi_part_sweep(s, k, send)              sweep kernel + pack owned spins
+ *   all-gather of the W send buffers        (e.g. ncclAllGather, same stream)
+ *   gdi_part_finish(s, k, recv)             unpack, counter, barrier
+ * with send = gdi_part_exchange_bytes() bytes and recv = W times that
+ * (rank-major). Trace cuts and the final cut from gdi_part_fetch are this
+ * rank's share (edges [r*m/W, (r+1)*m/W) of the canonical list); the sum over
+ * ranks is the cut. Imbalance, counters and spins are global on every rank.
+ * W == 1 gives the single-device K4 path. */
+typedef struct gdi_part gdi_part;
+int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int32_t rank, uint64_t seed,
+                    void* stream, gdi_part** out);
+int gdi_part_exchange_bytes(const gdi_part* s, int64_t* bytes);
+int gdi_part_init(gdi_part* s);
+int gdi_part_sweep(gdi_part* s, int32_t sweep, void* send);
+int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv);
+int gdi_part_fetch(gdi_part* s, gdi_outputs* out);
+int gdi_part_destroy(gdi_part* s);
+
 /* Measurement utility (not a reference interface): sustained read bandwidth
  * in GB/s of an L2-resident buffer of `bytes` bytes re-read `iters` times on
  * `device`; the roofline denominator for cache-resident graphs. */

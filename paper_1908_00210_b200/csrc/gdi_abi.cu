@@ -385,6 +385,9 @@ int gdi_session_launch(gdi_session* s) {
       a.chains = s->kplan.chains;
       a.world_chains = s->kplan.chains;
       a.chain0 = 0;
+      a.chain_stride = 1;
+      a.rank = 0;
+      a.world = 1;
       a.sweeps = s->p.sweeps;
       a.replicas = s->replicas;
       a.seeds = s->seeds.as<uint64_t>();
@@ -663,6 +666,191 @@ int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas
     scores[r].hamiltonian_scaled = a_num * sum * sum + b_num * cut;
     scores[r].hamiltonian = static_cast<double>(scores[r].hamiltonian_scaled) / static_cast<double>(denom);
     scores[r].balance_counter = sum;
+  }
+  return GDI_OK;
+}
+
+// ---- vertex-partitioned sessions (gdi.h) ------------------------------------
+
+}  // extern "C"
+
+struct gdi_part {
+  gdi_graph* g = nullptr;
+  gdi_params p{};
+  int world = 1, rank = 0;
+  PartPlan plan;
+  PartArgs args{};
+  cudaStream_t stream = nullptr;
+  std::vector<double> pf;
+  std::vector<long long> thr;
+  std::vector<unsigned long long> tmask;
+  DevBuf seeds, thr_d, tmask_d, live, spins, gsum, gdelta, acc, done, finished, bits, trace, stamps, final_out, watchdog;
+  bool inited = false;
+};
+
+extern "C" {
+
+int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int32_t rank, uint64_t seed,
+                    void* stream, gdi_part** out) {
+  if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (!g) return fail(GDI_ERR_CONFIG, "graph is NULL");
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (p->mode != GDI_MODE_THROUGHPUT) return fail(GDI_ERR_CONFIG, "vertex partitioning is a throughput-mode path");
+  if (world < 1 || rank < 0 || rank >= world) return fail(GDI_ERR_CONFIG, "bad world / rank");
+  if ((rc = use_device(g->device))) return rc;
+  auto s = std::make_unique<gdi_part>();
+  s->g = const_cast<gdi_graph*>(g);
+  s->p = *p;
+  s->world = world;
+  s->rank = rank;
+  s->stream = static_cast<cudaStream_t>(stream);
+  // chains per rank as for one replica on one device; chunks per rank shrink by W
+  if (part_plan(g->st, g->wkind, 1, 4 * p->a_num, p->b_num, &s->plan))
+    return fail(GDI_ERR_CAPACITY, "decision arithmetic exceeds the 32-bit kernel bound");
+  const int nck = (g->st.n + 31) / 32;
+  int ctas = s->plan.ctas;
+  const int max_ctas = nck / world / 64;  // >= 4 chunks per chain
+  ctas = ctas < max_ctas ? ctas : max_ctas;
+  s->plan.ctas = ctas < 1 ? 1 : ctas;
+  s->plan.chains = s->plan.ctas * 16;
+  if ((rc = ensure_thru(s->g))) return rc;
+  schedule(s->p, s->pf, s->thr, s->tmask);
+  const size_t n = g->st.n, S = p->sweeps;
+  GDI_CUDA(s->seeds.alloc(sizeof(uint64_t)));
+  GDI_CUDA(s->thr_d.alloc(S * sizeof(long long)));
+  GDI_CUDA(s->tmask_d.alloc(S * sizeof(unsigned long long)));
+  GDI_CUDA(s->live.alloc(part_stride(g->st.n)));
+  GDI_CUDA(s->spins.alloc(n));
+  GDI_CUDA(s->gsum.alloc(sizeof(long long)));
+  GDI_CUDA(s->gdelta.alloc(sizeof(long long)));
+  GDI_CUDA(s->acc.alloc(2 * sizeof(unsigned long long)));
+  GDI_CUDA(s->done.alloc(sizeof(unsigned int)));
+  GDI_CUDA(s->finished.alloc(sizeof(unsigned int)));
+  GDI_CUDA(s->bits.alloc(((n + 31) / 32) * sizeof(uint32_t)));
+  GDI_CUDA(s->trace.alloc(S * sizeof(DevTrace)));
+  GDI_CUDA(s->stamps.alloc((S + 1) * sizeof(unsigned long long)));
+  GDI_CUDA(s->final_out.alloc(sizeof(DevTrace)));
+  GDI_CUDA(s->watchdog.alloc(8 * sizeof(int)));
+  GDI_CUDA(cudaMemcpy(s->seeds.p, &seed, sizeof seed, cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemcpy(s->thr_d.p, s->thr.data(), S * sizeof(long long), cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemcpy(s->tmask_d.p, s->tmask.data(), S * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  GDI_CUDA(cudaMemset(s->watchdog.p, 0, s->watchdog.bytes));
+  PartArgs& a = s->args;
+  a.g = g->csr();
+  a.order = g->thru.order.as<int32_t>();
+  a.sell = g->thru.sell.as<int4>();
+  a.sell_off = g->thru.sell_off.as<int32_t>();
+  a.sell_w = g->thru.sell_w.as<int4>();
+  a.edges = g->thru.edges.as<int2>();
+  a.edge_w = g->thru.edge_w.as<int32_t>();
+  a.e_begin = g->st.m * rank / world;
+  a.e_end = g->st.m * (rank + 1) / world;
+  a.chains = s->plan.chains;
+  a.world_chains = s->plan.chains * world;
+  a.chain0 = rank;
+  a.chain_stride = world;
+  a.rank = rank;
+  a.world = world;
+  a.sweeps = p->sweeps;
+  a.replicas = 1;
+  a.seeds = s->seeds.as<uint64_t>();
+  a.thr = s->thr_d.as<long long>();
+  a.tmask = s->tmask_d.as<unsigned long long>();
+  a.spins = s->live.as<int8_t>();
+  a.gsum = s->gsum.as<long long>();
+  a.gdelta = s->gdelta.as<long long>();
+  a.acc = s->acc.as<unsigned long long>();
+  a.done = s->done.as<unsigned int>();
+  a.finished = s->finished.as<unsigned int>();
+  a.bits = s->bits.as<uint32_t>();
+  a.trace = s->trace.as<DevTrace>();
+  a.stamps = s->stamps.as<unsigned long long>();
+  a.final_out = s->final_out.as<DevTrace>();
+  a.watchdog = s->watchdog.as<int>();
+  *out = s.release();
+  return GDI_OK;
+}
+
+int gdi_part_exchange_bytes(const gdi_part* s, int64_t* bytes) {
+  if (!s || !bytes) return fail(GDI_ERR_CONFIG, "NULL argument");
+  *bytes = part_exchange_bytes(s->g->st.n, s->world);
+  return GDI_OK;
+}
+
+int gdi_part_init(gdi_part* s) {
+  if (!s) return fail(GDI_ERR_CONFIG, "NULL argument");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(part_init_launch(s->plan, s->args, s->stream));
+  s->inited = true;
+  return GDI_OK;
+}
+
+int gdi_part_sweep(gdi_part* s, int32_t sweep, void* send) {
+  if (!s || !send) return fail(GDI_ERR_CONFIG, "NULL argument");
+  if (!s->inited) return fail(GDI_ERR_CONFIG, "gdi_part_init not called");
+  if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(part_sweep_launch(s->plan, s->args, sweep, s->stream));
+  GDI_CUDA(part_xpack_launch(s->plan, s->args, send, s->stream));
+  return GDI_OK;
+}
+
+int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv) {
+  if (!s || !recv) return fail(GDI_ERR_CONFIG, "NULL argument");
+  if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(part_xunpack_launch(s->plan, s->args, recv, part_exchange_bytes(s->g->st.n, s->world), sweep, s->stream));
+  GDI_CUDA(part_barrier_launch(s->plan, s->args, sweep, s->spins.as<int8_t>(), s->stream));
+  return GDI_OK;
+}
+
+int gdi_part_fetch(gdi_part* s, gdi_outputs* out) {
+  if (!s || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(cudaStreamSynchronize(s->stream));
+  int w = 0;
+  GDI_CUDA(cudaMemcpy(&w, s->watchdog.p, sizeof w, cudaMemcpyDeviceToHost));
+  if (w != 0) return fail(GDI_ERR_RUNTIME, "k4 watchdog fired");
+  const size_t n = s->g->st.n, S = s->p.sweeps;
+  const long long A = s->p.a_num, B = s->p.b_num;
+  const double denom = static_cast<double>(s->p.denom);
+  if (out->spins) GDI_CUDA(cudaMemcpy(out->spins, s->spins.p, n, cudaMemcpyDeviceToHost));
+  std::vector<DevTrace> tr(S);
+  std::vector<unsigned long long> st(S + 1);
+  GDI_CUDA(cudaMemcpy(tr.data(), s->trace.p, S * sizeof(DevTrace), cudaMemcpyDeviceToHost));
+  GDI_CUDA(cudaMemcpy(st.data(), s->stamps.p, (S + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  out->seconds = static_cast<double>(st[S] - st[0]) * 1e-9;
+  if (out->scores) {
+    const DevTrace& f = tr[S - 1];
+    gdi_score& sc = out->scores[0];
+    sc.cut = f.cut;  // this rank's share
+    sc.imbalance = f.sum < 0 ? -f.sum : f.sum;
+    sc.hamiltonian_scaled = A * f.sum * f.sum + B * f.cut;
+    sc.hamiltonian = static_cast<double>(sc.hamiltonian_scaled) / denom;
+    sc.balance_counter = f.counter;
+  }
+  for (size_t k = 0; k < S; k++) {
+    if (out->counters) out->counters[k] = tr[k].counter;
+    if (out->trace) {
+      gdi_trace_rec& t = out->trace[k];
+      t.cut = tr[k].cut;
+      t.imbalance = tr[k].sum < 0 ? -tr[k].sum : tr[k].sum;
+      t.hamiltonian_scaled = A * tr[k].sum * tr[k].sum + B * tr[k].cut;
+      t.hamiltonian = static_cast<double>(t.hamiltonian_scaled) / denom;
+      t.flip_probability = s->pf[k];
+      t.seconds = static_cast<double>(st[k + 1] - st[k]) * 1e-9;
+    }
+  }
+  return GDI_OK;
+}
+
+int gdi_part_destroy(gdi_part* s) {
+  if (s) {
+    cudaSetDevice(s->g->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    delete s;
   }
   return GDI_OK;
 }

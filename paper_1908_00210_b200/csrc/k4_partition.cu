@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
   __shared__ ChunkIn stage[kTailMax][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
-  const int J = a.chain0 + blockIdx.x * kNW + warp, P = a.world_chains;
+  const int J = a.chain0 + (blockIdx.x * kNW + warp) * a.chain_stride, P = a.world_chains;
   const int n = a.g.n, nck = (n + 31) >> 5, T = (a.debug & 4) ? 0 : a.tail, nmain = nck - T;
   const int K = J < nmain ? (nmain - J + P - 1) / P : 0;
   int8_t* s = a.spins + static_cast<size_t>(r) * ns;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
     if (cta_delta != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(a.gdelta + r), static_cast<unsigned long long>(cta_delta));
     last = 0;
-    if (T > 0) {
+    if (T > 0 && a.tail_ticket) {
       __threadfence();
       last = atomicAdd(a.finished + r, 1u) == gridDim.x - 1;
       if (last) {
@@ -350,6 +350,80 @@ __global__ void __launch_bounds__(kCutBlock) k4_cut(const PartArgs a) {
   a.done[r] = 0u;
 }
 
+// Vertex-partition exchange (rank r of W ranks owns chunks c = r (mod W)).
+// Send buffer: [int64 counter delta of this sweep][uint32 word i = spins of
+// chunk r + i*W, bit l = lane l's vertex is +1]. Every rank receives all W
+// buffers (stride bytes apart), rewrites the other ranks' vertices in its own
+// spin copy and sets the sweep's total delta for the barrier.
+__global__ void __launch_bounds__(256) k4_xpack(const PartArgs a, int ns, unsigned char* send) {
+  const int n = a.g.n, nck = (n + 31) >> 5, W = a.world, rk = a.rank;
+  const int lane = threadIdx.x & 31;
+  const int8_t* s = a.spins;
+  uint32_t* words = reinterpret_cast<uint32_t*>(send + 8);
+  const int nmain = nck - a.tail;  // tail chunks are recomputed identically on every rank
+  const int nw = nmain > rk ? (nmain - rk + W - 1) / W : 0;
+  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < nw; i += gridDim.x * 8) {
+    const int idx = (rk + i * W) * 32 + lane;
+    const int8_t x = idx < n ? __ldcg(s + __ldg(a.order + idx)) : static_cast<int8_t>(-1);
+    const unsigned b = __ballot_sync(0xffffffffu, x > 0);
+    if (lane == 0) words[i] = b;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<long long*>(send) = a.gdelta[0];
+}
+
+__global__ void __launch_bounds__(256) k4_xunpack(const PartArgs a, int ns, const unsigned char* recv,
+                                                  long long stride) {
+  const int n = a.g.n, nck = (n + 31) >> 5, W = a.world, rk = a.rank;
+  const int lane = threadIdx.x & 31;
+  int8_t* s = a.spins;
+  const int nmain = nck - a.tail;
+  for (int c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nmain; c += gridDim.x * 8) {
+    const int q = c % W;
+    if (q == rk) continue;
+    const uint32_t w = reinterpret_cast<const uint32_t*>(recv + q * stride + 8)[c / W];
+    const int idx = c * 32 + lane;
+    if (idx < n) s[__ldg(a.order + idx)] = ((w >> lane) & 1u) ? 1 : -1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long d = 0;
+    for (int q = 0; q < W; q++) d += *reinterpret_cast<const long long*>(recv + q * stride);
+    a.gdelta[0] = d;  // the barrier folds it into the counter
+  }
+}
+
+// Global tail for ranks > 1: after the exchange every rank holds the same
+// spins and the exact counter, so each runs the tail chunks itself (same
+// gathers, same Philox draws, one warp deciding in order) and the ranks stay
+// identical without a second exchange.
+template <int WK, int KMAX>
+__global__ void __launch_bounds__(32 * kNW) k4_gtail(const PartArgs a, int ns) {
+  __shared__ ChunkIn stage[kTailMax][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = a.g.n, nck = (n + 31) >> 5, T = a.tail, nmain = nck - T;
+  const int r = blockIdx.y, sweep = a.sweep;
+  int8_t* s = a.spins + static_cast<size_t>(r) * ns;
+  const uint64_t seed = a.seeds[r];
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  const unsigned long long tm = a.tmask[sweep];
+  const bool en = a.thr[sweep] >= 0;
+  for (int t = warp; t < T; t += kNW) stage[t][lane] = gather<WK, KMAX>(a, s, nmain + t, sweep, k0, k1, tm, en, lane);
+  __syncthreads();
+  if (warp != 0) return;
+  const int g0 = static_cast<int>(a.gsum[r] + a.gdelta[r]);
+  int Gt = g0;
+  for (int t = 0; t < T; t++) decide_chunk(stage[t][lane], Gt, s, a.a4, a.b, lane);
+  if (lane == 0) a.gdelta[r] += Gt - g0;
+}
+
+template <int WK>
+const void* gtail_fn(int kmax) {
+  switch (kmax) {
+    case 1: return reinterpret_cast<const void*>(&k4_gtail<WK, 1>);
+    case 2: return reinterpret_cast<const void*>(&k4_gtail<WK, 2>);
+    default: return reinterpret_cast<const void*>(&k4_gtail<WK, 4>);
+  }
+}
+
 template <int WK>
 const void* sweep_fn(int kmax) {
   switch (kmax) {
@@ -389,6 +463,7 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   // tail chunks run by the last CTA against the exact counter (see k4_sweep)
   plan->tail = nck / 8 < kTailMax ? nck / 8 : kTailMax;
   plan->sweep_fn = wkind == 0 ? sweep_fn<0>(kmax) : wkind == 1 ? sweep_fn<1>(kmax) : sweep_fn<2>(kmax);
+  plan->gtail_fn = wkind == 0 ? gtail_fn<0>(kmax) : wkind == 1 ? gtail_fn<1>(kmax) : gtail_fn<2>(kmax);
   plan->cut_fn = wkind == 0   ? reinterpret_cast<const void*>(&k4_cut<0>)
                  : wkind == 1 ? reinterpret_cast<const void*>(&k4_cut<1>)
                               : reinterpret_cast<const void*>(&k4_cut<2>);
@@ -407,14 +482,24 @@ int part_launch_count(const PartPlan&, int32_t sweeps) { return 1 + 3 * sweeps; 
 
 int part_stride(int n) { return (n + 1 + 15) & ~15; }
 
-cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream) {
+namespace {
+
+PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   PartArgs a = args;
   a.a4 = plan.a4;
   a.b = plan.b;
-  a.tail = a.chains == a.world_chains ? plan.tail : 0;  // single device only
+  a.tail = plan.tail;
+  a.tail_ticket = a.world == 1 ? 1 : 0;  // ranks > 1: k4_gtail after the exchange
   const char* dbg = std::getenv("GDI_K4_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
-  int ns = part_stride(a.g.n);
+  return a;
+}
+
+}  // namespace
+
+cudaError_t part_init_launch(const PartPlan& plan, const PartArgs& args, cudaStream_t stream) {
+  PartArgs a = prepared(plan, args);
+  const int ns = part_stride(a.g.n);
   const int R = a.replicas;
   cudaError_t err;
   if ((err = cudaMemsetAsync(a.gsum, 0, R * sizeof(long long), stream))) return err;
@@ -423,15 +508,64 @@ cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spin
   if ((err = cudaMemsetAsync(a.done, 0, R * sizeof(unsigned int), stream))) return err;
   if ((err = cudaMemsetAsync(a.finished, 0, R * sizeof(unsigned int), stream))) return err;
   k4_init<<<dim3((ns + 255) / 256, R), 256, 0, stream>>>(a, ns);
-  if ((err = cudaGetLastError())) return err;
-  for (int sw = 0; sw < a.sweeps; sw++) {
-    a.sweep = sw;
-    void* p1[] = {&a, &ns};
-    if ((err = cudaLaunchKernel(plan.sweep_fn, dim3(plan.ctas, R), dim3(plan.block), p1, 0, stream))) return err;
-    k4_pack<<<dim3(plan.pack_grid, R), kPackBlock, 0, stream>>>(a, ns, spins_out);
-    if ((err = cudaGetLastError())) return err;
-    void* p3[] = {&a};
-    if ((err = cudaLaunchKernel(plan.cut_fn, dim3(plan.cut_grid, R), dim3(kCutBlock), p3, 0, stream))) return err;
+  return cudaGetLastError();
+}
+
+cudaError_t part_sweep_launch(const PartPlan& plan, const PartArgs& args, int sweep, cudaStream_t stream) {
+  PartArgs a = prepared(plan, args);
+  a.sweep = sweep;
+  int ns = part_stride(a.g.n);
+  void* p1[] = {&a, &ns};
+  return cudaLaunchKernel(plan.sweep_fn, dim3(plan.ctas, a.replicas), dim3(plan.block), p1, 0, stream);
+}
+
+cudaError_t part_barrier_launch(const PartPlan& plan, const PartArgs& args, int sweep, int8_t* spins_out,
+                                cudaStream_t stream) {
+  PartArgs a = prepared(plan, args);
+  a.sweep = sweep;
+  const int ns = part_stride(a.g.n);
+  k4_pack<<<dim3(plan.pack_grid, a.replicas), kPackBlock, 0, stream>>>(a, ns, spins_out);
+  cudaError_t err = cudaGetLastError();
+  if (err) return err;
+  void* p3[] = {&a};
+  return cudaLaunchKernel(plan.cut_fn, dim3(plan.cut_grid, a.replicas), dim3(kCutBlock), p3, 0, stream);
+}
+
+cudaError_t part_xpack_launch(const PartPlan& plan, const PartArgs& args, void* send, cudaStream_t stream) {
+  PartArgs a = prepared(plan, args);
+  const int nck = (a.g.n + 31) / 32;
+  const int nw = (nck - a.rank + a.world - 1) / a.world;
+  k4_xpack<<<(nw + 7) / 8 > 0 ? ((nw + 7) / 8 < 1184 ? (nw + 7) / 8 : 1184) : 1, 256, 0, stream>>>(
+      a, part_stride(a.g.n), static_cast<unsigned char*>(send));
+  return cudaGetLastError();
+}
+
+cudaError_t part_xunpack_launch(const PartPlan& plan, const PartArgs& args, const void* recv, long long stride,
+                                int sweep, cudaStream_t stream) {
+  PartArgs a = prepared(plan, args);
+  a.sweep = sweep;
+  int ns = part_stride(a.g.n);
+  const int nck = (a.g.n + 31) / 32;
+  k4_xunpack<<<(nck + 7) / 8 < 1184 ? (nck + 7) / 8 : 1184, 256, 0, stream>>>(
+      a, ns, static_cast<const unsigned char*>(recv), stride);
+  cudaError_t err = cudaGetLastError();
+  if (err || a.tail == 0 || a.tail_ticket) return err;
+  void* p[] = {&a, &ns};
+  return cudaLaunchKernel(plan.gtail_fn, dim3(1, a.replicas), dim3(plan.block), p, 0, stream);
+}
+
+long long part_exchange_bytes(int n, int world) {
+  const int nck = (n + 31) / 32;
+  const long long words = (nck + world - 1) / world;  // rank 0 owns the most
+  return (8 + 4 * words + 15) & ~15LL;
+}
+
+cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream) {
+  cudaError_t err = part_init_launch(plan, args, stream);
+  if (err) return err;
+  for (int sw = 0; sw < args.sweeps; sw++) {
+    if ((err = part_sweep_launch(plan, args, sw, stream))) return err;
+    if ((err = part_barrier_launch(plan, args, sw, spins_out, stream))) return err;
   }
   return cudaSuccess;
 }

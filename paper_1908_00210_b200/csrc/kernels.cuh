@@ -101,8 +101,10 @@ struct ThruArgs {
 
 // k4 (vertex-partitioned throughput sweep for large graphs): the chunks of
 // the SELL order are dealt round-robin to `world_chains` chains (chain J owns
-// chunks J, J + world_chains, ...); this device runs chains chain0 ..
-// chain0 + gridDim.x - 1. Spins live in global memory ([R][n], L2-resident).
+// chunks J, J + world_chains, ...); this device runs the chains
+// chain0 + i * chain_stride (i = warp index in the grid): one device has
+// chain0 = 0, stride 1; rank r of W ranks has chain0 = r, stride W, so it owns
+// the chunks c = r (mod W). Spins live in global memory ([R][n], L2-resident).
 struct PartArgs {
   DevCsr g;
   const int32_t* order;
@@ -113,7 +115,8 @@ struct PartArgs {
   const int32_t* edge_w;
   int64_t e_begin, e_end;
   int32_t chains;                  // chains per replica on this device
-  int32_t world_chains, chain0;
+  int32_t world_chains, chain0, chain_stride;
+  int32_t rank, world;              // vertex partition (1 device: 0, 1)
   int32_t sweeps;
   int32_t replicas;
   int32_t sweep;                   // set per launch
@@ -128,7 +131,8 @@ struct PartArgs {
   unsigned int* done;              // [R] barrier blocks finished
   unsigned int* finished;          // [R] CTAs finished (tail ticket)
   uint32_t* bits;                  // [R][ceil(n/32)] packed spins at the barrier
-  int32_t tail;                    // chunks run by the last chain against the exact counter
+  int32_t tail;                    // last chunks of the order, decided against the exact counter
+  int32_t tail_ticket;             // 1: by the last CTA of k4_sweep (one device); 0: k4_gtail on every rank
   int32_t debug;                   // timing experiments only (GDI_K4_DEBUG); 0 in production
   DevTrace* trace;
   unsigned long long* stamps;

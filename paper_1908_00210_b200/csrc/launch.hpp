@@ -72,6 +72,7 @@ cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t
 struct PartPlan {
   const void* sweep_fn = nullptr;
   const void* cut_fn = nullptr;
+  const void* gtail_fn = nullptr;  // ranks > 1: global tail after the exchange
   int32_t a4 = 4, b = 4;
   int ctas = 1;        // per replica
   int chains = 16;     // per replica (one per warp)
@@ -84,6 +85,16 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
 // Enqueues init + sweeps x (sweep, pack, cut) kernels: 1 + 3 * sweeps launches.
 // spins_out [R][n] receives the final spins (the live array has stride part_stride(n)).
 cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream);
+// The same sequence in pieces, for the vertex-partitioned multi-rank driver:
+// init; per sweep: sweep, xpack (send), [caller all-gathers], xunpack (recv), barrier.
+cudaError_t part_init_launch(const PartPlan& plan, const PartArgs& args, cudaStream_t stream);
+cudaError_t part_sweep_launch(const PartPlan& plan, const PartArgs& args, int sweep, cudaStream_t stream);
+cudaError_t part_barrier_launch(const PartPlan& plan, const PartArgs& args, int sweep, int8_t* spins_out,
+                                cudaStream_t stream);
+cudaError_t part_xpack_launch(const PartPlan& plan, const PartArgs& args, void* send, cudaStream_t stream);
+cudaError_t part_xunpack_launch(const PartPlan& plan, const PartArgs& args, const void* recv, long long stride,
+                                int sweep, cudaStream_t stream);
+long long part_exchange_bytes(int n, int world);  // per-rank send buffer bytes (16-aligned)
 int part_launch_count(const PartPlan& plan, int32_t sweeps);
 int part_stride(int n);
 

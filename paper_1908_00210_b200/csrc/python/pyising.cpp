@@ -171,6 +171,88 @@ std::vector<Edge> edges_from(const py::iterable& it) {
 
 } // namespace
 
+// One rank of a vertex-partitioned anneal (gdi_part_*): the caller moves the
+// exchange buffers between ranks (NCCL all-gather, or copies when emulating
+// the ranks on one device); buffers are passed as device addresses.
+class PartSession {
+public:
+  PartSession(const MinCutProblem& problem, const AnnealParams& params_in, int world, int rank, std::uint64_t seed,
+              std::uintptr_t stream, int dev)
+      : n_(problem.graph().num_nodes()) {
+    const AnnealParams params = params_in.validated();
+    const Graph& g = problem.graph();
+    std::vector<std::int32_t> nbr, w;
+    for (const Neighbor& nb : g.csr_adjacency()) {
+      nbr.push_back(nb.node);
+      w.push_back(nb.weight);
+    }
+    check_abi(gdi_graph_create(dev, n_, g.csr_offsets().data(), nbr.data(), g.all_unit_weights() ? nullptr : w.data(),
+                               &graph_));
+    gdi_params q{};
+    q.sweeps = params.sweeps;
+    q.strategy = params.strategy == Strategy::standard ? GDI_STRATEGY_STANDARD : GDI_STRATEGY_GDI;
+    q.mode = GDI_MODE_THROUGHPUT;
+    q.flip_fraction0 = params.flip_fraction0;
+    q.decay_rate = params.decay_rate;
+    q.a_num = problem.coefficients().a_num;
+    q.b_num = problem.coefficients().b_num;
+    q.denom = problem.coefficients().denom;
+    sweeps_ = q.sweeps;
+    check_abi(gdi_part_create(graph_, &q, world, rank, seed, reinterpret_cast<void*>(stream), &sess_));
+  }
+  ~PartSession() {
+    if (sess_) gdi_part_destroy(sess_);
+    if (graph_) gdi_graph_destroy(graph_);
+  }
+  std::int64_t exchange_bytes() const {
+    std::int64_t b = 0;
+    check_abi(gdi_part_exchange_bytes(sess_, &b));
+    return b;
+  }
+  void init() { check_abi(gdi_part_init(sess_)); }
+  void sweep(int k, std::uintptr_t send) { check_abi(gdi_part_sweep(sess_, k, reinterpret_cast<void*>(send))); }
+  void finish(int k, std::uintptr_t recv) {
+    check_abi(gdi_part_finish(sess_, k, reinterpret_cast<const void*>(recv)));
+  }
+  py::dict fetch() {
+    const std::size_t n = n_, S = sweeps_;
+    std::vector<std::int8_t> sp(n);
+    std::vector<gdi_score> sc(1);
+    std::vector<gdi_trace_rec> tr(S);
+    std::vector<std::int64_t> ctr(S);
+    gdi_outputs out{};
+    out.spins = sp.data();
+    out.scores = sc.data();
+    out.trace = tr.data();
+    out.counters = ctr.data();
+    {
+      py::gil_scoped_release nogil;
+      check_abi(gdi_part_fetch(sess_, &out));
+    }
+    std::vector<std::int64_t> tcut(S), timb(S);
+    for (std::size_t k = 0; k < S; k++) {
+      tcut[k] = tr[k].cut;
+      timb[k] = tr[k].imbalance;
+    }
+    py::dict d;
+    d["spins"] = to_numpy(std::move(sp), {static_cast<py::ssize_t>(n)});
+    d["cut_part"] = sc[0].cut;
+    d["imbalance"] = sc[0].imbalance;
+    d["balance_counter"] = sc[0].balance_counter;
+    d["trace_cut_part"] = to_numpy(std::move(tcut), {static_cast<py::ssize_t>(S)});
+    d["trace_imbalance"] = to_numpy(std::move(timb), {static_cast<py::ssize_t>(S)});
+    d["counters"] = to_numpy(std::move(ctr), {static_cast<py::ssize_t>(S)});
+    d["seconds"] = out.seconds;
+    return d;
+  }
+
+private:
+  gdi_graph* graph_ = nullptr;
+  gdi_part* sess_ = nullptr;
+  std::int32_t n_ = 0;
+  int sweeps_ = 0;
+};
+
 PYBIND11_MODULE(pyising, m) {
   m.doc() = "gdi-b200: GDI Ising annealing for balanced min-cut on NVIDIA B200 (sm_100a)";
 
@@ -460,6 +542,17 @@ PYBIND11_MODULE(pyising, m) {
       .def("fetch", &Session::fetch, py::arg("spins") = true, py::arg("trace") = false)
       .def_property_readonly("launch_count", &Session::launch_count)
       .def_property_readonly("kernel", &Session::kernel);
+
+  py::class_<PartSession>(m, "PartSession",
+                          "One rank of a vertex-partitioned throughput-mode anneal (C ABI gdi_part_*).")
+      .def(py::init<const MinCutProblem&, const AnnealParams&, int, int, std::uint64_t, std::uintptr_t, int>(),
+           py::arg("problem"), py::arg("params"), py::arg("world"), py::arg("rank"), py::arg("seed"),
+           py::arg("stream") = 0, py::arg("device") = 0)
+      .def_property_readonly("exchange_bytes", &PartSession::exchange_bytes)
+      .def("init", &PartSession::init)
+      .def("sweep", &PartSession::sweep, py::arg("k"), py::arg("send"))
+      .def("finish", &PartSession::finish, py::arg("k"), py::arg("recv"))
+      .def("fetch", &PartSession::fetch);
 
   m.def(
       "probe_l2_bandwidth",
