@@ -89,13 +89,14 @@ struct gdi_session {
   ThruPlan tplan;
   PartPlan kplan;
   bool use_pipe = false;
+  bool use_win = false;  // the pipe plan is a k1_window plan
   bool use_thru = false;
   bool use_part = false;
   cudaGraphExec_t part_exec = nullptr;  // k4: 1 + 3M launches replayed as one graph
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
-  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords;
+  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords, gspins;
   DevBuf live, gsum, gdelta, acc, done, finished, bits;  // k4 state
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
@@ -308,8 +309,19 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   else if (thru_ok && force != "part" &&
            thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
     s->use_thru = true;
-  const bool pipe_ok = !s->use_thru && force != "exact" &&
-                       pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
+  // exact mode: k1_window (speculative visit windows) by default; k1_pipe on
+  // request (GDI_FORCE_KERNEL=pipe|pipe_gmem); k1_exact for everything else
+  const bool want_pipe = force == "pipe" || force == "pipe_gmem";
+  bool pipe_ok = false;
+  if (!s->use_thru && force != "exact" && !want_pipe &&
+      window_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0) {
+    pipe_ok = true;
+    s->use_win = true;
+  } else if (!s->use_thru && force != "exact" && force != "window" && force != "window_gmem") {
+    pipe_ok = pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
+  }
+  if ((force == "window" || force == "window_gmem") && !s->use_win)
+    return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=window but k1_window does not apply");
   if ((force == "pipe" || force == "pipe_gmem") && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
   s->use_pipe = pipe_ok;
   if (!s->use_thru && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
@@ -334,8 +346,10 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   GDI_CUDA(s->final_out.alloc(R * sizeof(DevTrace)));
   GDI_CUDA(s->watchdog.alloc(8 * sizeof(int)));
   GDI_CUDA(s->prof.alloc(16 * sizeof(unsigned long long)));
-  if (s->use_pipe && s->pplan.gw)
+  if (s->use_pipe && s->pplan.gw && !s->use_win)
     GDI_CUDA(s->gwords.alloc(static_cast<size_t>(s->pplan.grid) * g->pipe.n_words * sizeof(uint32_t)));
+  if (s->use_win && s->pplan.gw)
+    GDI_CUDA(s->gspins.alloc(static_cast<size_t>(replicas) * s->pplan.n_words));
   if (p->flags & GDI_FLAG_TRACE) {
     GDI_CUDA(s->trace.alloc(R * S * sizeof(DevTrace)));
     GDI_CUDA(s->stamps.alloc(R * (S + 1) * sizeof(unsigned long long)));
@@ -459,7 +473,8 @@ int gdi_session_launch(gdi_session* s) {
     a.win_pos = s->g->pipe.win_pos;
     a.win_neg = s->g->pipe.win_neg;
     a.n_words = s->g->pipe.n_words;
-    a.gwords = s->pplan.gw ? s->gwords.as<uint32_t>() : nullptr;
+    a.gwords = s->pplan.gw && !s->use_win ? s->gwords.as<uint32_t>() : nullptr;
+    a.gspins = s->use_win && s->pplan.gw ? s->gspins.as<int8_t>() : nullptr;
     a.sweeps = s->p.sweeps;
     a.replicas = s->replicas;
     a.seeds = s->seeds.as<uint64_t>();
@@ -477,7 +492,7 @@ int gdi_session_launch(gdi_session* s) {
     GDI_CUDA(cudaMemsetAsync(s->watchdog.p, 0, s->watchdog.bytes, s->stream));
     if (s->pplan.prof) GDI_CUDA(cudaMemsetAsync(s->prof.p, 0, s->prof.bytes, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
-    GDI_CUDA(pipe_launch(s->pplan, a, s->stream));
+    GDI_CUDA(s->use_win ? window_launch(s->pplan, a, s->stream) : pipe_launch(s->pplan, a, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
     s->launched = true;
     return GDI_OK;
@@ -519,7 +534,7 @@ static int check_watchdog(gdi_session* s) {
     return GDI_OK;
   }
   if (!s->use_pipe) return GDI_OK;
-  if (s->pplan.prof) {
+  if (s->pplan.prof && !s->use_win) {
     unsigned long long c[16] = {0};
     GDI_CUDA(cudaMemcpy(c, s->prof.p, sizeof c, cudaMemcpyDeviceToHost));
     const double nb = c[4] ? static_cast<double>(c[4]) : 1.0;

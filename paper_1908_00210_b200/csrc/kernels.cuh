@@ -54,6 +54,7 @@ struct PipeArgs {
   const uint32_t* win_neg;
   int32_t n_words;                 // spin words per CTA (>= n + 1)
   uint32_t* gwords;                // [grid][n_words] global spin words, or nullptr (shared memory)
+  int8_t* gspins;                  // k1_window: [R][n_words] global int8 spins, or nullptr (shared memory)
   int32_t sweeps;
   int32_t replicas;
   int32_t rc;                      // replicas (lanes) per CTA

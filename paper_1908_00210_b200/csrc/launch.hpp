@@ -51,6 +51,7 @@ struct PipePlan {
   int smem = 0;
   bool prof = false;
   bool gw = false;  // spin words in global memory (graph too large for shared memory)
+  int n_words = 0;  // k1_window: per-replica spin stride
   const char* name = "";
 };
 
@@ -59,6 +60,10 @@ size_t pipe_smem_bytes(int n_words, int nwarps);
 int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b,
               int32_t sweeps, PipePlan* plan);
 cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);
+// k1_window (speculative visit windows; same eligibility as k1_pipe)
+int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b,
+                int32_t sweeps, PipePlan* plan);
+cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);
 
 struct ThruPlan {
   const void* fn = nullptr;

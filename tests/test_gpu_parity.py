@@ -173,7 +173,7 @@ def test_session_device_resident_matches_batch(kernel_variant):
     assert np.array_equal(got["spins"], ref["spins"])
     assert np.array_equal(got["trace"], ref["trace"])
     assert s.launch_count >= 1 and s.kernel
-    assert ("pipe" in s.kernel) == (kernel_variant == "auto")
+    assert ("window" in s.kernel) == (kernel_variant == "auto")
 
 
 def test_pipe_window_edge_cases_match_oracle():
@@ -202,14 +202,18 @@ def test_pipe_window_edge_cases_match_oracle():
 # fit in shared memory, e.g. the 1M-vertex config (BASELINE configs[4])
 
 
+@pytest.mark.parametrize("variant", ["pipe", "pipe_gmem", "window_gmem"])
 @pytest.mark.parametrize("name,count", [("G1", 16), ("G22", 256), ("G81pm1", 16)])
-def test_gmem_pipe_variant_bit_exact(name, count, kernel_variant, monkeypatch):
+def test_forced_exact_variants_bit_exact(name, count, variant, kernel_variant, monkeypatch):
+    """The other exact kernels on the golden configs: k1_pipe (warp-specialised),
+    its global-memory spin words, and k1_window with global-memory spins."""
     if kernel_variant != "auto":
-        pytest.skip("one forced variant is enough")
-    monkeypatch.setenv("GDI_FORCE_KERNEL", "pipe_gmem")
+        pytest.skip("one forced variant per case")
+    monkeypatch.setenv("GDI_FORCE_KERNEL", variant)
     s = pi.Session(pi.MinCutProblem.with_default_coefficients(product_graph(golden_configs()[name]["recipe"])),
                    det_params(), 1)
-    assert s.kernel.endswith("gmem>"), s.kernel
+    assert ("gmem" in s.kernel) == variant.endswith("gmem"), s.kernel
+    assert s.kernel.startswith("k1_" + variant.split("_")[0]), s.kernel
     check_batch_against_golden(name, count=count)
 
 
