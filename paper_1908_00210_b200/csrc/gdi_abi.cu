@@ -74,7 +74,7 @@ struct gdi_graph {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
                                 thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes +
                                 pipel.far_col.bytes + pipel.far_meta.bytes + pipel.win_pos.bytes +
-                                pipel.win_neg.bytes);
+                                pipel.win_neg.bytes + pipel.wsell.bytes + pipel.wsell_off.bytes);
   }
 };
 
@@ -174,6 +174,8 @@ int ensure_pipe(gdi_graph* g) {
   g->pipe.far_meta = g->pipel.far_meta.as<int4>();
   g->pipe.win_pos = g->pipel.win_pos.as<uint32_t>();
   g->pipe.win_neg = g->pipel.win_neg.as<uint32_t>();
+  g->pipe.wsell = g->pipel.wsell.as<int32_t>();
+  g->pipe.wsell_off = g->pipel.wsell_off.as<int32_t>();
   g->pipe_built = true;
   return GDI_OK;
 }
@@ -317,10 +319,10 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
       window_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0) {
     pipe_ok = true;
     s->use_win = true;
-  } else if (!s->use_thru && force != "exact" && force != "window" && force != "window_gmem") {
+  } else if (!s->use_thru && force != "exact" && force.rfind("window", 0) != 0) {
     pipe_ok = pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
   }
-  if ((force == "window" || force == "window_gmem") && !s->use_win)
+  if (force.rfind("window", 0) == 0 && !s->use_win)
     return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=window but k1_window does not apply");
   if ((force == "pipe" || force == "pipe_gmem") && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
   s->use_pipe = pipe_ok;
@@ -472,6 +474,8 @@ int gdi_session_launch(gdi_session* s) {
     a.far_meta = s->g->pipe.far_meta;
     a.win_pos = s->g->pipe.win_pos;
     a.win_neg = s->g->pipe.win_neg;
+    a.wsell = s->g->pipe.wsell;
+    a.wsell_off = s->g->pipe.wsell_off;
     a.n_words = s->g->pipe.n_words;
     a.gwords = s->pplan.gw && !s->use_win ? s->gwords.as<uint32_t>() : nullptr;
     a.gspins = s->use_win && s->pplan.gw ? s->gspins.as<int8_t>() : nullptr;
@@ -490,7 +494,7 @@ int gdi_session_launch(gdi_session* s) {
     a.watchdog = s->watchdog.as<int>();
     a.prof = s->prof.as<unsigned long long>();
     GDI_CUDA(cudaMemsetAsync(s->watchdog.p, 0, s->watchdog.bytes, s->stream));
-    if (s->pplan.prof) GDI_CUDA(cudaMemsetAsync(s->prof.p, 0, s->prof.bytes, s->stream));
+    GDI_CUDA(cudaMemsetAsync(s->prof.p, 0, s->prof.bytes, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
     GDI_CUDA(s->use_win ? window_launch(s->pplan, a, s->stream) : pipe_launch(s->pplan, a, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
@@ -534,6 +538,13 @@ static int check_watchdog(gdi_session* s) {
     return GDI_OK;
   }
   if (!s->use_pipe) return GDI_OK;
+  if (s->use_win && std::getenv("GDI_PIPE_DEBUG") && (std::atoi(std::getenv("GDI_PIPE_DEBUG")) & 4)) {
+    unsigned long long c[16] = {0};
+    GDI_CUDA(cudaMemcpy(c, s->prof.p, sizeof c, cudaMemcpyDeviceToHost));
+    const double st = c[0] ? static_cast<double>(c[0]) : 1.0;
+    std::fprintf(stderr, "[k1_window prof] steps %llu, visits/step %.2f, cycles/step %.0f (refill %.0f, draw wait %.0f)\n",
+                 c[0], c[1] / st, c[3] / st, c[2] / st, c[4] / st);
+  }
   if (s->pplan.prof && !s->use_win) {
     unsigned long long c[16] = {0};
     GDI_CUDA(cudaMemcpy(c, s->prof.p, sizeof c, cudaMemcpyDeviceToHost));

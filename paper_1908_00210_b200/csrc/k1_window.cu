@@ -48,7 +48,7 @@ namespace gdi {
 namespace {
 
 constexpr int kRing = 128;  // draws buffered per replica (power of two, >= 2 * 34)
-constexpr long long kWatchdog = 1LL << 26;
+constexpr long long kWatchdog = 1LL << 28;  // polling iterations before aborting (~seconds)
 
 __device__ __forceinline__ unsigned saddr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -62,53 +62,43 @@ __device__ __forceinline__ void st_release(unsigned a, int v) {
   asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Field of one row: index loads issued 8 (then 4) at a time before the spin
-// loads, so a row costs a few L1 + shared-memory round trips, not one per entry.
+// spin of SELL entry idx (bit 31 = weight -1; padding index n reads 0)
 template <bool SIGNED>
-__device__ __forceinline__ int row_field(const int8_t* s, const int32_t* __restrict__ col,
-                                         const int32_t* __restrict__ wgt, int e, int e1) {
-  int acc = 0;
-  for (; e + 8 <= e1; e += 8) {
-    int u[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) u[k] = __ldg(col + e + k);
-#pragma unroll
-    for (int k = 0; k < 8; k++) acc += SIGNED ? __ldg(wgt + e + k) * s[u[k]] : s[u[k]];
+__device__ __forceinline__ int nbv(const int8_t* s, int idx) {
+  if (SIGNED) {
+    const int v = s[idx & 0x7fffffff];
+    return idx < 0 ? -v : v;
   }
-  if (e + 4 <= e1) {
-    int u[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) u[k] = __ldg(col + e + k);
-#pragma unroll
-    for (int k = 0; k < 4; k++) acc += SIGNED ? __ldg(wgt + e + k) * s[u[k]] : s[u[k]];
-    e += 4;
-  }
-  for (; e < e1; e++) acc += SIGNED ? __ldg(wgt + e) * s[__ldg(col + e)] : s[__ldg(col + e)];
-  return acc;
+  return s[idx];
 }
 
 struct WinLayout {
-  int ring, genpos, cons, flags, spins, total;
-  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs) {
+  int ring, genpos, cons, flags, spins, fields, total;
+  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, bool incf) {
     WinLayout L;
     L.ring = 0;
     L.genpos = L.ring + rc * kRing * 8;
     L.cons = L.genpos + 4 * 32;
     L.flags = L.cons + 4 * 32;  // [0] consumers done, [1] abort
     L.spins = L.flags + 16;
-    L.total = L.spins + (gs ? 0 : rc * n_pad);
+    L.fields = L.spins + (gs ? 0 : rc * n_pad);
+    L.total = L.fields + (incf ? rc * n_pad * 2 : 0);
     return L;
   }
 };
 
-template <bool SIGNED, bool UNITAB, bool GS>
+// INCF: every vertex's field kept exact in shared memory (int16; scattered on
+// each spin change, ~2% of visits) so a window refill is two shared loads
+// instead of a row gather; else rows are gathered from the natural-order
+// SELL layout and pending lanes are corrected through the window masks.
+template <bool SIGNED, bool UNITAB, bool GS, bool INCF>
 __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.g.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rc = a.rc;  // replica warps 0..rc-1, producer warp rc
+  const int rc = a.rc;  // replica warps 0..rc-1, producer warps rc..rc+nprod-1
   const int n_pad = a.n_words;
-  const WinLayout L = WinLayout::make(rc, n_pad, GS);
+  const WinLayout L = WinLayout::make(rc, n_pad, GS, INCF);
   uint64_t* ring = reinterpret_cast<uint64_t*>(smem + L.ring);
   int* genpos = reinterpret_cast<int*>(smem + L.genpos);
   int* cons = reinterpret_cast<int*>(smem + L.cons);
@@ -121,13 +111,17 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   }
   __syncthreads();
 
-  if (warp == rc) {
-    // ============================ producer ============================
-    const int r = blockIdx.x * rc + lane;
-    const bool act = lane < rc && r < a.replicas;
+  if (warp >= rc) {
+    // ============================ producers ============================
+    // producer warp p serves replicas l = p, p + np, ... (lane = l / np): a
+    // stream costs ~25 instructions per draw, so one warp for all replicas
+    // could not keep up with the consumers
+    const int np = a.nprod, l = (warp - rc) + lane * np;
+    const int r = blockIdx.x * rc + l;
+    const bool act = l < rc && r < a.replicas;
     Xoshiro rng = Xoshiro::stream(act ? a.seeds[r] : 0ull, 1);  // anneal.cpp:191
-    uint64_t* my = ring + lane * kRing;
-    const unsigned gp_s = saddr(genpos + lane), cs_s = saddr(cons + lane);
+    uint64_t* my = ring + (act ? l : 0) * kRing;
+    const unsigned gp_s = saddr(genpos + (act ? l : 0)), cs_s = saddr(cons + (act ? l : 0));
     int gen = 0;
 #pragma unroll 1
     for (long long spin = 0;; spin++) {
@@ -139,6 +133,9 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         st_release(gp_s, gen);
       }
       if (!__any_sync(0xffffffffu, can)) {
+        // ring full: a short sleep keeps this warp's polling off the issue
+        // slots the consumers need (measured: spinning, or 4 producer warps,
+        // were both slower than one sleeping producer)
         if (ld_acquire(done_s) >= rc || ld_acquire(abort_s)) break;
         __nanosleep(32);
         if (spin > kWatchdog) {
@@ -159,6 +156,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   }
   const size_t rs = static_cast<size_t>(r);
   int8_t* s = GS ? a.gspins + rs * n_pad : reinterpret_cast<int8_t*>(smem + L.spins) + warp * n_pad;
+  int16_t* fld = reinterpret_cast<int16_t*>(smem + L.fields) + warp * n_pad;  // INCF only
   const int32_t* __restrict__ off = a.g.off;
   const int32_t* __restrict__ col = a.g.col;
   const int32_t* __restrict__ wgt = a.g.w;
@@ -175,6 +173,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       if ((i & 31) == lane) s[i] = static_cast<int8_t>(v);
     }
   }
+  for (int i = n + lane; i < n_pad; i += 32) s[i] = 0;  // padding index n reads spin 0
   __syncwarp();
   // exact initial cut (evaluate.cpp:10-18), lane = vertices u = lane (mod 32)
   long long cut = 0;
@@ -188,6 +187,15 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cut += __shfl_xor_sync(FULL, cut, o);
+  if (INCF) {
+    for (int v = lane; v < n; v += 32) {
+      int acc = 0;
+      const int e1 = __ldg(off + v + 1);
+      for (int e = __ldg(off + v); e < e1; e++) acc += SIGNED ? __ldg(wgt + e) * s[__ldg(col + e)] : s[__ldg(col + e)];
+      fld[v] = static_cast<int16_t>(acc);
+    }
+    __syncwarp();
+  }
   if (a.snaps != nullptr)
     for (int i = lane; i < n; i += 32) a.snaps[rs * (sweeps + 1) * n + i] = s[i];
   if (lane == 0 && a.stamps != nullptr) a.stamps[rs * (sweeps + 1)] = globaltimer_ns();
@@ -204,21 +212,44 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const unsigned gp_s = saddr(genpos + warp), cs_s = saddr(cons + warp);
   int gp = 0;
   bool aborted = false;
+  const bool prof = (a.debug & 4) != 0 && a.prof != nullptr;  // GDI_PIPE_DEBUG=4: step statistics
+  unsigned long long p_steps = 0, p_acc = 0, p_fill = 0, p_wait = 0, p_t0 = prof ? clock64() : 0;
 
 #pragma unroll 1
   while (sweep < sweeps) {
     // refill the empty lanes [F, lim) of the window (vertex i0 + lane)
     const int lim = min(32, n - i0);
+    const long long p_a = prof ? clock64() : 0;
     if (lane >= F && lane < lim) {
       const int v = i0 + lane;
       own = s[v];
-      f = row_field<SIGNED>(s, col, wgt, __ldg(off + v), __ldg(off + v + 1));
-      wp = __ldg(a.win_pos + v);
-      wn = SIGNED ? __ldg(a.win_neg + v) : 0u;
+      f = 0;
+      if (INCF) {
+        f = fld[v];
+      } else {
+        const int c = v >> 5, l = v & 31;
+        const int b0 = __ldg(a.wsell_off + c), kmax = __ldg(a.wsell_off + c + 1) - b0;
+        const int32_t* __restrict__ rowp = a.wsell + static_cast<size_t>(b0) * 32 + l;
+        int k = 0;
+        for (; k + 8 <= kmax; k += 8) {
+          int u[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) u[q] = __ldg(rowp + (k + q) * 32);
+#pragma unroll
+          for (int q = 0; q < 8; q++) f += nbv<SIGNED>(s, u[q]);
+        }
+        for (; k < kmax; k++) f += nbv<SIGNED>(s, __ldg(rowp + k * 32));
+      }
+      if (!INCF) {
+        wp = __ldg(a.win_pos + v);
+        wn = SIGNED ? __ldg(a.win_neg + v) : 0u;
+      }
     }
     F = lim;
+    if (prof) p_fill += clock64() - p_a;
     // draws pos .. pos + F must be in the ring
-    if (gp < pos + F + 1) {
+    const long long p_w = prof ? clock64() : 0;
+    if (gp < pos + F + 1 && !(a.debug & 8)) {
       for (long long k = 0; (gp = ld_acquire(gp_s)) < pos + F + 1; k++)
         if (k > kWatchdog || ld_acquire(abort_s)) {
           aborted = true;
@@ -226,6 +257,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         }
       if (aborted) break;
     }
+    if (prof) p_wait += clock64() - p_w;
     const bool act = lane < F;
     const uint64_t d0 = myring[(pos + lane) & (kRing - 1)];
     const uint64_t d1 = myring[(pos + lane + 1) & (kRing - 1)];
@@ -250,10 +282,24 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         const int d = fs - os;
         AG += UNITAB ? d : a4 * d;
         dcut -= (d >> 1) * fj;
-        const int k = lane - js;  // pending lanes behind the event: field correction
-        if (k >= 1) {
-          if ((wp >> (k - 1)) & 1u) f += d;
-          if (SIGNED && ((wn >> (k - 1)) & 1u)) f -= d;
+        if (INCF) {
+          // scatter the change into the neighbours' fields (a row has no
+          // repeated neighbour, so the lanes' updates never collide), then the
+          // pending lanes reload theirs
+          const int v = i0 + js;
+          const int e1 = __ldg(off + v + 1);
+          for (int e = __ldg(off + v) + lane; e < e1; e += 32) {
+            const int u = __ldg(col + e);
+            fld[u] = static_cast<int16_t>(fld[u] + (SIGNED ? __ldg(wgt + e) * d : d));
+          }
+          __syncwarp();
+          if (lane > js && lane < F) f = fld[i0 + lane];
+        } else {
+          const int k = lane - js;  // pending lanes behind the event: field correction
+          if (k >= 1) {
+            if ((wp >> (k - 1)) & 1u) f += d;
+            if (SIGNED && ((wn >> (k - 1)) & 1u)) f -= d;
+          }
         }
         __syncwarp();
       }
@@ -266,6 +312,10 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     wn = __shfl_down_sync(FULL, wn, adv);
     F -= adv;
     i0 += adv;
+    if (prof) {
+      p_steps++;
+      p_acc += adv;
+    }
     if (i0 == n) {  // record_barrier (anneal.cpp:165-187)
       cutv += dcut;
       dcut = 0;
@@ -292,6 +342,13 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     }
   }
   __syncwarp();
+  if (prof && lane == 0) {
+    atomicAdd(a.prof + 0, p_steps);
+    atomicAdd(a.prof + 1, p_acc);
+    atomicAdd(a.prof + 2, p_fill);
+    atomicAdd(a.prof + 3, static_cast<unsigned long long>(clock64() - p_t0));
+    atomicAdd(a.prof + 4, p_wait);
+  }
   const int Gf = UNITAB ? AG : AG / a4;
   if (lane == 0) {
     a.final_out[rs] = DevTrace{cutv, Gf, Gf};
@@ -301,9 +358,10 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
 }
 
 template <bool S, bool U>
-const void* win_fn(bool gs) {
-  return gs ? reinterpret_cast<const void*>(&k1_window<S, U, true>)
-            : reinterpret_cast<const void*>(&k1_window<S, U, false>);
+const void* win_fn(bool gs, bool incf) {
+  if (gs) return reinterpret_cast<const void*>(&k1_window<S, U, true, false>);
+  return incf ? reinterpret_cast<const void*>(&k1_window<S, U, false, true>)
+              : reinterpret_cast<const void*>(&k1_window<S, U, false, false>);
 }
 
 }  // namespace
@@ -325,23 +383,36 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   rc = rc < 1 ? 1 : rc > 15 ? 15 : rc;  // block <= 512 threads (__launch_bounds__)
   const int n_pad = (st.n + 1 + 15) & ~15;
   const char* force = std::getenv("GDI_FORCE_KERNEL");
-  bool gs = WinLayout::make(rc, n_pad, false).total > 200 * 1024 || (force && std::string(force) == "window_gmem");
+  const bool gs = WinLayout::make(rc, n_pad, false, false).total > 200 * 1024 ||
+                  (force && std::string(force) == "window_gmem");
+  // incremental fields when they fit next to the spins (int16 bound)
+  const bool incf = !gs && st.max_abs_field < 32768 && WinLayout::make(rc, n_pad, false, true).total <= 200 * 1024 &&
+                    !(force && std::string(force) == "window_masks");
   const bool unitab = ra == 1 && rb == 1;
-  plan->fn = st.unit ? (unitab ? win_fn<false, true>(gs) : win_fn<false, false>(gs))
-                     : (unitab ? win_fn<true, true>(gs) : win_fn<true, false>(gs));
+  plan->fn = st.unit ? (unitab ? win_fn<false, true>(gs, incf) : win_fn<false, false>(gs, incf))
+                     : (unitab ? win_fn<true, true>(gs, incf) : win_fn<true, false>(gs, incf));
   plan->prof = false;
   plan->gw = gs;
   plan->rc = rc;
-  plan->block = 32 * (rc + 1);
+  // one producer warp: a stream costs ~36 cycles per draw on one lane (the
+  // per-warp ALU issue rate, tools/xoshiro_micro.cu), which bounds a replica
+  // at ~1 visit per ~40 cycles; more producer warps did not help (issue
+  // contention with the consumers)
+  plan->nprod = 1;
+  plan->block = 32 * (rc + plan->nprod);
   plan->grid = (replicas + rc - 1) / rc;
-  plan->smem = WinLayout::make(rc, n_pad, gs).total;
+  plan->smem = WinLayout::make(rc, n_pad, gs, incf).total;
   plan->n_words = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
-  static const char* names[2][2][2] = {
-      {{"k1_window<signed>", "k1_window<signed,ab=1>"}, {"k1_window<signed,gmem>", "k1_window<signed,ab=1,gmem>"}},
-      {{"k1_window<unit>", "k1_window<unit,ab=1>"}, {"k1_window<unit,gmem>", "k1_window<unit,ab=1,gmem>"}}};
-  plan->name = names[st.unit ? 1 : 0][gs ? 1 : 0][unitab ? 1 : 0];
+  static const char* names[2][3][2] = {
+      {{"k1_window<signed>", "k1_window<signed,ab=1>"},
+       {"k1_window<signed,gmem>", "k1_window<signed,ab=1,gmem>"},
+       {"k1_window<signed,incf>", "k1_window<signed,ab=1,incf>"}},
+      {{"k1_window<unit>", "k1_window<unit,ab=1>"},
+       {"k1_window<unit,gmem>", "k1_window<unit,ab=1,gmem>"},
+       {"k1_window<unit,incf>", "k1_window<unit,ab=1,incf>"}}};
+  plan->name = names[st.unit ? 1 : 0][gs ? 1 : incf ? 2 : 0][unitab ? 1 : 0];
   return 0;
 }
 
@@ -353,6 +424,9 @@ cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream
   a.a4 = plan.a4;
   a.b = plan.b;
   a.n_words = plan.n_words;
+  a.nprod = plan.nprod;
+  const char* dbg = std::getenv("GDI_PIPE_DEBUG");
+  a.debug = dbg ? std::atoi(dbg) : 0;
   void* params[] = {&a};
   return cudaLaunchKernel(plan.fn, dim3(plan.grid), dim3(plan.block), params, plan.smem, stream);
 }

@@ -55,6 +55,9 @@ struct PipeArgs {
   int32_t n_words;                 // spin words per CTA (>= n + 1)
   uint32_t* gwords;                // [grid][n_words] global spin words, or nullptr (shared memory)
   int8_t* gspins;                  // k1_window: [R][n_words] global int8 spins, or nullptr (shared memory)
+  const int32_t* wsell;            // k1_window rows, SELL-32 over the natural order (layout.hpp)
+  const int32_t* wsell_off;
+  int32_t nprod;                   // k1_window: RNG producer warps
   int32_t sweeps;
   int32_t replicas;
   int32_t rc;                      // replicas (lanes) per CTA

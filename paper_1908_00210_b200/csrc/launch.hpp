@@ -40,6 +40,8 @@ struct PipeGraph {
   int4* far_meta = nullptr;  // device
   uint32_t* win_pos = nullptr;
   uint32_t* win_neg = nullptr;
+  int32_t* wsell = nullptr;  // k1_window rows
+  int32_t* wsell_off = nullptr;
 };
 
 struct PipePlan {
@@ -52,6 +54,7 @@ struct PipePlan {
   bool prof = false;
   bool gw = false;  // spin words in global memory (graph too large for shared memory)
   int n_words = 0;  // k1_window: per-replica spin stride
+  int nprod = 1;    // k1_window: RNG producer warps
   const char* name = "";
 };
 

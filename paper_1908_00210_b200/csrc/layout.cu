@@ -194,6 +194,32 @@ cudaError_t exclusive_scan(const T* in, T* out, int count, cudaStream_t st) {
   return cudaStreamSynchronize(st);  // tmp is released on return
 }
 
+// k1_window rows (natural order): chunk c's slot count = its longest row
+__global__ void k_wchunk_rows(const int32_t* off, int n, int chunks, int32_t* cnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > chunks) return;
+  if (c == chunks) {
+    cnt[c] = 0;
+    return;
+  }
+  int mx = 0;
+  for (int v = 32 * c; v < 32 * c + 32 && v < n; v++) mx = max(mx, off[v + 1] - off[v]);
+  cnt[c] = mx;
+}
+
+__global__ void k_wsell_fill(const int32_t* off, const int32_t* col, const int32_t* w, const int32_t* woff, int n,
+                             int32_t* wsell) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int c = v >> 5, l = v & 31;
+  const int base = woff[c];
+  for (int e = off[v]; e < off[v + 1]; e++) {
+    int32_t idx = col[e];
+    if (w && w[e] < 0) idx |= static_cast<int32_t>(0x80000000u);
+    wsell[static_cast<long long>(base + (e - off[v])) * 32 + l] = idx;
+  }
+}
+
 }  // namespace
 
 cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, int n, int64_t nnz,
@@ -305,6 +331,20 @@ cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStrea
   k_fill_i32<<<1, 32, 0, st>>>(L->far_col.as<int32_t>() + total, 1, n);  // never empty; index n = zero word
   k_far_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, foff.as<int32_t>(), n, win, L->far_col.as<int32_t>(),
                                        L->far_meta.as<int4>(), L->win_pos.as<uint32_t>(), L->win_neg.as<uint32_t>());
+  if ((e = cudaGetLastError())) return e;
+  // k1_window rows
+  const int chunks = (n + 31) / 32;
+  DevBuf wcnt;
+  if ((e = wcnt.alloc((chunks + 1) * sizeof(int32_t))) || (e = L->wsell_off.alloc((chunks + 1) * sizeof(int32_t))))
+    return e;
+  k_wchunk_rows<<<blocks(chunks + 1), kB, 0, st>>>(g.off, n, chunks, wcnt.as<int32_t>());
+  if ((e = exclusive_scan(wcnt.as<int32_t>(), L->wsell_off.as<int32_t>(), chunks + 1, st))) return e;
+  int rows = 0;
+  if ((e = cudaMemcpy(&rows, L->wsell_off.as<int32_t>() + chunks, sizeof rows, cudaMemcpyDeviceToHost))) return e;
+  const long long cells = static_cast<long long>(rows > 0 ? rows : 1) * 32;
+  if ((e = L->wsell.alloc(cells * sizeof(int32_t)))) return e;
+  k_fill_i32<<<1024, kB, 0, st>>>(L->wsell.as<int32_t>(), cells, n);
+  k_wsell_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, L->wsell_off.as<int32_t>(), n, L->wsell.as<int32_t>());
   if ((e = cudaGetLastError())) return e;
   return cudaStreamSynchronize(st);
 }

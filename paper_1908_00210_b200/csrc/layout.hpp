@@ -27,6 +27,10 @@ struct ThruLayout {
 
 struct PipeLayout {
   DevBuf far_col, far_meta, win_pos, win_neg;
+  // k1_window rows: SELL-32 over the natural vertex order (chunk c = vertices
+  // 32c..32c+31, entry k of lane l at (wsell_off[c] + k) * 32 + l; padding
+  // index n; -1 weights in bit 31 of the index)
+  DevBuf wsell, wsell_off;
 };
 
 // Uploads the reference CSR (int64 offsets, int32 neighbours, optional int32

@@ -202,7 +202,7 @@ def test_pipe_window_edge_cases_match_oracle():
 # fit in shared memory, e.g. the 1M-vertex config (BASELINE configs[4])
 
 
-@pytest.mark.parametrize("variant", ["pipe", "pipe_gmem", "window_gmem"])
+@pytest.mark.parametrize("variant", ["pipe", "pipe_gmem", "window_gmem", "window_masks"])
 @pytest.mark.parametrize("name,count", [("G1", 16), ("G22", 256), ("G81pm1", 16)])
 def test_forced_exact_variants_bit_exact(name, count, variant, kernel_variant, monkeypatch):
     """The other exact kernels on the golden configs: k1_pipe (warp-specialised),
@@ -213,6 +213,7 @@ def test_forced_exact_variants_bit_exact(name, count, variant, kernel_variant, m
     s = pi.Session(pi.MinCutProblem.with_default_coefficients(product_graph(golden_configs()[name]["recipe"])),
                    det_params(), 1)
     assert ("gmem" in s.kernel) == variant.endswith("gmem"), s.kernel
+    assert ("incf" in s.kernel) == (variant == "window" and name != "G81pm1"), s.kernel
     assert s.kernel.startswith("k1_" + variant.split("_")[0]), s.kernel
     check_batch_against_golden(name, count=count)
 
