@@ -11,6 +11,8 @@
 //   golden <recipe...> --seeds A B [params]    per-seed final score, spins, trace
 //   bench  <recipe...> --replicas R --threads T [params]
 //                                              replica-throughput timing
+//   runbench <gset paths...> --replicas RUNS --seeds BASE _ --strategy gdi|standard|both
+//            [--sweeps S]                      the reference's own run_benchmark rows
 // Recipes: random N M SEED | torus R C SEED | torus_pm1 R C SEED | file PATH
 //   torus_pm1 = SURVEY §8(c) G81±1 recipe: torus_graph(R,C,SEED), then over the
 //   canonical edges() order w = Rng(SEED).coin() ? +1 : -1, rebuilt by from_edges.
@@ -24,6 +26,7 @@
 #include <vector>
 
 #include "ising/anneal.hpp"
+#include "ising/bench.hpp"
 #include "ising/evaluate.hpp"
 #include "ising/gen.hpp"
 #include "ising/graph.hpp"
@@ -190,6 +193,37 @@ int cmd_bench(const Args& a) {
   return 0;
 }
 
+// The reference batched caller itself (bench.cpp:64-202): rows in its own
+// order, JSON without the timing fields.
+int cmd_runbench(const Args& a) {
+  BenchConfig cfg;
+  cfg.graph_paths = a.pos;
+  cfg.runs_per_graph = a.replicas;
+  cfg.base_seed = a.seed_lo;
+  if (a.strategy == "both")
+    cfg.strategies = {Strategy::gdi, Strategy::standard};
+  else
+    cfg.strategies = {a.strategy == "standard" ? Strategy::standard : Strategy::gdi};
+  cfg.overrides.sweeps = a.sweeps;
+  std::vector<RunReport> rows = run_benchmark(cfg);
+  std::printf("[");
+  for (std::size_t i = 0; i < rows.size(); i++) {
+    const RunReport& r = rows[i];
+    std::printf("%s\n{\"graph_id\": \"%s\", \"nodes\": %d, \"edges\": %lld, \"density\": %.17g, "
+                "\"strategy\": \"%s\", \"best_cut\": %lld, \"best_imbalance\": %lld, \"cut_mean\": %.17g, "
+                "\"cut_min\": %lld, \"cut_max\": %lld, \"seeds\": [",
+                i ? "," : "", r.graph_id.c_str(), r.nodes, static_cast<long long>(r.edges), r.density,
+                r.strategy == Strategy::gdi ? "gdi" : "standard", static_cast<long long>(r.best_cut),
+                static_cast<long long>(r.best_imbalance), r.cut_mean, static_cast<long long>(r.cut_min),
+                static_cast<long long>(r.cut_max));
+    for (std::size_t k = 0; k < r.seeds.size(); k++)
+      std::printf("%s%llu", k ? ", " : "", static_cast<unsigned long long>(r.seeds[k]));
+    std::printf("], \"error\": %s}", r.error.empty() ? "\"\"" : "\"unreadable\"");
+  }
+  std::printf("\n]\n");
+  return 0;
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -203,6 +237,7 @@ int main(int argc, char** argv) {
     if (cmd == "gset") return cmd_gset(a);
     if (cmd == "golden") return cmd_golden(a);
     if (cmd == "bench") return cmd_bench(a);
+    if (cmd == "runbench") return cmd_runbench(a);
     std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
     return 2;
   } catch (const std::exception& e) {

@@ -15,6 +15,7 @@
 #include <memory>
 
 #include "gdi.h"
+#include "ising/bench.hpp"
 #include "ising/ising.hpp"
 
 namespace py = pybind11;
@@ -542,6 +543,58 @@ PYBIND11_MODULE(pyising, m) {
       .def("fetch", &Session::fetch, py::arg("spins") = true, py::arg("trace") = false)
       .def_property_readonly("launch_count", &Session::launch_count)
       .def_property_readonly("kernel", &Session::kernel);
+
+  // batched callers (include/ising/bench.hpp; reference bench.hpp run_benchmark)
+  py::class_<BenchConfig>(m, "BenchConfig")
+      .def(py::init<>())
+      .def_readwrite("graph_paths", &BenchConfig::graph_paths)
+      .def_readwrite("strategies", &BenchConfig::strategies)
+      .def_readwrite("runs_per_graph", &BenchConfig::runs_per_graph)
+      .def_readwrite("base_seed", &BenchConfig::base_seed)
+      .def_readwrite("unit_weights", &BenchConfig::unit_weights)
+      .def_property(
+          "sweeps", [](const BenchConfig& c) { return c.overrides.sweeps; },
+          [](BenchConfig& c, std::optional<std::int32_t> v) { c.overrides.sweeps = v; })
+      .def_property(
+          "flip_fraction0", [](const BenchConfig& c) { return c.overrides.flip_fraction0; },
+          [](BenchConfig& c, std::optional<double> v) { c.overrides.flip_fraction0 = v; })
+      .def_property(
+          "workers", [](const BenchConfig& c) { return c.overrides.workers; },
+          [](BenchConfig& c, std::optional<std::int32_t> v) { c.overrides.workers = v; });
+  py::class_<RunReport>(m, "RunReport")
+      .def_readonly("graph_id", &RunReport::graph_id)
+      .def_readonly("nodes", &RunReport::nodes)
+      .def_readonly("edges", &RunReport::edges)
+      .def_readonly("density", &RunReport::density)
+      .def_readonly("strategy", &RunReport::strategy)
+      .def_readonly("best_cut", &RunReport::best_cut)
+      .def_readonly("best_imbalance", &RunReport::best_imbalance)
+      .def_readonly("cut_mean", &RunReport::cut_mean)
+      .def_readonly("cut_min", &RunReport::cut_min)
+      .def_readonly("cut_max", &RunReport::cut_max)
+      .def_readonly("run_seconds", &RunReport::run_seconds)
+      .def_readonly("seeds", &RunReport::seeds)
+      .def_readonly("error", &RunReport::error);
+  m.def(
+      "run_benchmark",
+      [](const BenchConfig& c) {
+        py::gil_scoped_release nogil;
+        return run_benchmark(c);
+      },
+      py::arg("config"), "Reference run_benchmark rows, one device launch per (graph, strategy) row.");
+  py::class_<BestOfRuns>(m, "BestOfRuns")
+      .def_readonly("best", &BestOfRuns::best)
+      .def_readonly("score", &BestOfRuns::score)
+      .def_readonly("seed", &BestOfRuns::seed)
+      .def_readonly("scores", &BestOfRuns::scores);
+  m.def(
+      "anneal_best_of",
+      [](const MinCutProblem& p, const AnnealParams& params, int runs) {
+        py::gil_scoped_release nogil;
+        return anneal_best_of(p, params, runs);
+      },
+      py::arg("problem"), py::arg("params"), py::arg("runs"),
+      "solve --runs as one launch: lowest H, first seed on ties (ising_cli.cpp:148-166).");
 
   py::class_<PartSession>(m, "PartSession",
                           "One rank of a vertex-partitioned throughput-mode anneal (C ABI gdi_part_*).")

@@ -11,8 +11,12 @@ oracle/_ref by `make -C oracle`). Produces:
                     coefficients / schedules) with full spins, full trace and
                     the barrier counter, via the reference pybind module
                     oracle/_ref/pyising (proj/python/module.cpp).
+  bench_rows.json   the reference's own run_benchmark rows (bench.cpp:64-202)
+                    for BENCH_GRAPHS (G-set files written from the recipes by
+                    the reference generators) plus one unreadable file, both
+                    strategies, via ref_tool runbench.
 
-Usage: python tests/golden/make_golden.py
+Usage: python tests/golden/make_golden.py [--only bench]
 """
 from __future__ import annotations
 
@@ -128,9 +132,46 @@ def small_cases():
     return json.loads(out)
 
 
+# run_benchmark parity set: name -> recipe (written as <name>.txt G-set files)
+BENCH_GRAPHS = {
+    "rnd500": ["random", "500", "5000", "5"],
+    "torus30x20": ["torus", "30", "20", "7"],
+    "pm1_20x20": ["torus_pm1", "20", "20", "9"],
+    "rnd200": ["random", "200", "600", "11"],
+}
+BENCH_ARGS = {"runs": 6, "base_seed": 21, "sweeps": 300}
+
+
+def bench_rows():
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        paths = []
+        for name, recipe in BENCH_GRAPHS.items():
+            text = subprocess.run([TOOL, "gset", *recipe], check=True, capture_output=True, text=True).stdout
+            path = os.path.join(d, name + ".txt")
+            with open(path, "w") as f:
+                f.write(text)
+            paths.append(path)
+        bad = os.path.join(d, "unreadable.txt")
+        with open(bad, "w") as f:
+            f.write("3 1\n1 9 1\n")
+        paths.insert(1, bad)
+        rows = run_tool(["runbench", *paths, "--replicas", str(BENCH_ARGS["runs"]), "--seeds",
+                         str(BENCH_ARGS["base_seed"]), "0", "--strategy", "both", "--sweeps",
+                         str(BENCH_ARGS["sweeps"])])
+    return {"graphs": BENCH_GRAPHS, "args": BENCH_ARGS, "order": [os.path.basename(p)[:-4] for p in paths],
+            "rows": rows}
+
+
 def main():
     if not os.path.exists(TOOL):
         sys.exit("build the reference first: make -C oracle")
+    with open(os.path.join(HERE, "bench_rows.json"), "w") as f:
+        json.dump(bench_rows(), f, indent=1)
+    if "--only" in sys.argv:
+        print("wrote bench_rows.json")
+        return
     docs = dict(golden_config(n) for n in CONFIGS)
     with open(os.path.join(HERE, "config_runs.json"), "w") as f:
         json.dump(docs, f, separators=(",", ":"))
