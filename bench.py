@@ -109,6 +109,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def measured_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/roofline_traffic.json), or None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "roofline_traffic.json")) as f:
+            doc = json.load(f)
+    except OSError:
+        return None
+    rec = doc.get(f"{config}:{kernel}")
+    return rec["dram_bytes_per_launch"] if rec else None
+
+
 def l2_probe_gbs(pi) -> float:
     """Measured L2-resident read bandwidth (library probe, 48 MB buffer)."""
     return pi.probe_l2_bandwidth(48 << 20, 50)
@@ -377,7 +389,7 @@ def main():
                        "parallelism": f"replicas x{world} (weak)", "l2": "flushed between steps (256 MB write)",
                        "kernel": sess.kernel},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
+                         "frac": achieved / hbm, "traffic": measured_traffic(args.config, sess.kernel),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                          "bytes_per_update": bpu, "l2_peak_gbs": l2, "frac_of_l2": achieved / l2,
                          "note": ("exact mode is bound by the serial per-replica decision chain, not bandwidth; "
