@@ -303,13 +303,16 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   // degrade as under Jacobi updates.
   const bool thru_ok = p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" &&
                        force != "pipe_gmem";
-  if (thru_ok && force != "part" && (replicas >= 148 || g->st.n <= 32768) &&
-      thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
+  // (the literal `standard` strategy only exists in K2: its O(n) traversal per
+  // visit needs the replica's spins on chip)
+  if (thru_ok && force != "part" &&
+      (replicas >= 148 || g->st.n <= 32768 || p->strategy == GDI_STRATEGY_STANDARD) &&
+      thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
     s->use_thru = true;
   else if (thru_ok && part_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->kplan) == 0)
     s->use_part = s->use_thru = true;
   else if (thru_ok && force != "part" &&
-           thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->tplan) == 0)
+           thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
     s->use_thru = true;
   // exact mode: k1_window (speculative visit windows) by default; k1_pipe on
   // request (GDI_FORCE_KERNEL=pipe|pipe_gmem); k1_exact for everything else

@@ -106,7 +106,13 @@ __device__ __forceinline__ ChunkIn gather_chunk(const ThruArgs& a, const int8_t*
   return c;
 }
 
-template <int WK, int KMAX>
+// STD: the reference's literal `standard` strategy (anneal.cpp:97-101): every
+// visit re-reads all n spins (the "full traversal" the paper's GDI removes,
+// PAPER.md Alg. 2 vs Alg. 3). Each lane sums the replica's spins itself for
+// its own visit (O(n) work per visit, as on the reference's threads); the sum
+// equals the live counter here, so the decisions are those of `gdi` and only
+// the cost differs (acceptance criterion 6 measures exactly that ratio).
+template <int WK, int KMAX, bool STD>
 __global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
   extern __shared__ __align__(16) int8_t smem[];
   const int n = a.g.n;
@@ -150,6 +156,14 @@ __global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
       ChunkIn nxt{0, 0, 0, false, false, false};
       if (base + 32 < n) nxt = gather_chunk<WK, KMAX>(a, s, base + 32, sweep, k0, k1, tm, en, lane);
       // sequentially consistent counter inside the chunk (see header)
+      if (STD) {  // full traversal per visit
+        __syncwarp();  // the previous chunk's spin writes are visible to every lane
+        int tot = 0;
+#pragma unroll 4
+        for (int j = 0; j < n; j++) tot += s[j];
+        G = cur.live ? tot : G;
+        G = __shfl_sync(0xffffffffu, G, 0);  // every lane summed the same spins
+      }
       const int base_diff = -a4 * cur.own - bb * cur.f;  // diff = a4 (G + excl) + base_diff
       int fin = cur.live ? decide(a4 * G + base_diff, cur.coin, cur.flip) : 0;
       int d = cur.live ? fin - cur.own : 0;
@@ -197,20 +211,21 @@ __global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
   for (int i = lane; i < n; i += 32) a.spins_out[rs * n + i] = s[i];
 }
 
-template <int WK>
+template <int WK, bool STD>
 const void* k2_fn(int kmax) {
   switch (kmax) {
-    case 1: return reinterpret_cast<const void*>(&k2_sweep<WK, 1>);
-    case 2: return reinterpret_cast<const void*>(&k2_sweep<WK, 2>);
-    case 4: return reinterpret_cast<const void*>(&k2_sweep<WK, 4>);
-    case 8: return reinterpret_cast<const void*>(&k2_sweep<WK, 8>);
-    default: return reinterpret_cast<const void*>(&k2_sweep<WK, 16>);
+    case 1: return reinterpret_cast<const void*>(&k2_sweep<WK, 1, STD>);
+    case 2: return reinterpret_cast<const void*>(&k2_sweep<WK, 2, STD>);
+    case 4: return reinterpret_cast<const void*>(&k2_sweep<WK, 4, STD>);
+    case 8: return reinterpret_cast<const void*>(&k2_sweep<WK, 8, STD>);
+    default: return reinterpret_cast<const void*>(&k2_sweep<WK, 16, STD>);
   }
 }
 
 }  // namespace
 
-int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, ThruPlan* plan) {
+int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, bool standard,
+              ThruPlan* plan) {
   // 32-bit decision arithmetic must be exact (same bound as k1_pipe)
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
   while (y) {
@@ -231,14 +246,19 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const double mean_deg = st.n > 0 ? 2.0 * static_cast<double>(st.m) / st.n : 0.0;
   const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : groups <= 4 ? 4 : groups <= 8 ? 8 : 16;
-  plan->fn = wkind == 0 ? k2_fn<0>(kmax) : wkind == 1 ? k2_fn<1>(kmax) : k2_fn<2>(kmax);
+  if (standard)
+    plan->fn = wkind == 0 ? k2_fn<0, true>(kmax) : wkind == 1 ? k2_fn<1, true>(kmax) : k2_fn<2, true>(kmax);
+  else
+    plan->fn = wkind == 0 ? k2_fn<0, false>(kmax) : wkind == 1 ? k2_fn<1, false>(kmax) : k2_fn<2, false>(kmax);
   plan->block = 32 * kWarps;
   plan->grid = (replicas + kWarps - 1) / kWarps;
   plan->smem = static_cast<int>(smem);
   plan->n_pad = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
-  plan->name = wkind == 0 ? "k2_sweep<unit>" : wkind == 1 ? "k2_sweep<pm1>" : "k2_sweep<weighted>";
+  static const char* names[2][3] = {{"k2_sweep<unit>", "k2_sweep<pm1>", "k2_sweep<weighted>"},
+                                     {"k2_sweep<unit,standard>", "k2_sweep<pm1,standard>", "k2_sweep<weighted,standard>"}};
+  plan->name = names[standard ? 1 : 0][wkind];
   return 0;
 }
 

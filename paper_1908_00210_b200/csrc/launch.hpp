@@ -74,7 +74,9 @@ struct ThruPlan {
   int block = 128, grid = 1, smem = 0, n_pad = 0;
   const char* name = "";
 };
-int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, ThruPlan* plan);
+// standard: the literal O(n)-per-visit `standard` strategy (anneal.cpp:97-101)
+int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, bool standard,
+              ThruPlan* plan);
 cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t stream);
 
 struct PartPlan {

@@ -166,3 +166,46 @@ def test_k4_single_replica_selected_and_counter_integrity_hooks():
     assert abs(sum(r.state)) == r.trace[-1].imbalance
     s = pi.Session(p, params(sweeps=5, workers=8), 1)
     assert s.kernel.startswith("k4_sweep"), s.kernel
+
+
+# ---- the literal `standard` strategy (anneal.cpp:97-101) -----------------------
+
+
+def test_standard_strategy_same_decisions_as_gdi():
+    """K2 `standard` re-sums all spins per visit; the sum equals the counter, so
+    the partitions equal the `gdi` ones on the same seeds (only the cost differs)."""
+    g = pi.random_graph(1000, 9990, 47)
+    prob = pi.MinCutProblem.with_default_coefficients(g)
+    seeds = np.arange(1, 9, dtype=np.uint64)
+    out = {}
+    for strat in (pi.Strategy.gdi, pi.Strategy.standard):
+        p = params(sweeps=100, workers=8, strategy=strat)
+        s = pi.Session(prob, p, len(seeds), trace=True)
+        assert s.kernel.startswith("k2_sweep") and (("standard" in s.kernel) == (strat == pi.Strategy.standard))
+        s.set_seeds(seeds)
+        s.launch()
+        s.sync()
+        out[strat] = s.fetch(spins=True, trace=True)
+    assert np.array_equal(out[pi.Strategy.gdi]["spins"], out[pi.Strategy.standard]["spins"])
+    assert np.array_equal(out[pi.Strategy.gdi]["trace"], out[pi.Strategy.standard]["trace"])
+
+
+def test_acceptance_criterion6_standard_vs_gdi_scaling():
+    """acceptance.cpp:217-270: fastest sweep of standard / gdi over 9 sweeps
+    (workers = hardware -> throughput mode), three graphs of growing N; the
+    ratio must grow with N and exceed 5 at N = 10000."""
+    graphs = [pi.random_graph(1000, 9990, 47), pi.torus_graph(100, 50, 57), pi.torus_graph(200, 50, 67)]
+
+    def fastest(prob, strat):
+        p = params(strategy=strat, sweeps=9, flip_fraction0=0.04, decay_rate=0.99, workers=0, seed=3)
+        r = pi.anneal(prob, p)
+        return min(t.seconds for t in r.trace)
+
+    ratios = []
+    for g in graphs:
+        prob = pi.MinCutProblem.with_default_coefficients(g)
+        t_std = min(fastest(prob, pi.Strategy.standard) for _ in range(3))
+        t_gdi = min(fastest(prob, pi.Strategy.gdi) for _ in range(3))
+        ratios.append(t_std / t_gdi)
+    assert ratios[0] < ratios[1] < ratios[2], ratios
+    assert ratios[2] > 5.0, ratios
