@@ -53,6 +53,16 @@ int use_device(int device) {
   int major = 0;
   GDI_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
   if (major != 10) return fail(GDI_ERR_RUNTIME, "gdi-b200 kernels require an sm_100 (B200) device");
+  // keep freed pool memory cached across sessions (see devbuf.hpp)
+  static std::once_flag pool_once[64];
+  if (device < 64)
+    std::call_once(pool_once[device], [device]() {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    });
   return GDI_OK;
 }
 
@@ -603,11 +613,19 @@ int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
   if (out->trace || out->counters) {
     if (!(s->p.flags & GDI_FLAG_TRACE))
       return fail(GDI_ERR_CONFIG, "trace requested but the session was created without GDI_FLAG_TRACE");
-    std::vector<DevTrace> tr(R * S);
-    std::vector<unsigned long long> st(R * (S + 1));
-    GDI_CUDA(cudaMemcpy(tr.data(), s->trace.p, tr.size() * sizeof(DevTrace), cudaMemcpyDeviceToHost));
-    GDI_CUDA(cudaMemcpy(st.data(), s->stamps.p, st.size() * sizeof(unsigned long long),
-                        cudaMemcpyDeviceToHost));
+    // pinned staging: the trace is the bulk of a batch's
+    // result (24 B per sweep per replica + a timestamp), pageable copies of it
+    // cost more than the conversion
+    const size_t tb = R * S * sizeof(DevTrace), sb = R * (S + 1) * sizeof(unsigned long long);
+    // (one buffer per host thread, reused across sessions: one-shot batches
+    // create a session per call)
+    thread_local PinnedBuf stage;
+    GDI_CUDA(stage.ensure(tb + sb));
+    GDI_CUDA(cudaMemcpyAsync(stage.p, s->trace.p, tb, cudaMemcpyDeviceToHost, s->stream));
+    GDI_CUDA(cudaMemcpyAsync(stage.as<char>() + tb, s->stamps.p, sb, cudaMemcpyDeviceToHost, s->stream));
+    GDI_CUDA(cudaStreamSynchronize(s->stream));
+    const DevTrace* tr = stage.as<DevTrace>();
+    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(stage.as<char>() + tb);
     for (size_t r = 0; r < R; r++)
       for (size_t k = 0; k < S; k++) {
         const DevTrace& d = tr[r * S + k];

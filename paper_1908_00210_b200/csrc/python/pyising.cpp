@@ -42,6 +42,14 @@ void check_abi(int rc) {
   if (rc != GDI_OK) raise_abi(rc);
 }
 
+// Per-thread scratch for C-ABI trace records: reused across calls so a batch
+// of R x S records does not page-fault ~50 MB of fresh memory every call.
+gdi_trace_rec* trace_scratch(std::size_t count) {
+  thread_local std::vector<gdi_trace_rec> buf;
+  if (buf.size() < count) buf.resize(count);
+  return buf.data();
+}
+
 // Device-resident session over the C ABI: graph + buffers stay in HBM; the
 // caller times launch() on the stream it passes in.
 class Session {
@@ -89,11 +97,11 @@ public:
     const std::size_t R = replicas_, n = n_, S = sweeps_;
     std::vector<std::int8_t> sp(spins ? R * n : 0);
     std::vector<gdi_score> sc(R);
-    std::vector<gdi_trace_rec> tr(trace ? R * S : 0);
+    gdi_trace_rec* tr = trace ? trace_scratch(R * S) : nullptr;
     gdi_outputs out{};
     out.spins = spins ? sp.data() : nullptr;
     out.scores = sc.data();
-    out.trace = trace ? tr.data() : nullptr;
+    out.trace = tr;
     std::vector<std::int64_t> ctr(trace ? R * S : 0);
     out.counters = trace ? ctr.data() : nullptr;
     {
@@ -112,9 +120,8 @@ public:
   }
   std::string kernel() const { return gdi_session_kernel(sess_); }
 
-  static py::dict pack(std::vector<std::int8_t>&& sp, const std::vector<gdi_score>& sc,
-                       const std::vector<gdi_trace_rec>& tr, std::size_t R, std::size_t n, std::size_t S,
-                       double seconds, bool spins, bool trace) {
+  static py::dict pack(std::vector<std::int8_t>&& sp, const std::vector<gdi_score>& sc, const gdi_trace_rec* tr,
+                       std::size_t R, std::size_t n, std::size_t S, double seconds, bool spins, bool trace) {
     py::dict d;
     std::vector<std::int64_t> cut(R), imb(R), h(R), ctr(R);
     for (std::size_t r = 0; r < R; r++) {
@@ -443,7 +450,7 @@ PYBIND11_MODULE(pyising, m) {
         const std::size_t S = trace ? static_cast<std::size_t>(params.sweeps) : 0;
         std::vector<std::int8_t> sp(R * n);
         std::vector<gdi_score> sc(R);
-        std::vector<gdi_trace_rec> tr(R * S);
+        gdi_trace_rec* tr = trace_scratch(R * S);
         for (std::size_t r = 0; r < R; r++) {
           std::copy(b.runs[r].state.begin(), b.runs[r].state.end(), sp.begin() + r * n);
           const PartitionScore& p = b.scores[r];
@@ -471,7 +478,7 @@ PYBIND11_MODULE(pyising, m) {
         const std::size_t n = static_cast<std::size_t>(g.num_nodes()), S = static_cast<std::size_t>(params.sweeps);
         std::vector<std::int8_t> sp(R * n);
         std::vector<gdi_score> sc(R);
-        std::vector<gdi_trace_rec> tr(trace ? R * S : 0);
+        gdi_trace_rec* tr = trace ? trace_scratch(R * S) : nullptr;
         double secs = 0.0;
         std::vector<std::uint64_t> sd(seeds.data(), seeds.data() + R);
         {
@@ -496,7 +503,7 @@ PYBIND11_MODULE(pyising, m) {
           gdi_outputs out{};
           out.spins = sp.data();
           out.scores = sc.data();
-          out.trace = trace ? tr.data() : nullptr;
+          out.trace = tr;
           const int rc = gdi_anneal_batch(dg, &q, sd.data(), static_cast<std::int32_t>(R), &out);
           gdi_graph_destroy(dg);
           check_abi(rc);
