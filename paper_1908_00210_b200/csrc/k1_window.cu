@@ -111,12 +111,21 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   }
   __syncthreads();
 
-  if (warp >= rc) {
+  // Warp roles. rolemap 1 (default): the producer is warp 3, alone on SM
+  // sub-partition 3 (warp w issues on sub-partition w % 4); consumers take the
+  // warps of sub-partitions 0-2 (consumer c = warp c + c/3); the producer
+  // otherwise shared its sub-partition's ALU pipe with a consumer and ran at
+  // half its standalone rate. rolemap 0: consumers 0..rc-1, producers after.
+  const bool rm1 = a.rolemap == 1;
+  const bool producer = rm1 ? warp == 3 : warp >= rc;
+  const int cw = rm1 ? (warp % 4 == 3 ? -1 : warp - warp / 4) : (producer ? -1 : warp);
+  if (!producer && (cw < 0 || cw >= rc)) return;  // idle padding warp
+  if (producer) {
     // ============================ producers ============================
     // producer warp p serves replicas l = p, p + np, ... (lane = l / np): a
     // stream costs ~25 instructions per draw, so one warp for all replicas
     // could not keep up with the consumers
-    const int np = a.nprod, l = (warp - rc) + lane * np;
+    const int np = a.nprod, l = (rm1 ? 0 : warp - rc) + lane * np;
     const int r = blockIdx.x * rc + l;
     const bool act = l < rc && r < a.replicas;
     Xoshiro rng = Xoshiro::stream(act ? a.seeds[r] : 0ull, 1);  // anneal.cpp:191
@@ -149,14 +158,14 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   }
 
   // ============================ replica warp ============================
-  const int r = blockIdx.x * rc + warp;
+  const int r = blockIdx.x * rc + cw;
   if (r >= a.replicas) {
     if (lane == 0) atomicAdd(flags, 1);
     return;
   }
   const size_t rs = static_cast<size_t>(r);
-  int8_t* s = GS ? a.gspins + rs * n_pad : reinterpret_cast<int8_t*>(smem + L.spins) + warp * n_pad;
-  int16_t* fld = reinterpret_cast<int16_t*>(smem + L.fields) + warp * n_pad;  // INCF only
+  int8_t* s = GS ? a.gspins + rs * n_pad : reinterpret_cast<int8_t*>(smem + L.spins) + cw * n_pad;
+  int16_t* fld = reinterpret_cast<int16_t*>(smem + L.fields) + cw * n_pad;  // INCF only
   const int32_t* __restrict__ off = a.g.off;
   const int32_t* __restrict__ col = a.g.col;
   const int32_t* __restrict__ wgt = a.g.w;
@@ -208,8 +217,8 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   bool en = a.thr[0] >= 0;
   int own = 0, f = 0;
   uint32_t wp = 0u, wn = 0u;
-  const uint64_t* myring = ring + warp * kRing;
-  const unsigned gp_s = saddr(genpos + warp), cs_s = saddr(cons + warp);
+  const uint64_t* myring = ring + cw * kRing;
+  const unsigned gp_s = saddr(genpos + cw), cs_s = saddr(cons + cw);
   int gp = 0;
   bool aborted = false;
   const bool prof = (a.debug & 4) != 0 && a.prof != nullptr;  // GDI_PIPE_DEBUG=4: step statistics
@@ -380,7 +389,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   const double bound = static_cast<double>(ra) * (st.n + 3) + static_cast<double>(rb) * (st.max_abs_field + 2);
   if (bound >= 2147483647.0) return -1;
   int rc = (replicas + 147) / 148;
-  rc = rc < 1 ? 1 : rc > 15 ? 15 : rc;  // block <= 512 threads (__launch_bounds__)
+  rc = rc < 1 ? 1 : rc > 12 ? 12 : rc;  // block <= 512 threads (__launch_bounds__) with role padding
   const int n_pad = (st.n + 1 + 15) & ~15;
   const char* force = std::getenv("GDI_FORCE_KERNEL");
   const bool gs = WinLayout::make(rc, n_pad, false, false).total > 200 * 1024 ||
@@ -399,7 +408,14 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   // at ~1 visit per ~40 cycles; more producer warps did not help (issue
   // contention with the consumers)
   plan->nprod = 1;
-  plan->block = 32 * (rc + plan->nprod);
+  const char* rm = std::getenv("GDI_WINDOW_ROLEMAP");  // tuning experiments
+  plan->rolemap = rm ? std::atoi(rm) : 1;
+  if (plan->rolemap == 1) {
+    const int last = (rc - 1) + (rc - 1) / 3;  // warp of the last consumer
+    plan->block = 32 * (last + 1 > 4 ? last + 1 : 4);
+  } else {
+    plan->block = 32 * (rc + plan->nprod);
+  }
   plan->grid = (replicas + rc - 1) / rc;
   plan->smem = WinLayout::make(rc, n_pad, gs, incf).total;
   plan->n_words = n_pad;
@@ -425,6 +441,7 @@ cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream
   a.b = plan.b;
   a.n_words = plan.n_words;
   a.nprod = plan.nprod;
+  a.rolemap = plan.rolemap;
   const char* dbg = std::getenv("GDI_PIPE_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
   void* params[] = {&a};

@@ -58,6 +58,7 @@ struct PipeArgs {
   const int32_t* wsell;            // k1_window rows, SELL-32 over the natural order (layout.hpp)
   const int32_t* wsell_off;
   int32_t nprod;                   // k1_window: RNG producer warps
+  int32_t rolemap;                 // k1_window: warp role layout (see k1_window.cu)
   int32_t sweeps;
   int32_t replicas;
   int32_t rc;                      // replicas (lanes) per CTA

@@ -55,6 +55,7 @@ struct PipePlan {
   bool gw = false;  // spin words in global memory (graph too large for shared memory)
   int n_words = 0;  // k1_window: per-replica spin stride
   int nprod = 1;    // k1_window: RNG producer warps
+  int rolemap = 1;  // k1_window: warp role layout
   const char* name = "";
 };
 
