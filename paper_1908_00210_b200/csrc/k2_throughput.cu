@@ -35,6 +35,9 @@
 // spin sum for the trace and the counter-integrity value.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "device_rng.cuh"
 #include "kernels.cuh"
 #include "launch.hpp"
@@ -211,6 +214,122 @@ __global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
   for (int i = lane; i < n; i += 32) a.spins_out[rs * n + i] = s[i];
 }
 
+// K2 with incremental fields (chosen when 4 replicas' spins + int32 fields fit
+// in shared memory): every vertex's field is kept exact in shared memory, so
+// a visit reads own spin and field (two loads) instead of gathering its row.
+// Each chunk's few spin changes are then applied in lane order: the exact cut
+// moves by -(d/2) * field (the field as of that change), and the change is
+// scattered into the neighbours' fields. The decisions inside a chunk read
+// the fields as of the chunk start (racy within the chunk, as K2 always was;
+// the counter stays sequentially consistent); the per-sweep cut needs no
+// edge-list pass.
+template <int WK>
+__global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
+  extern __shared__ __align__(16) int8_t smem[];
+  const int n = a.g.n, n_pad = a.n_pad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * kWarps + warp;
+  if (r >= a.replicas) return;
+  int8_t* s = smem + static_cast<size_t>(warp) * n_pad;
+  int* fld = reinterpret_cast<int*>(smem + static_cast<size_t>(kWarps) * n_pad) + static_cast<size_t>(warp) * n_pad;
+  const int32_t* __restrict__ off = a.g.off;
+  const int32_t* __restrict__ col = a.g.col;
+  const int32_t* __restrict__ wgt = a.g.w;
+  const uint64_t seed = a.seeds[r];
+  const size_t rs = static_cast<size_t>(r);
+  const unsigned FULL = 0xffffffffu;
+
+  int G = 0;
+  {
+    Xoshiro r0 = Xoshiro::stream(seed, 0);  // anneal.cpp:148-155
+    for (int i = 0; i < n; i++) {
+      const int v = (r0.next() >> 63) ? 1 : -1;
+      G += v;
+      if ((i & 31) == lane) s[i] = static_cast<int8_t>(v);
+    }
+  }
+  __syncwarp();
+  long long cut = 0;
+  for (int v = lane; v < n; v += 32) {
+    int f = 0;
+    const int sv = s[v];
+    for (int e = __ldg(off + v); e < __ldg(off + v + 1); e++) {
+      const int u = __ldg(col + e);
+      const int w = WK == 0 ? 1 : __ldg(wgt + e);
+      f += w * s[u];
+      if (u > v && s[u] != sv) cut += w;
+    }
+    fld[v] = f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cut += __shfl_xor_sync(FULL, cut, o);
+  __syncwarp();
+  if (a.snaps != nullptr)
+    for (int i = lane; i < n; i += 32) a.snaps[rs * (a.sweeps + 1) * n + i] = s[i];
+  if (lane == 0 && a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1)] = globaltimer_ns();
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  const int a4 = a.a4, bb = a.b;
+  const unsigned below = (1u << lane) - 1u;
+
+  for (int sweep = 0; sweep < a.sweeps; sweep++) {
+    const unsigned long long tm = a.tmask[sweep];
+    const bool en = a.thr[sweep] >= 0;
+    long long dcut = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int idx = base + lane;
+      const bool live = idx < n;
+      const int v = live ? __ldg(a.order + idx) : 0;
+      const int own = live ? s[v] : 0, f = live ? fld[v] : 0;
+      const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(v), 0u, 0u, k0, k1);
+      const bool coin = (x.z >> 31) != 0;
+      const bool flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
+      const int base_diff = -a4 * own - bb * f;
+      int fin = live ? decide(a4 * G + base_diff, coin, flip) : 0;
+      int d = live ? fin - own : 0;
+      unsigned up = __ballot_sync(FULL, d > 0), dn = __ballot_sync(FULL, d < 0);
+      if ((up | dn) != 0u) {
+        for (int round = 0; round < 33; round++) {
+          const int excl = 2 * (__popc(up & below) - __popc(dn & below));
+          const int fin2 = live ? decide(a4 * (G + excl) + base_diff, coin, flip) : 0;
+          if (__all_sync(FULL, fin2 == fin)) break;
+          fin = fin2;
+          d = live ? fin - own : 0;
+          up = __ballot_sync(FULL, d > 0);
+          dn = __ballot_sync(FULL, d < 0);
+        }
+        G += 2 * (__popc(up) - __popc(dn));
+        // apply the changes in lane order: exact cut, spin, field scatter
+        for (unsigned chg = up | dn; chg != 0u; chg &= chg - 1u) {
+          const int j = __ffs(chg) - 1;
+          const int vj = __shfl_sync(FULL, v, j), dj = __shfl_sync(FULL, d, j);
+          dcut -= static_cast<long long>(dj >> 1) * fld[vj];
+          if (lane == 0) s[vj] = static_cast<int8_t>(s[vj] + dj);
+          const int e1 = __ldg(off + vj + 1);
+          for (int e = __ldg(off + vj) + lane; e < e1; e += 32) {
+            const int u = __ldg(col + e);  // a row has no repeated neighbour: no two lanes hit one field
+            fld[u] += WK == 0 ? dj : __ldg(wgt + e) * dj;
+          }
+          __syncwarp();
+        }
+      }
+    }
+    cut += dcut;
+    // record_barrier: spin sum (the counter-integrity check) + the exact cut
+    int sum = 0;
+    for (int u = lane; u < n; u += 32) sum += s[u];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    if (lane == 0) {
+      if (a.trace != nullptr) a.trace[rs * a.sweeps + sweep] = DevTrace{cut, sum, G};
+      if (a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1) + sweep + 1] = globaltimer_ns();
+      if (sweep + 1 == a.sweeps) a.final_out[rs] = DevTrace{cut, sum, G};
+    }
+    if (a.snaps != nullptr)
+      for (int i = lane; i < n; i += 32) a.snaps[(rs * (a.sweeps + 1) + sweep + 1) * n + i] = s[i];
+  }
+  for (int i = lane; i < n; i += 32) a.spins_out[rs * n + i] = s[i];
+}
+
 template <int WK, bool STD>
 const void* k2_fn(int kmax) {
   switch (kmax) {
@@ -246,19 +365,27 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const double mean_deg = st.n > 0 ? 2.0 * static_cast<double>(st.m) / st.n : 0.0;
   const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : groups <= 4 ? 4 : groups <= 8 ? 8 : 16;
+  // incremental fields when 4 replicas' spins (1 B) + fields (4 B) fit
+  const char* force = std::getenv("GDI_FORCE_KERNEL");
+  const bool incf = !standard && 5LL * n_pad * kWarps <= 200 * 1024 && !(force && std::string(force) == "k2_gather");
   if (standard)
     plan->fn = wkind == 0 ? k2_fn<0, true>(kmax) : wkind == 1 ? k2_fn<1, true>(kmax) : k2_fn<2, true>(kmax);
+  else if (incf)
+    plan->fn = wkind == 0   ? reinterpret_cast<const void*>(&k2_incf<0>)
+               : wkind == 1 ? reinterpret_cast<const void*>(&k2_incf<1>)
+                            : reinterpret_cast<const void*>(&k2_incf<2>);
   else
     plan->fn = wkind == 0 ? k2_fn<0, false>(kmax) : wkind == 1 ? k2_fn<1, false>(kmax) : k2_fn<2, false>(kmax);
   plan->block = 32 * kWarps;
   plan->grid = (replicas + kWarps - 1) / kWarps;
-  plan->smem = static_cast<int>(smem);
   plan->n_pad = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
-  static const char* names[2][3] = {{"k2_sweep<unit>", "k2_sweep<pm1>", "k2_sweep<weighted>"},
-                                     {"k2_sweep<unit,standard>", "k2_sweep<pm1,standard>", "k2_sweep<weighted,standard>"}};
-  plan->name = names[standard ? 1 : 0][wkind];
+  static const char* names[3][3] = {{"k2_sweep<unit>", "k2_sweep<pm1>", "k2_sweep<weighted>"},
+                                     {"k2_sweep<unit,standard>", "k2_sweep<pm1,standard>", "k2_sweep<weighted,standard>"},
+                                     {"k2_sweep<unit,incf>", "k2_sweep<pm1,incf>", "k2_sweep<weighted,incf>"}};
+  plan->name = names[standard ? 1 : incf ? 2 : 0][wkind];
+  plan->smem = static_cast<int>((incf ? 5LL : 1LL) * n_pad * kWarps);
   return 0;
 }
 

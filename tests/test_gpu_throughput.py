@@ -171,9 +171,11 @@ def test_k4_single_replica_selected_and_counter_integrity_hooks():
 # ---- the literal `standard` strategy (anneal.cpp:97-101) -----------------------
 
 
-def test_standard_strategy_same_decisions_as_gdi():
+def test_standard_strategy_same_decisions_as_gdi(monkeypatch):
     """K2 `standard` re-sums all spins per visit; the sum equals the counter, so
-    the partitions equal the `gdi` ones on the same seeds (only the cost differs)."""
+    the partitions equal those of `gdi` in the same (row-gathering) K2 kernel on
+    the same seeds: only the cost differs."""
+    monkeypatch.setenv("GDI_FORCE_KERNEL", "k2_gather")
     g = pi.random_graph(1000, 9990, 47)
     prob = pi.MinCutProblem.with_default_coefficients(g)
     seeds = np.arange(1, 9, dtype=np.uint64)
@@ -181,7 +183,8 @@ def test_standard_strategy_same_decisions_as_gdi():
     for strat in (pi.Strategy.gdi, pi.Strategy.standard):
         p = params(sweeps=100, workers=8, strategy=strat)
         s = pi.Session(prob, p, len(seeds), trace=True)
-        assert s.kernel.startswith("k2_sweep") and (("standard" in s.kernel) == (strat == pi.Strategy.standard))
+        assert s.kernel.startswith("k2_sweep") and "incf" not in s.kernel
+        assert ("standard" in s.kernel) == (strat == pi.Strategy.standard)
         s.set_seeds(seeds)
         s.launch()
         s.sync()
