@@ -285,10 +285,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NCCL, one GPU per rank (the driver's scaling runs). BENCH_DIST_BACKEND=gloo
+    # lets several ranks share fewer GPUs to rehearse the multi-rank plumbing
+    # (replica sharding has no kernels that wait across ranks; the numbers of
+    # such a run are not measurements).
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # where collective tensors live
     pi.set_device(local)
 
     recipe, R, sweeps = CONFIGS[args.config]
@@ -349,7 +359,7 @@ def main():
         dist.barrier()
     kernel_ms = [a.elapsed_time(b) for a, b in evs]
     step_ms = sum(kernel_ms) / len(kernel_ms)
-    t_local = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    t_local = torch.tensor([step_ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     step_ms_max = float(t_local.item())
@@ -358,7 +368,7 @@ def main():
 
     # results of the last step: best balanced cut across all replicas of all ranks
     res = sess.fetch(spins=False, trace=False)
-    sc = sh.gather_scores(sh.score_rows(res, seeds), dist if world > 1 else None, device=dev)
+    sc = sh.gather_scores(sh.score_rows(res, seeds), dist if world > 1 else None, device=cdev)
     summ = sh.summarize(sc, n % 2)
     best = {k: summ[k] for k in ("cut", "imbalance", "seed", "best_balanced_cut")}
 
@@ -418,7 +428,7 @@ def main():
         tev = [step_on(tsess) for _ in range(args.steps)]
         torch.cuda.synchronize(dev)
         t_ms = sum(a.elapsed_time(b) for a, b in tev) / len(tev)
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tsess.sync()
@@ -451,7 +461,7 @@ def main():
             torch.cuda.synchronize(dev)
             if i >= 2:
                 e2e_times.append(time.perf_counter() - t0)
-        t_e2e = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
+        t_e2e = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         if rank == 0:
