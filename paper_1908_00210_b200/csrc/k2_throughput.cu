@@ -223,6 +223,11 @@ __global__ void __launch_bounds__(32 * kWarps) k2_sweep(const ThruArgs a) {
 // the fields as of the chunk start (racy within the chunk, as K2 always was;
 // the counter stays sequentially consistent); the per-sweep cut needs no
 // edge-list pass.
+struct IncfIn {
+  int v, own, f;
+  bool live, coin, flip;
+};
+
 template <int WK>
 __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
   extern __shared__ __align__(16) int8_t smem[];
@@ -275,14 +280,27 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
     const unsigned long long tm = a.tmask[sweep];
     const bool en = a.thr[sweep] >= 0;
     long long dcut = 0;
+    // software pipeline: chunk c+1's own spins, fields and draws are read
+    // before chunk c is decided and applied (a racy read one chunk ahead, as
+    // the row-gathering K2 does); the cut uses the fields as of each change
+    auto load = [&](int b) -> IncfIn {
+      IncfIn c;
+      const int idx = b + lane;
+      c.live = idx < n;
+      c.v = c.live ? __ldg(a.order + idx) : 0;
+      c.own = c.live ? s[c.v] : 0;
+      c.f = c.live ? fld[c.v] : 0;
+      const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(c.v), 0u, 0u, k0, k1);
+      c.coin = (x.z >> 31) != 0;
+      c.flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
+      return c;
+    };
+    IncfIn cur = load(0);
     for (int base = 0; base < n; base += 32) {
-      const int idx = base + lane;
-      const bool live = idx < n;
-      const int v = live ? __ldg(a.order + idx) : 0;
-      const int own = live ? s[v] : 0, f = live ? fld[v] : 0;
-      const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(v), 0u, 0u, k0, k1);
-      const bool coin = (x.z >> 31) != 0;
-      const bool flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
+      const IncfIn nx = base + 32 < n ? load(base + 32) : IncfIn{0, 0, 0, false, false, false};
+      const bool live = cur.live, coin = cur.coin, flip = cur.flip;
+      const int v = cur.v, own = cur.own, f = cur.f;
+      cur = nx;
       const int base_diff = -a4 * own - bb * f;
       int fin = live ? decide(a4 * G + base_diff, coin, flip) : 0;
       int d = live ? fin - own : 0;
