@@ -55,6 +55,7 @@ constexpr int kRing = 256;  // draws buffered per replica (power of two, >= 34 +
 // batch; 8 -> 16 -> 32 -> 64 measured 73.7 -> 63.8 -> 58.2 -> 54.8 ms on G22 x1024
 // x1000 sweeps (128 fully unrolled thrashed the instruction cache)
 constexpr int kGen = K1W_GEN;
+static_assert(kRing % kGen == 0, "producer batches must not wrap the ring");
 constexpr long long kWatchdog = 1LL << 28;  // polling iterations before aborting (~seconds)
 
 __device__ __forceinline__ unsigned saddr(const void* p) {
@@ -143,8 +144,9 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     for (long long spin = 0;; spin++) {
       const bool can = act && gen + kGen <= ld_acquire(cs_s) + kRing;
       if (can) {
+        uint64_t* dst = my + (gen & (kRing - 1));  // batches are kGen-aligned and kGen | kRing: no wrap
 #pragma unroll
-        for (int k = 0; k < kGen; k++) my[(gen + k) & (kRing - 1)] = rng.next();
+        for (int k = 0; k < kGen; k++) dst[k] = rng.next();
         gen += kGen;
         st_release(gp_s, gen);
       }
