@@ -387,7 +387,8 @@ const void* win_fn(bool gs, bool incf) {
 int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b, int32_t sweeps,
                 PipePlan* plan) {
   if (!pg.ok) return -1;
-  (void)sweeps;
+  // draw positions are 32-bit: at most one visit + one tie coin per visit
+  if (2.0 * static_cast<double>(sweeps) * st.n + 2 * kRing >= 2147483647.0) return -1;
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
   while (y) {
     const long long t = x % y;
