@@ -350,7 +350,21 @@ __global__ void __launch_bounds__(kCutBlock) k4_cut(const PartArgs a) {
   const long long tid = static_cast<long long>(blockIdx.x) * kCutBlock + threadIdx.x;
   const long long stride = static_cast<long long>(gridDim.x) * kCutBlock;
   long long cut = 0;
-  for (long long e = a.e_begin + tid; e < a.e_end; e += stride) {
+  // four edges per thread in flight (the loop was latency-serial: edge load,
+  // then the two bit loads, per iteration)
+  long long e = a.e_begin + tid;
+  for (; e + 3 * stride < a.e_end; e += 4 * stride) {
+    int2 uv[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) uv[q] = __ldg(a.edges + e + q * stride);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t x =
+          (__ldg(bits + (uv[q].x >> 5)) >> (uv[q].x & 31)) ^ (__ldg(bits + (uv[q].y >> 5)) >> (uv[q].y & 31));
+      if (x & 1u) cut += WK == 0 ? 1 : __ldg(a.edge_w + e + q * stride);
+    }
+  }
+  for (; e < a.e_end; e += stride) {
     const int2 uv = __ldg(a.edges + e);
     const uint32_t x = (__ldg(bits + (uv.x >> 5)) >> (uv.x & 31)) ^ (__ldg(bits + (uv.y >> 5)) >> (uv.y & 31));
     if (x & 1u) cut += WK == 0 ? 1 : __ldg(a.edge_w + e);

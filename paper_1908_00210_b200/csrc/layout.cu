@@ -31,28 +31,42 @@ inline unsigned blocks(long long n) { return static_cast<unsigned>((n + kB - 1) 
 __global__ void k_validate(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                            const int32_t* __restrict__ w, int n, int32_t* off32, GraphScan* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t o0 = off[i], o1 = off[i + 1];
-  off32[i] = static_cast<int32_t>(o0);
-  if (i == n - 1) off32[n] = static_cast<int32_t>(o1);
   unsigned bad = 0;
-  if (o1 < o0) bad |= 1u;
   bool unit = true, pm1 = true;
   long long row = 0;
-  for (int64_t e = o0; e < o1; e++) {
-    const int32_t v = col[e];
-    if (v < 0 || v >= n) bad |= 2u;
-    if (v == i) bad |= 4u;
-    const long long wv = w ? w[e] : 1;
-    unit &= wv == 1;
-    pm1 &= wv == 1 || wv == -1;
-    row += wv < 0 ? -wv : wv;
+  int deg = 0;
+  if (i < n) {
+    const int64_t o0 = off[i], o1 = off[i + 1];
+    off32[i] = static_cast<int32_t>(o0);
+    if (i == n - 1) off32[n] = static_cast<int32_t>(o1);
+    if (o1 < o0) bad |= 1u;
+    for (int64_t e = o0; e < o1; e++) {
+      const int32_t v = col[e];
+      if (v < 0 || v >= n) bad |= 2u;
+      if (v == i) bad |= 4u;
+      const long long wv = w ? w[e] : 1;
+      unit &= wv == 1;
+      pm1 &= wv == 1 || wv == -1;
+      row += wv < 0 ? -wv : wv;
+    }
+    deg = static_cast<int>(o1 > o0 ? o1 - o0 : 0);
   }
+  // one atomic per warp and statistic (1M threads hitting the same words
+  // serialised: 0.7 ms for the 1M-vertex graph)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    row = max(row, __shfl_xor_sync(0xffffffffu, row, o));
+    deg = max(deg, __shfl_xor_sync(0xffffffffu, deg, o));
+  }
+  unit = __all_sync(0xffffffffu, unit);
+  pm1 = __all_sync(0xffffffffu, pm1);
+  if ((threadIdx.x & 31) != 0) return;
   if (bad) atomicOr(&out->bad, bad);
   if (!unit) atomicOr(&out->non_unit, 1u);
   if (!pm1) atomicOr(&out->non_pm1, 1u);
   atomicMax(&out->max_abs_field, static_cast<unsigned long long>(row));
-  atomicMax(&out->max_degree, static_cast<int>(o1 > o0 ? o1 - o0 : 0));
+  atomicMax(&out->max_degree, deg);
 }
 
 // ---- throughput layout -------------------------------------------------------

@@ -20,12 +20,24 @@ class Outputs(ctypes.Structure):
                 ("snapshots", ctypes.c_void_p), ("counters", ctypes.c_void_p), ("seconds", ctypes.c_double)]
 
 
+VP = ctypes.c_void_p  # pointer arguments must be declared (bare ints pass as 32-bit)
+lib.gdi_graph_create.argtypes = [ctypes.c_int, ctypes.c_int32, VP, VP, VP, ctypes.POINTER(VP)]
+lib.gdi_graph_destroy.argtypes = [VP]
+lib.gdi_session_create.argtypes = [VP, ctypes.POINTER(Params), ctypes.c_int32, VP, ctypes.POINTER(VP)]
+lib.gdi_session_set_seeds.argtypes = [VP, VP]
+lib.gdi_session_launch.argtypes = [VP]
+lib.gdi_session_sync.argtypes = [VP]
+lib.gdi_session_fetch.argtypes = [VP, ctypes.POINTER(Outputs)]
+lib.gdi_session_destroy.argtypes = [VP]
+
+
 def ck(rc):
     if rc:
         raise RuntimeError(lib.gdi_last_error())
 
 
 name = sys.argv[1] if len(sys.argv) > 1 else "G22"
+mode = 1 if (len(sys.argv) > 2 and sys.argv[2] == "throughput") else 0
 g = build_graph(pi, CONFIGS[name][0])
 R, S = CONFIGS[name][1], CONFIGS[name][2]
 off, nbr, _w = g.csr()
@@ -41,7 +53,7 @@ for it in range(3):
     gr = ctypes.c_void_p()
     ck(lib.gdi_graph_create(0, n, off.ctypes.data, nbr.ctypes.data, None, ctypes.byref(gr)))
     t.append(time.perf_counter())
-    p = Params(S, 1, 0, 1, 0.04, 0.99, 1, 4, 1)
+    p = Params(S, 1, mode, 1, 0.04, 0.99, 1, 4, 1)
     s = ctypes.c_void_p()
     ck(lib.gdi_session_create(gr, ctypes.byref(p), R, None, ctypes.byref(s)))
     t.append(time.perf_counter())

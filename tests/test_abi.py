@@ -25,6 +25,9 @@ def declared_symbols():
 def lib():
     L = ctypes.CDLL(pkg.LIBGDI)
     L.gdi_last_error.restype = ctypes.c_char_p
+    # pointers must be declared: ctypes passes bare Python ints as 32-bit ints
+    VP = ctypes.c_void_p
+    L.gdi_graph_create.argtypes = [ctypes.c_int, ctypes.c_int32, VP, VP, VP, ctypes.POINTER(VP)]
     return L
 
 
