@@ -122,6 +122,10 @@ int gdi_device_count(int* count);
  * self loops); the caller's Graph already enforces the rest. */
 int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_t* nbr,
                      const int32_t* weights, gdi_graph** out);
+/* The same from the reference's own adjacency array (graph.hpp:67:
+ * Neighbor{int32 node, int32 weight}, interleaved): pairs[2e] = neighbour,
+ * pairs[2e+1] = weight, split on the device (one upload, no host copy). */
+int gdi_graph_create_pairs(int device, int32_t n, const int64_t* offsets, const int32_t* pairs, gdi_graph** out);
 int gdi_graph_destroy(gdi_graph* g);
 int gdi_graph_query(const gdi_graph* g, gdi_graph_info* info);
 

@@ -11,6 +11,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -214,8 +215,52 @@ int gdi_device_count(int* count) {
   return GDI_OK;
 }
 
-int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_t* nbr,
-                     const int32_t* weights, gdi_graph** out) {
+}  // extern "C"
+
+namespace {
+
+// graph.cpp:47-61 invariants on the host, before any device work, so that a
+// bad CSR is a domain error on every machine (the statistics come from the
+// device pass). Rows are split over host threads for large graphs.
+int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int stride) {
+  auto rows = [&](int32_t lo, int32_t hi) -> int {
+    for (int32_t i = lo; i < hi; i++) {
+      const int64_t o0 = offsets[i], o1 = offsets[i + 1];
+      if (o1 < o0) return 1;
+      for (int64_t e = o0; e < o1; e++) {
+        const int32_t v = nbr[e * stride];
+        if (v < 0 || v >= n) return 2;
+        if (v == i) return 3;
+      }
+    }
+    return 0;
+  };
+  const int64_t nnz = offsets[n];
+  unsigned threads = std::thread::hardware_concurrency();
+  threads = nnz < (1 << 20) ? 1 : threads < 1 ? 1 : threads > 16 ? 16 : threads;
+  std::vector<int> codes(threads, 0);
+  if (threads == 1) {
+    codes[0] = rows(0, n);
+  } else {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < threads; t++) {
+      const int32_t lo = static_cast<int32_t>(static_cast<int64_t>(n) * t / threads);
+      const int32_t hi = static_cast<int32_t>(static_cast<int64_t>(n) * (t + 1) / threads);
+      pool.emplace_back([&, t, lo, hi]() { codes[t] = rows(lo, hi); });
+    }
+    for (auto& th : pool) th.join();
+  }
+  for (int c : codes) {
+    if (c == 1) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
+    if (c == 2) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
+    if (c == 3) return fail(GDI_ERR_DOMAIN, "self-loop");
+  }
+  return GDI_OK;
+}
+
+// nbr/weights (separate arrays) or pairs (interleaved {node, weight}).
+int create_graph(int device, int32_t n, const int64_t* offsets, const int32_t* nbr, const int32_t* weights,
+                 const int32_t* pairs, gdi_graph** out) {
   if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
   *out = nullptr;
   if (n <= 0) return fail(GDI_ERR_DOMAIN, "graph needs a positive node count");
@@ -224,37 +269,26 @@ int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_
   if (offsets[0] != 0 || nnz < 0 || (nnz % 2) != 0)
     return fail(GDI_ERR_DOMAIN, "offsets must start at 0 and hold an even entry count");
   if (nnz > 0x7fffffffLL) return fail(GDI_ERR_CAPACITY, "more than 2^31-1 adjacency entries");
-  if (nnz > 0 && !nbr) return fail(GDI_ERR_DOMAIN, "nbr is NULL");
-  // graph.cpp:47-61 invariants, checked before any device work so that a bad
-  // CSR is a domain error on every machine (the statistics come from the
-  // device pass below)
-  for (int32_t i = 0; i < n; i++) {
-    const int64_t o0 = offsets[i], o1 = offsets[i + 1];
-    if (o1 < o0) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
-    for (int64_t e = o0; e < o1; e++) {
-      const int32_t v = nbr[e];
-      if (v < 0 || v >= n) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
-      if (v == i) return fail(GDI_ERR_DOMAIN, "self-loop");
-    }
-  }
+  if (nnz > 0 && !(pairs ? pairs : nbr)) return fail(GDI_ERR_DOMAIN, "adjacency is NULL");
+  int rc = validate_host(n, offsets, pairs ? pairs : nbr, pairs ? 2 : 1);
+  if (rc) return rc;
 
   auto g = std::make_unique<gdi_graph>();
   g->device = device;
   g->st.n = n;
   g->st.m = nnz / 2;
-  int rc = use_device(device);
-  if (rc) return rc;
+  if ((rc = use_device(device))) return rc;
   // upload + validation + statistics on the device (layout.cu)
   GraphScan scan{};
   cudaStream_t st = nullptr;
   GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const cudaError_t ue = upload_and_scan(offsets, nbr, weights, n, nnz, g->off, g->col, g->w, &scan, st);
+  const cudaError_t ue = upload_and_scan(offsets, nbr, weights, pairs, n, nnz, g->off, g->col, g->w, &scan, st);
   cudaStreamDestroy(st);
   GDI_CUDA(ue);
   if (scan.bad & 1u) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
   if (scan.bad & 2u) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
   if (scan.bad & 4u) return fail(GDI_ERR_DOMAIN, "self-loop");
-  g->st.unit = !weights || !scan.non_unit;
+  g->st.unit = !(weights || pairs) || !scan.non_unit;
   g->st.max_abs_field = static_cast<long long>(scan.max_abs_field);
   g->st.max_degree = scan.max_degree;
   g->wkind = g->st.unit ? 0 : (!scan.non_pm1 ? 1 : 2);
@@ -263,6 +297,19 @@ int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_
   g->pipe.n_words = (n + 1 + 3) & ~3;
   *out = g.release();
   return GDI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gdi_graph_create(int device, int32_t n, const int64_t* offsets, const int32_t* nbr, const int32_t* weights,
+                     gdi_graph** out) {
+  return create_graph(device, n, offsets, nbr, weights, nullptr, out);
+}
+
+int gdi_graph_create_pairs(int device, int32_t n, const int64_t* offsets, const int32_t* pairs, gdi_graph** out) {
+  return create_graph(device, n, offsets, nullptr, nullptr, pairs, out);
 }
 
 int gdi_graph_destroy(gdi_graph* g) {

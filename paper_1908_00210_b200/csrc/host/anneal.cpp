@@ -19,6 +19,7 @@
 #include <mutex>
 #include <thread>
 
+#include "abi_util.hpp"
 #include "gdi.h"
 #include "ising/ising.hpp"
 
@@ -71,15 +72,8 @@ const gdi_graph* device_graph(const Graph& g, int dev) {
   if (static_cast<int>(cache.per_device.size()) <= dev) cache.per_device.resize(dev + 1, nullptr);
   if (!cache.per_device[dev]) {
     const std::int32_t n = g.num_nodes();
-    const auto& adj = g.csr_adjacency();
-    std::vector<std::int32_t> nbr(adj.size()), w;
-    for (std::size_t e = 0; e < adj.size(); e++) nbr[e] = adj[e].node;
-    if (!g.all_unit_weights()) {
-      w.resize(adj.size());
-      for (std::size_t e = 0; e < adj.size(); e++) w[e] = adj[e].weight;
-    }
     gdi_graph* h = nullptr;
-    check(gdi_graph_create(dev, n, g.csr_offsets().data(), nbr.data(), w.empty() ? nullptr : w.data(), &h));
+    check(gdi_graph_create_pairs(dev, n, g.csr_offsets().data(), adjacency_pairs(g), &h));
     cache.per_device[dev] = h;
   }
   return cache.per_device[dev];

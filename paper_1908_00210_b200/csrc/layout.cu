@@ -234,10 +234,20 @@ __global__ void k_wsell_fill(const int32_t* off, const int32_t* col, const int32
   }
 }
 
+__global__ void k_split_pairs(const int2* pairs, long long nnz, int32_t* col, int32_t* w) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int2 p = pairs[e];
+    col[e] = p.x;
+    w[e] = p.y;
+  }
+}
+
 }  // namespace
 
-cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, int n, int64_t nnz,
-                            DevBuf& off32, DevBuf& col, DevBuf& w, GraphScan* scan, cudaStream_t st) {
+cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, const int32_t* pairs,
+                            int n, int64_t nnz, DevBuf& off32, DevBuf& col, DevBuf& w, GraphScan* scan,
+                            cudaStream_t st) {
   cudaError_t e;
   DevBuf off64, d_scan;
   if ((e = off64.alloc((n + 1) * sizeof(int64_t)))) return e;
@@ -245,10 +255,23 @@ cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const in
   if ((e = col.alloc((nnz > 0 ? nnz : 1) * sizeof(int32_t)))) return e;
   if ((e = d_scan.alloc(sizeof(GraphScan)))) return e;
   if ((e = cudaMemcpyAsync(off64.p, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st))) return e;
-  if (nnz && (e = cudaMemcpyAsync(col.p, nbr, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
-  if (weights) {
-    if ((e = w.alloc(nnz * sizeof(int32_t)))) return e;
-    if (nnz && (e = cudaMemcpyAsync(w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
+  if (pairs) {  // one upload of the interleaved entries, split on the device
+    DevBuf dp;
+    if ((e = dp.alloc((nnz > 0 ? nnz : 1) * 2 * sizeof(int32_t)))) return e;
+    if ((e = w.alloc((nnz > 0 ? nnz : 1) * sizeof(int32_t)))) return e;
+    if (nnz && (e = cudaMemcpyAsync(dp.p, pairs, nnz * 2 * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
+    if (nnz) {
+      k_split_pairs<<<blocks(nnz), kB, 0, st>>>(dp.as<int2>(), nnz, col.as<int32_t>(), w.as<int32_t>());
+      if ((e = cudaGetLastError())) return e;
+    }
+    weights = w.as<int32_t>();  // (device pointer) marks "weights present" below
+    if ((e = cudaStreamSynchronize(st))) return e;  // dp is released on return
+  } else {
+    if (nnz && (e = cudaMemcpyAsync(col.p, nbr, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
+    if (weights) {
+      if ((e = w.alloc(nnz * sizeof(int32_t)))) return e;
+      if (nnz && (e = cudaMemcpyAsync(w.p, weights, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st))) return e;
+    }
   }
   if ((e = cudaMemsetAsync(d_scan.p, 0, sizeof(GraphScan), st))) return e;
   k_validate<<<blocks(n), kB, 0, st>>>(off64.as<int64_t>(), col.as<int32_t>(), w.as<int32_t>(), n,

@@ -36,8 +36,11 @@ struct PipeLayout {
 // Uploads the reference CSR (int64 offsets, int32 neighbours, optional int32
 // weights), converts the offsets to int32 and validates on the device.
 // `w` is released when every weight is 1.
-cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, int n, int64_t nnz,
-                            DevBuf& off32, DevBuf& col, DevBuf& w, GraphScan* scan, cudaStream_t st);
+// pairs != nullptr: interleaved {neighbour, weight} entries (the reference's
+// Neighbor array, graph.hpp:67), split on the device; nbr / weights unused.
+cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const int32_t* weights, const int32_t* pairs,
+                            int n, int64_t nnz, DevBuf& off32, DevBuf& col, DevBuf& w, GraphScan* scan,
+                            cudaStream_t st);
 
 // K2/K4 layout. wkind: 0 unit, 1 +-1 (sign bit), 2 general weights.
 // Returns cudaErrorInvalidValue when SELL would exceed 2^31 int4 cells.

@@ -14,6 +14,7 @@
 
 #include <memory>
 
+#include "../host/abi_util.hpp"
 #include "gdi.h"
 #include "ising/bench.hpp"
 #include "ising/ising.hpp"
@@ -59,13 +60,7 @@ public:
       : n_(problem.graph().num_nodes()), replicas_(replicas) {
     const AnnealParams params = params_in.validated();
     const Graph& g = problem.graph();
-    std::vector<std::int32_t> nbr, w;
-    for (const Neighbor& nb : g.csr_adjacency()) {
-      nbr.push_back(nb.node);
-      w.push_back(nb.weight);
-    }
-    check_abi(gdi_graph_create(dev, n_, g.csr_offsets().data(), nbr.data(),
-                         g.all_unit_weights() ? nullptr : w.data(), &graph_));
+    check_abi(gdi_graph_create_pairs(dev, n_, g.csr_offsets().data(), adjacency_pairs(g), &graph_));
     gdi_params q{};
     q.sweeps = params.sweeps;
     q.strategy = params.strategy == Strategy::standard ? GDI_STRATEGY_STANDARD : GDI_STRATEGY_GDI;
@@ -189,13 +184,7 @@ public:
       : n_(problem.graph().num_nodes()) {
     const AnnealParams params = params_in.validated();
     const Graph& g = problem.graph();
-    std::vector<std::int32_t> nbr, w;
-    for (const Neighbor& nb : g.csr_adjacency()) {
-      nbr.push_back(nb.node);
-      w.push_back(nb.weight);
-    }
-    check_abi(gdi_graph_create(dev, n_, g.csr_offsets().data(), nbr.data(), g.all_unit_weights() ? nullptr : w.data(),
-                               &graph_));
+    check_abi(gdi_graph_create_pairs(dev, n_, g.csr_offsets().data(), adjacency_pairs(g), &graph_));
     gdi_params q{};
     q.sweeps = params.sweeps;
     q.strategy = params.strategy == Strategy::standard ? GDI_STRATEGY_STANDARD : GDI_STRATEGY_GDI;
@@ -483,14 +472,8 @@ PYBIND11_MODULE(pyising, m) {
         std::vector<std::uint64_t> sd(seeds.data(), seeds.data() + R);
         {
           py::gil_scoped_release nogil;
-          std::vector<std::int32_t> nbr, w;
-          nbr.reserve(g.csr_adjacency().size());
-          for (const Neighbor& nb : g.csr_adjacency()) nbr.push_back(nb.node);
-          if (!g.all_unit_weights())
-            for (const Neighbor& nb : g.csr_adjacency()) w.push_back(nb.weight);
           gdi_graph* dg = nullptr;
-          check_abi(gdi_graph_create(device(), g.num_nodes(), g.csr_offsets().data(), nbr.data(),
-                                     w.empty() ? nullptr : w.data(), &dg));
+          check_abi(gdi_graph_create_pairs(device(), g.num_nodes(), g.csr_offsets().data(), adjacency_pairs(g), &dg));
           gdi_params q{};
           q.sweeps = params.sweeps;
           q.strategy = params.strategy == Strategy::standard ? GDI_STRATEGY_STANDARD : GDI_STRATEGY_GDI;
@@ -520,18 +503,12 @@ PYBIND11_MODULE(pyising, m) {
         if (spins.ndim() != 2 || spins.shape(1) != g.num_nodes())
           throw domain_error("spins must have shape (replicas, num_nodes)");
         const auto R = static_cast<std::int32_t>(spins.shape(0));
-        std::vector<std::int32_t> nbr, w;
-        for (const Neighbor& nb : g.csr_adjacency()) {
-          nbr.push_back(nb.node);
-          w.push_back(nb.weight);
-        }
         std::vector<gdi_score> sc(static_cast<std::size_t>(R));
         const Coefficients& c = problem.coefficients();
         {
           py::gil_scoped_release nogil;
           gdi_graph* dg = nullptr;
-          check_abi(gdi_graph_create(device(), g.num_nodes(), g.csr_offsets().data(), nbr.data(),
-                               g.all_unit_weights() ? nullptr : w.data(), &dg));
+          check_abi(gdi_graph_create_pairs(device(), g.num_nodes(), g.csr_offsets().data(), adjacency_pairs(g), &dg));
           const int rc = gdi_evaluate_batch(dg, spins.data(), R, c.a_num, c.b_num, c.denom, sc.data());
           gdi_graph_destroy(dg);
           check_abi(rc);
