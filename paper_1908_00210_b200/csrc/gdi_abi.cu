@@ -108,7 +108,7 @@ struct gdi_session {
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
   DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords, gspins;
-  DevBuf live, gsum, gdelta, acc, done, finished, bits, fields;  // k4 state
+  DevBuf live, gsum, gdelta, acc, done, finished, bits;  // k4 state
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
   ~gdi_session() {
@@ -366,7 +366,7 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
       (replicas >= 148 || g->st.n <= 32768 || p->strategy == GDI_STRATEGY_STANDARD) &&
       thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
     s->use_thru = true;
-  else if (thru_ok && part_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, true, &s->kplan) == 0)
+  else if (thru_ok && part_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, &s->kplan) == 0)
     s->use_part = s->use_thru = true;
   else if (thru_ok && force != "part" &&
            thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
@@ -425,7 +425,6 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
     GDI_CUDA(s->done.alloc(R * sizeof(unsigned int)));
     GDI_CUDA(s->finished.alloc(R * sizeof(unsigned int)));
     GDI_CUDA(s->bits.alloc(R * ((n + 31) / 32) * sizeof(uint32_t)));
-    if (s->kplan.incf) GDI_CUDA(s->fields.alloc(R * part_stride(g->st.n) * sizeof(int)));
   }
   GDI_CUDA(cudaMemcpyAsync(s->thr_d.p, s->thr.data(), S * sizeof(long long),
                            cudaMemcpyHostToDevice, s->stream));
@@ -477,7 +476,6 @@ int gdi_session_launch(gdi_session* s) {
       a.done = s->done.as<unsigned int>();
       a.finished = s->finished.as<unsigned int>();
       a.bits = s->bits.as<uint32_t>();
-      a.fields = s->fields.as<int>();
       a.trace = s->trace.as<DevTrace>();
       a.stamps = s->stamps.as<unsigned long long>();
       a.snaps = s->snaps.as<int8_t>();
@@ -803,7 +801,7 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   s->rank = rank;
   s->stream = static_cast<cudaStream_t>(stream);
   // chains per rank as for one replica on one device; chunks per rank shrink by W
-  if (part_plan(g->st, g->wkind, 1, 4 * p->a_num, p->b_num, false, &s->plan))
+  if (part_plan(g->st, g->wkind, 1, 4 * p->a_num, p->b_num, &s->plan))
     return fail(GDI_ERR_CAPACITY, "decision arithmetic exceeds the 32-bit kernel bound");
   const int nck = (g->st.n + 31) / 32;
   int ctas = s->plan.ctas;

@@ -90,17 +90,9 @@ __device__ __forceinline__ ChunkIn gather(const PartArgs& a, const int8_t* s, in
   ci.live = idx < a.g.n;
   if (!ci.live) return ci;
   ci.v = __ldg(a.order + idx);
-  if (KMAX == 0) {  // incremental fields: own spin + maintained field, no row gather
-    const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(ci.v), 0u, 0u, k0, k1);
-    ci.coin = (x.z >> 31) != 0;
-    ci.flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
-    ci.own = __ldcg(s + ci.v);
-    ci.f = __ldcg(a.fields + (s - a.spins) + ci.v);
-    return ci;
-  }
   const int c0 = __ldg(a.sell_off + c), c1 = __ldg(a.sell_off + c + 1);
   const int groups = (c1 - c0) >> 5;
-  int4 g4[KMAX > 0 ? KMAX : 1], w4[KMAX > 0 ? KMAX : 1];
+  int4 g4[KMAX], w4[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; k++)
     if (k < groups) {
@@ -129,11 +121,8 @@ __device__ __forceinline__ ChunkIn gather(const PartArgs& a, const int8_t* s, in
 }
 
 // The 32 decisions of one chunk against counter G (sequentially consistent
-// inside the chunk); writes the changed spins and advances G. With fields
-// (fld != nullptr) each change is also scattered into its neighbours' fields
-// (global atomics: other chains read them racily, as they read spins).
-__device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t* s, int a4, int bb, int lane,
-                                             const PartArgs* ap = nullptr, int* fld = nullptr) {
+// inside the chunk); writes the changed spins and advances G.
+__device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t* s, int a4, int bb, int lane) {
   const unsigned below = (1u << lane) - 1u;
   const int base_diff = -a4 * cur.own - bb * cur.f;
   int fin = cur.live ? decide(a4 * G + base_diff, cur.coin, cur.flip) : 0;
@@ -149,27 +138,9 @@ __device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t*
       up = __ballot_sync(0xffffffffu, d > 0);
       dn = __ballot_sync(0xffffffffu, d < 0);
     }
-    if (cur.live && d != 0) {
-      s[cur.v] = static_cast<int8_t>(fin);
-      if (fld != nullptr) {
-        const int e1 = __ldg(ap->g.off + cur.v + 1);
-        for (int e = __ldg(ap->g.off + cur.v); e < e1; e++)
-          atomicAdd(fld + __ldg(ap->g.col + e), ap->g.w ? __ldg(ap->g.w + e) * d : d);
-      }
-    }
+    if (cur.live && d != 0) s[cur.v] = static_cast<int8_t>(fin);
   }
   G += 2 * (__popc(up) - __popc(dn));
-}
-
-// Exact initial fields (incremental-field variant), after k4_init.
-__global__ void __launch_bounds__(256) k4_fields(const PartArgs a, int ns) {
-  const int r = blockIdx.y, v = blockIdx.x * 256 + threadIdx.x;
-  if (v >= a.g.n) return;
-  const int8_t* s = a.spins + static_cast<size_t>(r) * ns;
-  int f = 0;
-  const int e1 = __ldg(a.g.off + v + 1);
-  for (int e = __ldg(a.g.off + v); e < e1; e++) f += (a.g.w ? __ldg(a.g.w + e) : 1) * s[__ldg(a.g.col + e)];
-  a.fields[static_cast<size_t>(r) * ns + v] = f;
 }
 
 // Initial spins (one Philox draw per vertex: the throughput mode is not
@@ -202,7 +173,6 @@ __global__ void __launch_bounds__(256) k4_init(const PartArgs a, int ns) {
 
 template <int WK, int KMAX>
 __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const PartArgs a, int ns) {
-  int* const fld = KMAX == 0 ? a.fields + static_cast<size_t>(blockIdx.y) * ns : nullptr;
   __shared__ int cta_delta, cta_share, last, tail_g;
   __shared__ ChunkIn stage[kTailMax][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -242,7 +212,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
 #pragma unroll 1
   for (int k = 0; k + kDefer < K; k++) {
     const ChunkIn cur = gather<WK, KMAX>(a, s, J + k * P, sweep, k0, k1, tm, en, lane);
-    decide_chunk(cur, G, s, a4, bb, lane, &a, fld);
+    decide_chunk(cur, G, s, a4, bb, lane);
   }
   // CTA tail: the 16 * kDefer deferred chunks (low-degree end of the order)
   // are decided in order by warp 0 against the CTA's exact counter (sum of
@@ -262,7 +232,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
   if (warp == 0) {
     const int gc0 = cta_share + cta_delta;
     int Gc = gc0;
-    for (int t = 0; t < kDefer * kNW; t++) decide_chunk(stage[t][lane], Gc, s, a4, bb, lane, &a, fld);
+    for (int t = 0; t < kDefer * kNW; t++) decide_chunk(stage[t][lane], Gc, s, a4, bb, lane);
     if (lane == 0) cta_delta += Gc - gc0;
     if ((a.debug & 8) && lane == 0 && a.watchdog != nullptr && sweep + 1 == a.sweeps) {
       atomicAdd(a.watchdog + 6, Gc != 0 ? 1 : 0);
@@ -296,7 +266,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
   if (warp != 0) return;
   const int g0 = tail_g;
   int Gt = g0;
-  for (int t = 0; t < T; t++) decide_chunk(stage[t][lane], Gt, s, a4, bb, lane, &a, fld);
+  for (int t = 0; t < T; t++) decide_chunk(stage[t][lane], Gt, s, a4, bb, lane);
   if ((a.debug & 8) && lane == 0 && a.watchdog != nullptr && sweep + 1 == a.sweeps) {
     a.watchdog[2] = g0;
     a.watchdog[3] = Gt;
@@ -472,7 +442,6 @@ const void* gtail_fn(int kmax) {
 template <int WK>
 const void* sweep_fn(int kmax) {
   switch (kmax) {
-    case 0: return reinterpret_cast<const void*>(&k4_sweep<WK, 0>);  // incremental fields
     case 1: return reinterpret_cast<const void*>(&k4_sweep<WK, 1>);
     case 2: return reinterpret_cast<const void*>(&k4_sweep<WK, 2>);
     default: return reinterpret_cast<const void*>(&k4_sweep<WK, 4>);
@@ -481,8 +450,7 @@ const void* sweep_fn(int kmax) {
 
 }  // namespace
 
-int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, bool incf_ok,
-              PartPlan* plan) {
+int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan) {
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
   while (y) {
     const long long t = x % y;
@@ -509,15 +477,7 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->chains = plan->ctas * kNW;
   // tail chunks run by the last CTA against the exact counter (see k4_sweep)
   plan->tail = nck / 8 < kTailMax ? nck / 8 : kTailMax;
-  // incremental fields (one device, opt-in: GDI_FORCE_KERNEL=k4_incf): a visit
-  // reads own spin + field instead of its row, but every spin change scatters
-  // into its neighbours' fields with dependent global loads + atomics; on the
-  // 1M graph that measured slower (20 sweeps: 2.87 ms vs 2.2 ms with rows), so
-  // row gathers stay the default here (unlike K2, whose fields are on chip)
-  const char* force = std::getenv("GDI_FORCE_KERNEL");
-  plan->incf = incf_ok && force && std::string(force) == "k4_incf";
-  const int skmax = plan->incf ? 0 : kmax;
-  plan->sweep_fn = wkind == 0 ? sweep_fn<0>(skmax) : wkind == 1 ? sweep_fn<1>(skmax) : sweep_fn<2>(skmax);
+  plan->sweep_fn = wkind == 0 ? sweep_fn<0>(kmax) : wkind == 1 ? sweep_fn<1>(kmax) : sweep_fn<2>(kmax);
   plan->gtail_fn = wkind == 0 ? gtail_fn<0>(kmax) : wkind == 1 ? gtail_fn<1>(kmax) : gtail_fn<2>(kmax);
   plan->cut_fn = wkind == 0   ? reinterpret_cast<const void*>(&k4_cut<0>)
                  : wkind == 1 ? reinterpret_cast<const void*>(&k4_cut<1>)
@@ -529,13 +489,11 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->pack_grid = static_cast<int>(pg < 1 ? 1 : pg > 4 * 148 ? 4 * 148 : pg);
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
-  static const char* names[2][3] = {{"k4_sweep<unit>", "k4_sweep<pm1>", "k4_sweep<weighted>"},
-                                     {"k4_sweep<unit,incf>", "k4_sweep<pm1,incf>", "k4_sweep<weighted,incf>"}};
-  plan->name = names[plan->incf ? 1 : 0][wkind];
+  plan->name = wkind == 0 ? "k4_sweep<unit>" : wkind == 1 ? "k4_sweep<pm1>" : "k4_sweep<weighted>";
   return 0;
 }
 
-int part_launch_count(const PartPlan& plan, int32_t sweeps) { return (plan.incf ? 2 : 1) + 3 * sweeps; }
+int part_launch_count(const PartPlan&, int32_t sweeps) { return 1 + 3 * sweeps; }
 
 int part_stride(int n) { return (n + 1 + 15) & ~15; }
 
@@ -565,7 +523,6 @@ cudaError_t part_init_launch(const PartPlan& plan, const PartArgs& args, cudaStr
   if ((err = cudaMemsetAsync(a.done, 0, R * sizeof(unsigned int), stream))) return err;
   if ((err = cudaMemsetAsync(a.finished, 0, R * sizeof(unsigned int), stream))) return err;
   k4_init<<<dim3((ns + 255) / 256, R), 256, 0, stream>>>(a, ns);
-  if (plan.incf) k4_fields<<<dim3((a.g.n + 255) / 256, R), 256, 0, stream>>>(a, ns);
   return cudaGetLastError();
 }
 

@@ -88,15 +88,11 @@ struct PartPlan {
   int ctas = 1;        // per replica
   int chains = 16;     // per replica (one per warp)
   int tail = 0;        // tail chunks (exact counter) per sweep
-  bool incf = false;   // incremental fields (one device)
   int block = 512;
   int pack_grid = 148, cut_grid = 148;
   const char* name = "";
 };
-// incf_ok: one device (the incremental-field variant needs every change seen
-// locally; the multi-rank path exchanges spins, not field updates)
-int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, bool incf_ok,
-              PartPlan* plan);
+int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan);
 // Enqueues init + sweeps x (sweep, pack, cut) kernels: 1 + 3 * sweeps launches.
 // spins_out [R][n] receives the final spins (the live array has stride part_stride(n)).
 cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream);

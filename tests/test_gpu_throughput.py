@@ -212,18 +212,3 @@ def test_acceptance_criterion6_standard_vs_gdi_scaling():
         ratios.append(t_std / t_gdi)
     assert ratios[0] < ratios[1] < ratios[2], ratios
     assert ratios[2] > 5.0, ratios
-
-
-def test_k4_incremental_field_variant_quality(monkeypatch):
-    """Opt-in K4 variant with maintained fields (GDI_FORCE_KERNEL=k4_incf):
-    same bar as the default K4 on a 100K-vertex graph vs the row-gather K4."""
-    g = pi.random_graph(100000, 400000, 5)
-    prob = pi.MinCutProblem.with_default_coefficients(g)
-    seeds = np.arange(1, 5, dtype=np.uint64)
-    _, base = run_mode(prob, False, seeds, sweeps=100, trace=True)
-    monkeypatch.setenv("GDI_FORCE_KERNEL", "k4_incf")
-    k, inc = run_mode(prob, False, seeds, sweeps=100, trace=True)
-    assert k.endswith("incf>"), k
-    assert inc["cut"].mean() <= 1.01 * base["cut"].mean()
-    assert (inc["imbalance"] <= 2).all()
-    assert (np.abs(inc["counters"]) == inc["trace"][:, :, 2]).all()
