@@ -55,6 +55,7 @@
 #include "device_rng.cuh"
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "sweep_common.cuh"
 
 namespace gdi {
 
@@ -74,22 +75,6 @@ constexpr int kProducer = 1;  // RNG producer
 constexpr int kNG = kNW - 3;  // gatherer warps (2, 3, 5, 6, 7)
 constexpr int kRing = 64;     // draws buffered per lane (power of two, >= 4B)
 constexpr long long kWatchdog = 1LL << 26;
-
-__device__ __forceinline__ unsigned saddr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ int ld_acquire(unsigned a) {
-  int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned a, int v) {
-  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-// Relaxed store; callers order it after a preceding __threadfence_block().
-__device__ __forceinline__ void st_relaxed(unsigned a, int v) {
-  asm volatile("st.relaxed.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 
 // Shared-memory layout (byte offsets from the dynamic smem base).
 struct Layout {

@@ -42,6 +42,7 @@
 #include "device_rng.cuh"
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "sweep_common.cuh"
 
 namespace gdi {
 
@@ -57,18 +58,6 @@ constexpr int kRing = 256;  // draws buffered per replica (power of two, >= 34 +
 constexpr int kGen = K1W_GEN;
 static_assert(kRing % kGen == 0, "producer batches must not wrap the ring");
 constexpr long long kWatchdog = 1LL << 28;  // polling iterations before aborting (~seconds)
-
-__device__ __forceinline__ unsigned saddr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ int ld_acquire(unsigned a) {
-  int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned a, int v) {
-  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 
 // spin of SELL entry idx (bit 31 = weight -1; padding index n reads 0)
 template <bool SIGNED>

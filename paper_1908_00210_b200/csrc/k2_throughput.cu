@@ -41,17 +41,13 @@
 #include "device_rng.cuh"
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "sweep_common.cuh"
 
 namespace gdi {
 
 namespace {
 
 constexpr int kWarps = 4;  // replicas per CTA (one warp each)
-
-__device__ __forceinline__ int decide(int diff, bool coin, bool flip) {
-  const int c = diff < 0 ? 1 : diff > 0 ? -1 : (coin ? 1 : -1);
-  return flip ? -c : c;
-}
 
 // WK: 0 unit weights, 1 +-1 weights (sign bit of the SELL index), 2 general.
 template <int WK>

@@ -49,6 +49,7 @@
 #include "device_rng.cuh"
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "sweep_common.cuh"
 
 namespace gdi {
 
@@ -59,11 +60,6 @@ constexpr int kDefer = 2;     // chunks per chain deferred to the CTA tail
 constexpr int kTailMax = 32;  // global tail chunks (= kDefer * kNW: shares stage[])
 constexpr int kPackBlock = 256;
 constexpr int kCutBlock = 512;
-
-__device__ __forceinline__ int decide(int diff, bool coin, bool flip) {
-  const int c = diff < 0 ? 1 : diff > 0 ? -1 : (coin ? 1 : -1);
-  return flip ? -c : c;
-}
 
 // Racy neighbour read through L2 (other chains write concurrently; L1 would
 // keep a stale line for the whole sweep). WK as in K2.
