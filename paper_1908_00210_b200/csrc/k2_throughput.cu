@@ -224,7 +224,9 @@ struct IncfIn {
   bool live, coin, flip;
 };
 
-template <int WK>
+// FT: field storage, the narrowest type holding max_i sum_j |w_ij| (int8 for
+// every G-set config: 2 bytes per vertex per replica with the spin).
+template <int WK, typename FT>
 __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
   extern __shared__ __align__(16) int8_t smem[];
   const int n = a.g.n, n_pad = a.n_pad;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
   const int r = blockIdx.x * kWarps + warp;
   if (r >= a.replicas) return;
   int8_t* s = smem + static_cast<size_t>(warp) * n_pad;
-  int* fld = reinterpret_cast<int*>(smem + static_cast<size_t>(kWarps) * n_pad) + static_cast<size_t>(warp) * n_pad;
+  FT* fld = reinterpret_cast<FT*>(smem + static_cast<size_t>(kWarps) * n_pad) + static_cast<size_t>(warp) * n_pad;
   const int32_t* __restrict__ off = a.g.off;
   const int32_t* __restrict__ col = a.g.col;
   const int32_t* __restrict__ wgt = a.g.w;
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
       f += w * s[u];
       if (u > v && s[u] != sv) cut += w;
     }
-    fld[v] = f;
+    fld[v] = static_cast<FT>(f);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cut += __shfl_xor_sync(FULL, cut, o);
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
           const int e1 = __ldg(off + vj + 1);
           for (int e = __ldg(off + vj) + lane; e < e1; e += 32) {
             const int u = __ldg(col + e);  // a row has no repeated neighbour: no two lanes hit one field
-            fld[u] += WK == 0 ? dj : __ldg(wgt + e) * dj;
+            fld[u] = static_cast<FT>(fld[u] + (WK == 0 ? dj : __ldg(wgt + e) * dj));
           }
           __syncwarp();
         }
@@ -342,6 +344,13 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
       for (int i = lane; i < n; i += 32) a.snaps[(rs * (a.sweeps + 1) + sweep + 1) * n + i] = s[i];
   }
   for (int i = lane; i < n; i += 32) a.spins_out[rs * n + i] = s[i];
+}
+
+template <typename FT>
+const void* incf_fn(int wkind) {
+  return wkind == 0   ? reinterpret_cast<const void*>(&k2_incf<0, FT>)
+         : wkind == 1 ? reinterpret_cast<const void*>(&k2_incf<1, FT>)
+                      : reinterpret_cast<const void*>(&k2_incf<2, FT>);
 }
 
 template <int WK, bool STD>
@@ -379,15 +388,15 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const double mean_deg = st.n > 0 ? 2.0 * static_cast<double>(st.m) / st.n : 0.0;
   const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : groups <= 4 ? 4 : groups <= 8 ? 8 : 16;
-  // incremental fields when 4 replicas' spins (1 B) + fields (4 B) fit
+  // incremental fields when 4 replicas' spins (1 B) + fields (fb B) fit
   const char* force = std::getenv("GDI_FORCE_KERNEL");
-  const bool incf = !standard && 5LL * n_pad * kWarps <= 200 * 1024 && !(force && std::string(force) == "k2_gather");
+  const int fb = st.max_abs_field <= 127 ? 1 : st.max_abs_field <= 32767 ? 2 : 4;
+  const bool incf =
+      !standard && (1LL + fb) * n_pad * kWarps <= 200 * 1024 && !(force && std::string(force) == "k2_gather");
   if (standard)
     plan->fn = wkind == 0 ? k2_fn<0, true>(kmax) : wkind == 1 ? k2_fn<1, true>(kmax) : k2_fn<2, true>(kmax);
   else if (incf)
-    plan->fn = wkind == 0   ? reinterpret_cast<const void*>(&k2_incf<0>)
-               : wkind == 1 ? reinterpret_cast<const void*>(&k2_incf<1>)
-                            : reinterpret_cast<const void*>(&k2_incf<2>);
+    plan->fn = fb == 1 ? incf_fn<int8_t>(wkind) : fb == 2 ? incf_fn<int16_t>(wkind) : incf_fn<int>(wkind);
   else
     plan->fn = wkind == 0 ? k2_fn<0, false>(kmax) : wkind == 1 ? k2_fn<1, false>(kmax) : k2_fn<2, false>(kmax);
   plan->block = 32 * kWarps;
@@ -399,7 +408,7 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
                                      {"k2_sweep<unit,standard>", "k2_sweep<pm1,standard>", "k2_sweep<weighted,standard>"},
                                      {"k2_sweep<unit,incf>", "k2_sweep<pm1,incf>", "k2_sweep<weighted,incf>"}};
   plan->name = names[standard ? 1 : incf ? 2 : 0][wkind];
-  plan->smem = static_cast<int>((incf ? 5LL : 1LL) * n_pad * kWarps);
+  plan->smem = static_cast<int>((incf ? 1LL + fb : 1LL) * n_pad * kWarps);
   return 0;
 }
 
