@@ -177,6 +177,19 @@ int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv);
 int gdi_part_fetch(gdi_part* s, gdi_outputs* out);
 int gdi_part_destroy(gdi_part* s);
 
+/* Fused exchange (optional, before gdi_part_init): each rank's sweep kernel
+ * stores every spin change straight into the other ranks' spin copies (peer
+ * memory, NVLink), so remote spins are fresh during the sweep and the
+ * per-sweep collective shrinks to the counter deltas (exchange bytes = 16).
+ * gdi_part_ipc_handle exports this rank's spin copy (GDI_IPC_HANDLE_BYTES
+ * bytes); gdi_part_attach_peers takes every rank's handle, rank-major (the
+ * caller all-gathers them); gdi_part_attach_local wires W partitions of one
+ * process on one device (testing). At most 8 ranks. */
+#define GDI_IPC_HANDLE_BYTES 64
+int gdi_part_ipc_handle(const gdi_part* s, void* handle);
+int gdi_part_attach_peers(gdi_part* s, const void* handles);
+int gdi_part_attach_local(gdi_part* s, gdi_part* const* parts);
+
 /* Measurement utility (not a reference interface): sustained read bandwidth
  * in GB/s of an L2-resident buffer of `bytes` bytes re-read `iters` times on
  * `device`; the roofline denominator for cache-resident graphs. */

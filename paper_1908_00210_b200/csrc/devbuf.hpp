@@ -17,14 +17,27 @@ namespace gdi {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool plain = false;  // cudaMalloc'd (exportable through CUDA IPC; pool memory is not)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFreeAsync(p, 0);
+    if (p) {
+      if (plain)
+        cudaFree(p);
+      else
+        cudaFreeAsync(p, 0);
+    }
     p = nullptr;
     bytes = 0;
+    plain = false;
+  }
+  cudaError_t alloc_plain(size_t b) {
+    reset();
+    bytes = b;
+    plain = true;
+    return b ? cudaMalloc(&p, b) : cudaSuccess;
   }
   cudaError_t alloc(size_t b) {
     reset();

@@ -780,6 +780,11 @@ struct gdi_part {
   std::vector<unsigned long long> tmask;
   DevBuf seeds, thr_d, tmask_d, live, spins, gsum, gdelta, acc, done, finished, bits, trace, stamps, final_out, watchdog;
   bool inited = false;
+  bool peer = false;                 // fused exchange attached (gdi_part_attach_*)
+  std::vector<void*> ipc_opened;     // peer spin copies opened through CUDA IPC
+  ~gdi_part() {
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+  }
 };
 
 extern "C" {
@@ -815,7 +820,7 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   GDI_CUDA(s->seeds.alloc(sizeof(uint64_t)));
   GDI_CUDA(s->thr_d.alloc(S * sizeof(long long)));
   GDI_CUDA(s->tmask_d.alloc(S * sizeof(unsigned long long)));
-  GDI_CUDA(s->live.alloc(part_stride(g->st.n)));
+  GDI_CUDA(s->live.alloc_plain(part_stride(g->st.n)));  // exportable to the other ranks (CUDA IPC)
   GDI_CUDA(s->spins.alloc(n));
   GDI_CUDA(s->gsum.alloc(sizeof(long long)));
   GDI_CUDA(s->gdelta.alloc(sizeof(long long)));
@@ -869,8 +874,57 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
 
 int gdi_part_exchange_bytes(const gdi_part* s, int64_t* bytes) {
   if (!s || !bytes) return fail(GDI_ERR_CONFIG, "NULL argument");
-  *bytes = part_exchange_bytes(s->g->st.n, s->world);
+  *bytes = part_exchange_bytes(s->g->st.n, s->world, s->peer);
   return GDI_OK;
+}
+
+int gdi_part_ipc_handle(const gdi_part* s, void* handle) {
+  if (!s || !handle) return fail(GDI_ERR_CONFIG, "NULL argument");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  cudaIpcMemHandle_t h;
+  GDI_CUDA(cudaIpcGetMemHandle(&h, s->live.p));
+  std::memcpy(handle, &h, sizeof h);
+  return GDI_OK;
+}
+
+namespace {
+int attach(gdi_part* s, const std::vector<int8_t*>& ptrs) {
+  if (s->inited) return fail(GDI_ERR_CONFIG, "attach peers before gdi_part_init");
+  if (static_cast<int>(ptrs.size()) != s->world - 1 || s->world - 1 > 7)
+    return fail(GDI_ERR_CONFIG, "fused exchange needs world - 1 <= 7 peers");
+  for (int q = 0; q < s->world - 1; q++) s->args.peer[q] = ptrs[q];
+  s->args.npeer = s->world - 1;
+  s->peer = s->world > 1;
+  return GDI_OK;
+}
+}  // namespace
+
+int gdi_part_attach_peers(gdi_part* s, const void* handles) {
+  if (!s || !handles) return fail(GDI_ERR_CONFIG, "NULL argument");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  std::vector<int8_t*> ptrs;
+  for (int q = 0; q < s->world; q++) {
+    if (q == s->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + q * GDI_IPC_HANDLE_BYTES, sizeof h);
+    void* p = nullptr;
+    GDI_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    s->ipc_opened.push_back(p);
+    ptrs.push_back(static_cast<int8_t*>(p));
+  }
+  return attach(s, ptrs);
+}
+
+int gdi_part_attach_local(gdi_part* s, gdi_part* const* parts) {
+  if (!s || !parts) return fail(GDI_ERR_CONFIG, "NULL argument");
+  std::vector<int8_t*> ptrs;
+  for (int q = 0; q < s->world; q++) {
+    if (q == s->rank) continue;
+    if (!parts[q] || parts[q]->g->device != s->g->device)
+      return fail(GDI_ERR_CONFIG, "local peers must be partitions on the same device");
+    ptrs.push_back(parts[q]->live.as<int8_t>());
+  }
+  return attach(s, ptrs);
 }
 
 int gdi_part_init(gdi_part* s) {
@@ -895,7 +949,8 @@ int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv) {
   if (!s || !recv) return fail(GDI_ERR_CONFIG, "NULL argument");
   if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
   GDI_CUDA(cudaSetDevice(s->g->device));
-  GDI_CUDA(part_xunpack_launch(s->plan, s->args, recv, part_exchange_bytes(s->g->st.n, s->world), sweep, s->stream));
+  GDI_CUDA(part_xunpack_launch(s->plan, s->args, recv, part_exchange_bytes(s->g->st.n, s->world, s->peer), sweep,
+                                 s->stream));
   GDI_CUDA(part_barrier_launch(s->plan, s->args, sweep, s->spins.as<int8_t>(), s->stream));
   return GDI_OK;
 }

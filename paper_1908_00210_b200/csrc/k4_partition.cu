@@ -118,7 +118,8 @@ __device__ __forceinline__ ChunkIn gather(const PartArgs& a, const int8_t* s, in
 
 // The 32 decisions of one chunk against counter G (sequentially consistent
 // inside the chunk); writes the changed spins and advances G.
-__device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t* s, int a4, int bb, int lane) {
+__device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t* s, int a4, int bb, int lane,
+                                             const PartArgs* peers = nullptr) {
   const unsigned below = (1u << lane) - 1u;
   const int base_diff = -a4 * cur.own - bb * cur.f;
   int fin = cur.live ? decide(a4 * G + base_diff, cur.coin, cur.flip) : 0;
@@ -134,7 +135,11 @@ __device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t*
       up = __ballot_sync(0xffffffffu, d > 0);
       dn = __ballot_sync(0xffffffffu, d < 0);
     }
-    if (cur.live && d != 0) s[cur.v] = static_cast<int8_t>(fin);
+    if (cur.live && d != 0) {
+      s[cur.v] = static_cast<int8_t>(fin);
+      if (peers != nullptr)  // fused exchange: the change lands in every rank's copy
+        for (int q = 0; q < peers->npeer; q++) peers->peer[q][cur.v] = static_cast<int8_t>(fin);
+    }
   }
   G += 2 * (__popc(up) - __popc(dn));
 }
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
 #pragma unroll 1
   for (int k = 0; k + kDefer < K; k++) {
     const ChunkIn cur = gather<WK, KMAX>(a, s, J + k * P, sweep, k0, k1, tm, en, lane);
-    decide_chunk(cur, G, s, a4, bb, lane);
+    decide_chunk(cur, G, s, a4, bb, lane, a.npeer > 0 ? &a : nullptr);
   }
   // CTA tail: the 16 * kDefer deferred chunks (low-degree end of the order)
   // are decided in order by warp 0 against the CTA's exact counter (sum of
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
   if (warp == 0) {
     const int gc0 = cta_share + cta_delta;
     int Gc = gc0;
-    for (int t = 0; t < kDefer * kNW; t++) decide_chunk(stage[t][lane], Gc, s, a4, bb, lane);
+    for (int t = 0; t < kDefer * kNW; t++) decide_chunk(stage[t][lane], Gc, s, a4, bb, lane, a.npeer > 0 ? &a : nullptr);
     if (lane == 0) cta_delta += Gc - gc0;
     if ((a.debug & 8) && lane == 0 && a.watchdog != nullptr && sweep + 1 == a.sweeps) {
       atomicAdd(a.watchdog + 6, Gc != 0 ? 1 : 0);
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(256) k4_xpack(const PartArgs a, int ns, unsign
   const int8_t* s = a.spins;
   uint32_t* words = reinterpret_cast<uint32_t*>(send + 8);
   const int nmain = nck - a.tail;  // tail chunks are recomputed identically on every rank
-  const int nw = nmain > rk ? (nmain - rk + W - 1) / W : 0;
+  const int nw = a.npeer > 0 ? 0 : nmain > rk ? (nmain - rk + W - 1) / W : 0;  // peer mode: deltas only
   for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < nw; i += gridDim.x * 8) {
     const int idx = (rk + i * W) * 32 + lane;
     const int8_t x = idx < n ? __ldcg(s + __ldg(a.order + idx)) : static_cast<int8_t>(-1);
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(256) k4_xunpack(const PartArgs a, int ns, cons
   const int n = a.g.n, nck = (n + 31) >> 5, W = a.world, rk = a.rank;
   const int lane = threadIdx.x & 31;
   int8_t* s = a.spins;
-  const int nmain = nck - a.tail;
+  const int nmain = a.npeer > 0 ? 0 : nck - a.tail;  // peer mode: the spins arrived during the sweep
   for (int c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nmain; c += gridDim.x * 8) {
     const int q = c % W;
     if (q == rk) continue;
@@ -565,7 +570,8 @@ cudaError_t part_xunpack_launch(const PartPlan& plan, const PartArgs& args, cons
   return cudaLaunchKernel(plan.gtail_fn, dim3(1, a.replicas), dim3(plan.block), p, 0, stream);
 }
 
-long long part_exchange_bytes(int n, int world) {
+long long part_exchange_bytes(int n, int world, bool peer) {
+  if (peer) return 16;  // counter delta only
   const int nck = (n + 31) / 32;
   const long long words = (nck + world - 1) / world;  // rank 0 owns the most
   return (8 + 4 * words + 15) & ~15LL;

@@ -136,6 +136,11 @@ struct PartArgs {
   unsigned int* done;              // [R] barrier blocks finished
   unsigned int* finished;          // [R] CTAs finished (tail ticket)
   uint32_t* bits;                  // [R][ceil(n/32)] packed spins at the barrier
+  // fused exchange (ranks > 1): every spin change is also stored into the
+  // other ranks' spin copies (peer memory over NVLink); the per-sweep
+  // collective then only carries the counter deltas
+  int8_t* peer[7];
+  int32_t npeer;
   int32_t tail;                    // last chunks of the order, decided against the exact counter
   int32_t tail_ticket;             // 1: by the last CTA of k4_sweep (one device); 0: k4_gtail on every rank
   int32_t debug;                   // timing experiments only (GDI_K4_DEBUG); 0 in production

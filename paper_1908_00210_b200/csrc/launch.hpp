@@ -105,7 +105,7 @@ cudaError_t part_barrier_launch(const PartPlan& plan, const PartArgs& args, int 
 cudaError_t part_xpack_launch(const PartPlan& plan, const PartArgs& args, void* send, cudaStream_t stream);
 cudaError_t part_xunpack_launch(const PartPlan& plan, const PartArgs& args, const void* recv, long long stride,
                                 int sweep, cudaStream_t stream);
-long long part_exchange_bytes(int n, int world);  // per-rank send buffer bytes (16-aligned)
+long long part_exchange_bytes(int n, int world, bool peer);  // per-rank send buffer bytes (16-aligned)
 int part_launch_count(const PartPlan& plan, int32_t sweeps);
 int part_stride(int n);
 

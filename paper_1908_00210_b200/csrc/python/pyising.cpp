@@ -207,6 +207,20 @@ public:
     return b;
   }
   void init() { check_abi(gdi_part_init(sess_)); }
+  py::bytes ipc_handle() const {
+    char h[GDI_IPC_HANDLE_BYTES];
+    check_abi(gdi_part_ipc_handle(sess_, h));
+    return py::bytes(h, sizeof h);
+  }
+  void attach_peers(const py::bytes& handles) {
+    const std::string hs = handles;
+    check_abi(gdi_part_attach_peers(sess_, hs.data()));
+  }
+  void attach_local(const std::vector<PartSession*>& parts) {
+    std::vector<gdi_part*> ps;
+    for (PartSession* q : parts) ps.push_back(q->sess_);
+    check_abi(gdi_part_attach_local(sess_, ps.data()));
+  }
   void sweep(int k, std::uintptr_t send) { check_abi(gdi_part_sweep(sess_, k, reinterpret_cast<void*>(send))); }
   void finish(int k, std::uintptr_t recv) {
     check_abi(gdi_part_finish(sess_, k, reinterpret_cast<const void*>(recv)));
@@ -587,6 +601,11 @@ PYBIND11_MODULE(pyising, m) {
            py::arg("stream") = 0, py::arg("device") = 0)
       .def_property_readonly("exchange_bytes", &PartSession::exchange_bytes)
       .def("init", &PartSession::init)
+      .def("ipc_handle", &PartSession::ipc_handle, "this rank's spin copy as a CUDA IPC handle (bytes)")
+      .def("attach_peers", &PartSession::attach_peers, py::arg("handles"),
+           "fused exchange: every rank's ipc_handle(), rank-major, concatenated")
+      .def("attach_local", &PartSession::attach_local, py::arg("parts"),
+           "fused exchange between partitions of this process on one device (testing)")
       .def("sweep", &PartSession::sweep, py::arg("k"), py::arg("send"))
       .def("finish", &PartSession::finish, py::arg("k"), py::arg("recv"))
       .def("fetch", &PartSession::fetch);

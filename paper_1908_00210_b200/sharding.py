@@ -8,8 +8,11 @@
   ising_cli.cpp:160; bench: best balanced cut, bench.cpp:181-193).
 * Vertex partitioning (the 1M-vertex graph): one replica over W ranks. Rank r
   owns the chunks c = r (mod W) of the degree-binned order (K4 chains
-  r, r + W, ...), keeps a full spin copy and, once per sweep, all-gathers one
-  packed bit per owned vertex plus its counter delta (include/gdi.h
+  r, r + W, ...) and keeps a full spin copy. Fused (default): every spin
+  change is stored by the sweep kernel itself into the other ranks' copies
+  through peer memory (NVLink; CUDA IPC handles exchanged once), and the
+  per-sweep collective only sums the counter deltas. Unfused: once per sweep,
+  all-gather one packed bit per owned vertex plus the delta (include/gdi.h
   gdi_part_*). The edge list is split for the barrier cut; partial cuts are
   summed at the end with one all-reduce.
 
@@ -85,20 +88,29 @@ def exchange_bytes(n: int, world: int) -> int:
     return (8 + 4 * words + 15) & ~15
 
 
-def run_partitioned(sessions: Sequence, sweeps: int, exchange: Callable, buffers: Callable):
+def run_partitioned(sessions: Sequence, sweeps: int, exchange: Callable, buffers: Callable,
+                    barrier: Callable | None = None):
     """Drive W' local sessions (W' = 1 per process on real GPUs, W on one GPU
     when emulating) through init + per-sweep sweep / exchange / finish.
 
     buffers(i) -> (send_ptr, recv_ptr) for local session i; exchange() moves
-    every rank's send buffer into every rank's recv buffer (rank-major)."""
+    every rank's send buffer into every rank's recv buffer (rank-major).
+    barrier(), with the fused exchange: no rank may start sweep k+1 (whose
+    kernel stores into the other ranks' spin copies) before every rank has
+    finished sweep k's barrier work on its copy (tail replay, cut), nor sweep 0
+    before every rank has initialised its copy."""
     for s in sessions:
-        s.init()
+        s.init()  # writes the whole local copy: peers must not store into it before this
+    if barrier is not None:
+        barrier()
     for k in range(sweeps):
         for i, s in enumerate(sessions):
             s.sweep(k, buffers(i)[0])
         exchange()
         for i, s in enumerate(sessions):
             s.finish(k, buffers(i)[1])
+        if barrier is not None and k + 1 < sweeps:
+            barrier()
     return [s.fetch() for s in sessions]
 
 
@@ -115,9 +127,12 @@ def combine(results: Sequence[dict], all_reduce_sum: Callable | None = None) -> 
             "balance_counter": int(r0["balance_counter"]), "seconds": max(r["seconds"] for r in results)}
 
 
-def anneal_partitioned(problem, params, seed: int, dist, device: int, stream=None) -> dict:
+def anneal_partitioned(problem, params, seed: int, dist, device: int, stream=None, fused: bool = True) -> dict:
     """One rank of a W-rank vertex-partitioned anneal (call on every rank;
-    NCCL process group already initialised, one GPU per rank)."""
+    process group already initialised, one GPU per rank). fused: spin changes
+    go straight into the other ranks' copies over peer memory (CUDA IPC
+    handles exchanged once), and the per-sweep collective carries only the
+    counter deltas; otherwise one packed spin all-gather per sweep."""
     import torch
 
     import paper_1908_00210_b200 as pi
@@ -126,23 +141,45 @@ def anneal_partitioned(problem, params, seed: int, dist, device: int, stream=Non
     dev = torch.device("cuda", device)
     stream = stream or torch.cuda.current_stream(dev)
     ps = pi.PartSession(problem, params, world, rank, int(seed), stream=stream.cuda_stream, device=device)
+    if fused and world > 1:
+        handles = [None] * world
+        dist.all_gather_object(handles, ps.ipc_handle())
+        ps.attach_peers(b"".join(handles))
     nb = ps.exchange_bytes
+    cdev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
     send = torch.zeros(nb, dtype=torch.uint8, device=dev)
     recv = torch.zeros(world * nb, dtype=torch.uint8, device=dev)
+    def exchange():
+        if cdev.type == "cuda":
+            dist.all_gather_into_tensor(recv, send)
+        else:  # gloo (multi-rank rehearsal on fewer GPUs): host-staged
+            torch.cuda.current_stream(dev).synchronize()
+            out = torch.empty(world * nb, dtype=torch.uint8)
+            dist.all_gather_into_tensor(out, send.cpu())
+            recv.copy_(out)
+
+    token = torch.zeros(1, dtype=torch.int32, device=cdev)
+
+    def barrier():  # stream-ordered under NCCL: a device-side barrier, no host round trip
+        if cdev.type != "cuda":
+            torch.cuda.current_stream(dev).synchronize()
+        dist.all_reduce(token)
+
     with torch.cuda.stream(stream):
-        res = run_partitioned([ps], params.sweeps, lambda: dist.all_gather_into_tensor(recv, send),
-                              lambda i: (send.data_ptr(), recv.data_ptr()))
+        res = run_partitioned([ps], params.sweeps, exchange, lambda i: (send.data_ptr(), recv.data_ptr()),
+                              barrier if fused and world > 1 else None)
 
     def all_reduce_sum(a):
-        t = torch.as_tensor(a, device=dev)
+        t = torch.as_tensor(a, device=cdev)
         dist.all_reduce(t)
         return t.cpu().numpy()
 
     return combine(res, all_reduce_sum)
 
 
-def emulate_partitioned(problem, params, seed: int, world: int, device: int = 0) -> dict:
-    """All W ranks in this process on one device (see module docstring)."""
+def emulate_partitioned(problem, params, seed: int, world: int, device: int = 0, fused: bool = False) -> dict:
+    """All W ranks in this process on one device (see module docstring);
+    fused: the ranks' sweep kernels store into each other's spin copies."""
     import torch
 
     import paper_1908_00210_b200 as pi
@@ -151,6 +188,9 @@ def emulate_partitioned(problem, params, seed: int, world: int, device: int = 0)
     stream = torch.cuda.current_stream(dev)
     ss = [pi.PartSession(problem, params, world, r, int(seed), stream=stream.cuda_stream, device=device)
           for r in range(world)]
+    if fused and world > 1:
+        for s_ in ss:
+            s_.attach_local(ss)
     nb = ss[0].exchange_bytes
     sends = [torch.zeros(nb, dtype=torch.uint8, device=dev) for _ in range(world)]
     recv = torch.zeros(world * nb, dtype=torch.uint8, device=dev)
