@@ -53,7 +53,8 @@ struct DevBuf {
   }
 };
 
-// Page-locked host staging buffer (device -> host copies at DMA speed).
+// Page-locked host staging buffer (device -> host copies at DMA speed), also
+// mapped into the device address space (kernels may write it directly).
 struct PinnedBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -68,7 +69,7 @@ struct PinnedBuf {
     if (p) cudaFreeHost(p);
     p = nullptr;
     bytes = 0;
-    cudaError_t e = cudaHostAlloc(&p, b, cudaHostAllocDefault);
+    cudaError_t e = cudaHostAlloc(&p, b, cudaHostAllocMapped | cudaHostAllocPortable);
     if (e == cudaSuccess) bytes = b;
     return e;
   }

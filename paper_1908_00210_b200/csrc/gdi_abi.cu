@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -15,6 +16,7 @@
 #include <vector>
 
 #include "devbuf.hpp"
+#include "host/parallel.hpp"
 #include "gdi.h"
 #include "kernels.cuh"
 #include "launch.hpp"
@@ -109,6 +111,9 @@ struct gdi_session {
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
   DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords, gspins;
   DevBuf live, gsum, gdelta, acc, done, finished, bits;  // k4 state
+  DevTrace* tr = nullptr;              // trace records: s->trace, or pinned host memory
+  unsigned long long* st = nullptr;    // sweep timestamps: s->stamps, or pinned host memory
+  bool host_trace = false;             // one-shot batch: kernels write the trace straight to the host
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool launched = false;
   ~gdi_session() {
@@ -235,21 +240,13 @@ int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int str
     }
     return 0;
   };
-  const int64_t nnz = offsets[n];
-  unsigned threads = std::thread::hardware_concurrency();
-  threads = nnz < (1 << 20) ? 1 : threads < 1 ? 1 : threads > 16 ? 16 : threads;
-  std::vector<int> codes(threads, 0);
-  if (threads == 1) {
-    codes[0] = rows(0, n);
-  } else {
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < threads; t++) {
-      const int32_t lo = static_cast<int32_t>(static_cast<int64_t>(n) * t / threads);
-      const int32_t hi = static_cast<int32_t>(static_cast<int64_t>(n) * (t + 1) / threads);
-      pool.emplace_back([&, t, lo, hi]() { codes[t] = rows(lo, hi); });
-    }
-    for (auto& th : pool) th.join();
-  }
+  // rows are split evenly; below ~1M adjacency entries one thread does it all
+  const size_t min_rows = offsets[n] < (1 << 20) ? static_cast<size_t>(n) + 1 : 0;
+  std::vector<int> codes(16, 0);
+  std::atomic<unsigned> slot{0};
+  parallel_rows(static_cast<size_t>(n), min_rows, [&](size_t lo, size_t hi) {
+    codes[slot.fetch_add(1)] = rows(static_cast<int32_t>(lo), static_cast<int32_t>(hi));
+  });
   for (int c : codes) {
     if (c == 1) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
     if (c == 2) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
@@ -331,8 +328,38 @@ int gdi_graph_query(const gdi_graph* g, gdi_graph_info* info) {
   return GDI_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Pinned, device-mapped trace staging, one per host thread, reused across
+// calls (one-shot batches create a session per call). Sessions that
+// gdi_anneal_batch creates write their trace records straight into it over
+// PCIe while the kernel runs (~32 B per replica-sweep, far below link rate),
+// so no trace copy is left for after the kernel.
+PinnedBuf& trace_stage() {
+  thread_local PinnedBuf stage;
+  return stage;
+}
+
+int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, void* stream, gdi_session** out,
+                   bool host_trace);
+
+}  // namespace
+
+extern "C" {
+
 int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, void* stream,
                        gdi_session** out) {
+  return session_create(g, p, replicas, stream, out, false);
+}
+
+}  // extern "C"
+
+namespace {
+
+int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, void* stream, gdi_session** out,
+                   bool host_trace) {
   if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
   *out = nullptr;
   if (!g) return fail(GDI_ERR_CONFIG, "graph is NULL");
@@ -413,8 +440,21 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   if (s->use_win && s->pplan.gw)
     GDI_CUDA(s->gspins.alloc(static_cast<size_t>(replicas) * s->pplan.n_words));
   if (p->flags & GDI_FLAG_TRACE) {
-    GDI_CUDA(s->trace.alloc(R * S * sizeof(DevTrace)));
-    GDI_CUDA(s->stamps.alloc(R * (S + 1) * sizeof(unsigned long long)));
+    const size_t tb = R * S * sizeof(DevTrace), sb = R * (S + 1) * sizeof(unsigned long long);
+    if (host_trace) {
+      PinnedBuf& stage = trace_stage();
+      GDI_CUDA(stage.ensure(tb + sb));
+      void* d = nullptr;
+      GDI_CUDA(cudaHostGetDevicePointer(&d, stage.p, 0));
+      s->tr = static_cast<DevTrace*>(d);
+      s->st = reinterpret_cast<unsigned long long*>(static_cast<char*>(d) + tb);
+      s->host_trace = true;
+    } else {
+      GDI_CUDA(s->trace.alloc(tb));
+      GDI_CUDA(s->stamps.alloc(sb));
+      s->tr = s->trace.as<DevTrace>();
+      s->st = s->stamps.as<unsigned long long>();
+    }
   }
   if (p->flags & GDI_FLAG_SNAPSHOTS) GDI_CUDA(s->snaps.alloc(R * (S + 1) * n));
   if (s->use_part) {
@@ -434,6 +474,10 @@ int gdi_session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas
   *out = s.release();
   return GDI_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
   if (!s || !seeds) return fail(GDI_ERR_CONFIG, "NULL argument");
@@ -476,8 +520,8 @@ int gdi_session_launch(gdi_session* s) {
       a.done = s->done.as<unsigned int>();
       a.finished = s->finished.as<unsigned int>();
       a.bits = s->bits.as<uint32_t>();
-      a.trace = s->trace.as<DevTrace>();
-      a.stamps = s->stamps.as<unsigned long long>();
+      a.trace = s->tr;
+      a.stamps = s->st;
       a.snaps = s->snaps.as<int8_t>();
       a.final_out = s->final_out.as<DevTrace>();
       a.watchdog = s->watchdog.as<int>();
@@ -517,8 +561,8 @@ int gdi_session_launch(gdi_session* s) {
     a.thr = s->thr_d.as<long long>();
     a.tmask = s->tmask_d.as<unsigned long long>();
     a.spins_out = s->spins.as<int8_t>();
-    a.trace = s->trace.as<DevTrace>();
-    a.stamps = s->stamps.as<unsigned long long>();
+    a.trace = s->tr;
+    a.stamps = s->st;
     a.snaps = s->snaps.as<int8_t>();
     a.final_out = s->final_out.as<DevTrace>();
     GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
@@ -547,8 +591,8 @@ int gdi_session_launch(gdi_session* s) {
     a.a4 = static_cast<int32_t>(4 * s->p.a_num);
     a.b = static_cast<int32_t>(s->p.b_num);
     a.spins_out = s->spins.as<int8_t>();
-    a.trace = s->trace.as<DevTrace>();
-    a.stamps = s->stamps.as<unsigned long long>();
+    a.trace = s->tr;
+    a.stamps = s->st;
     a.snaps = s->snaps.as<int8_t>();
     a.final_out = s->final_out.as<DevTrace>();
     a.watchdog = s->watchdog.as<int>();
@@ -571,8 +615,8 @@ int gdi_session_launch(gdi_session* s) {
   a.a4 = 4 * s->p.a_num;
   a.b = s->p.b_num;
   a.spins_out = s->spins.as<int8_t>();
-  a.trace = s->trace.as<DevTrace>();
-  a.stamps = s->stamps.as<unsigned long long>();
+  a.trace = s->tr;
+  a.stamps = s->st;
   a.snaps = s->snaps.as<int8_t>();
   a.final_out = s->final_out.as<DevTrace>();
   GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
@@ -666,14 +710,17 @@ int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
     const size_t tb = R * S * sizeof(DevTrace), sb = R * (S + 1) * sizeof(unsigned long long);
     // (one buffer per host thread, reused across sessions: one-shot batches
     // create a session per call)
-    thread_local PinnedBuf stage;
-    GDI_CUDA(stage.ensure(tb + sb));
-    GDI_CUDA(cudaMemcpyAsync(stage.p, s->trace.p, tb, cudaMemcpyDeviceToHost, s->stream));
-    GDI_CUDA(cudaMemcpyAsync(stage.as<char>() + tb, s->stamps.p, sb, cudaMemcpyDeviceToHost, s->stream));
-    GDI_CUDA(cudaStreamSynchronize(s->stream));
+    PinnedBuf& stage = trace_stage();
+    if (!s->host_trace) {  // else the kernels wrote the records there already
+      GDI_CUDA(stage.ensure(tb + sb));
+      GDI_CUDA(cudaMemcpyAsync(stage.p, s->trace.p, tb, cudaMemcpyDeviceToHost, s->stream));
+      GDI_CUDA(cudaMemcpyAsync(stage.as<char>() + tb, s->stamps.p, sb, cudaMemcpyDeviceToHost, s->stream));
+      GDI_CUDA(cudaStreamSynchronize(s->stream));
+    }
     const DevTrace* tr = stage.as<DevTrace>();
     const unsigned long long* st = reinterpret_cast<const unsigned long long*>(stage.as<char>() + tb);
-    for (size_t r = 0; r < R; r++)
+    parallel_rows(R, 64 * 1024 / (S + 1) + 1, [&](size_t r0, size_t r1) {
+    for (size_t r = r0; r < r1; r++)
       for (size_t k = 0; k < S; k++) {
         const DevTrace& d = tr[r * S + k];
         if (out->counters) out->counters[r * S + k] = d.counter;
@@ -687,6 +734,7 @@ int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
           t.seconds = static_cast<double>(st[r * (S + 1) + k + 1] - st[r * (S + 1) + k]) * 1e-9;
         }
       }
+    });
   }
   if (out->snapshots) {
     if (!(s->p.flags & GDI_FLAG_SNAPSHOTS))
@@ -725,7 +773,8 @@ int gdi_anneal_batch(const gdi_graph* g, const gdi_params* p, const uint64_t* se
   if (out->trace || out->counters) q.flags |= GDI_FLAG_TRACE;
   if (out->snapshots) q.flags |= GDI_FLAG_SNAPSHOTS;
   gdi_session* s = nullptr;
-  int rc = gdi_session_create(g, &q, replicas, nullptr, &s);
+  // trace written by the kernels straight into pinned host memory (fetched from there below)
+  int rc = session_create(g, &q, replicas, nullptr, &s, (q.flags & GDI_FLAG_TRACE) != 0);
   if (rc) return rc;
   std::unique_ptr<gdi_session, int (*)(gdi_session*)> guard(s, gdi_session_destroy);
   if ((rc = gdi_session_set_seeds(s, seeds))) return rc;
