@@ -50,7 +50,70 @@ struct Xoshiro {
     s3 = rotl64(s3, 45);
     return out;
   }
+
+  // the state transition alone (next() without its output)
+  __host__ __device__ __forceinline__ void step() {
+    const uint64_t t = s1 << 17;
+    s2 ^= s0;
+    s3 ^= s1;
+    s1 ^= s2;
+    s0 ^= s3;
+    s2 ^= t;
+    s3 = rotl64(s3, 45);
+  }
+
+  // Jump ahead J draws: the transition is linear over GF(2), so J steps are
+  // one 256x256 bit matrix (xoshiro_jump_matrix). jm = the matrix in shared
+  // memory as 256 columns of 8 uint32 (the state words' little-endian
+  // halves); column c = the state J steps after the unit state with only
+  // bit c set (bit c = bit c%32 of half c/32). Every lane reads the same
+  // column at the same time (shared-memory broadcast).
+  __device__ __forceinline__ void jump(const uint32_t* jm) {
+    uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0, o4 = 0, o5 = 0, o6 = 0, o7 = 0;
+    const uint32_t w[8] = {static_cast<uint32_t>(s0), static_cast<uint32_t>(s0 >> 32),
+                           static_cast<uint32_t>(s1), static_cast<uint32_t>(s1 >> 32),
+                           static_cast<uint32_t>(s2), static_cast<uint32_t>(s2 >> 32),
+                           static_cast<uint32_t>(s3), static_cast<uint32_t>(s3 >> 32)};
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      uint32_t x = w[q];
+      const uint4* col = reinterpret_cast<const uint4*>(jm) + 2 * (q * 32 + 31);
+#pragma unroll 8
+      for (int b = 31; b >= 0; b--) {  // top bit first: m = all ones if bit b is set
+        const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(x) >> 31);
+        x <<= 1;
+        const uint4 c0 = col[0], c1 = col[1];
+        col -= 2;
+        o0 ^= c0.x & m;
+        o1 ^= c0.y & m;
+        o2 ^= c0.z & m;
+        o3 ^= c0.w & m;
+        o4 ^= c1.x & m;
+        o5 ^= c1.y & m;
+        o6 ^= c1.z & m;
+        o7 ^= c1.w & m;
+      }
+    }
+    s0 = o0 | (static_cast<uint64_t>(o1) << 32);
+    s1 = o2 | (static_cast<uint64_t>(o3) << 32);
+    s2 = o4 | (static_cast<uint64_t>(o5) << 32);
+    s3 = o6 | (static_cast<uint64_t>(o7) << 32);
+  }
 };
+
+// Host: the J-step jump matrix for Xoshiro::jump (256 columns x 4 uint64).
+inline void xoshiro_jump_matrix(uint64_t J, uint64_t* out) {
+  for (int c = 0; c < 256; c++) {
+    uint64_t e[4] = {0, 0, 0, 0};
+    e[c / 64] = 1ull << (c % 64);
+    Xoshiro r{e[0], e[1], e[2], e[3]};
+    for (uint64_t i = 0; i < J; i++) r.step();
+    out[4 * c + 0] = r.s0;
+    out[4 * c + 1] = r.s1;
+    out[4 * c + 2] = r.s2;
+    out[4 * c + 3] = r.s3;
+  }
+}
 
 // Philox4x32-10 (Salmon et al., SC'11). Returns four 32-bit words.
 struct Philox4 {

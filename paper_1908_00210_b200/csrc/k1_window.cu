@@ -37,7 +37,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "device_rng.cuh"
 #include "kernels.cuh"
@@ -48,15 +52,12 @@ namespace gdi {
 
 namespace {
 
-constexpr int kRing = 256;  // draws buffered per replica (power of two, >= 34 + kGen)
-#ifndef K1W_GEN
-#define K1W_GEN 64
+// Draw ring per replica: nr rounds of kp segments of L draws (kp lanes of the
+// producer warp per stream; nr, L chosen per plan to fit shared memory)
+constexpr int kRingMax = 4096;
+#ifndef K1W_PROF
+#define K1W_PROF 0  // 1: step statistics (GDI_PIPE_DEBUG=4) and the no-wait timing mode (8)
 #endif
-// draws per producer batch, fully unrolled: one acquire + one release per
-// batch; 8 -> 16 -> 32 -> 64 measured 73.7 -> 63.8 -> 58.2 -> 54.8 ms on G22 x1024
-// x1000 sweeps (128 fully unrolled thrashed the instruction cache)
-constexpr int kGen = K1W_GEN;
-static_assert(kRing % kGen == 0, "producer batches must not wrap the ring");
 constexpr long long kWatchdog = 1LL << 28;  // polling iterations before aborting (~seconds)
 
 // spin of SELL entry idx (bit 31 = weight -1; padding index n reads 0)
@@ -70,16 +71,18 @@ __device__ __forceinline__ int nbv(const int8_t* s, int idx) {
 }
 
 struct WinLayout {
-  int ring, genpos, cons, flags, spins, fields, total;
-  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, bool incf) {
+  int ring, jump, genpos, cons, flags, spins, fields, masks, total;
+  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, bool incf, int ring_n, int mask_words = 0) {
     WinLayout L;
     L.ring = 0;
-    L.genpos = L.ring + rc * kRing * 8;
+    L.jump = L.ring + rc * ring_n * 8;  // 256 x 32 B jump matrix
+    L.genpos = L.jump + 256 * 32;
     L.cons = L.genpos + 4 * 32;
     L.flags = L.cons + 4 * 32;  // [0] consumers done, [1] abort
     L.spins = L.flags + 16;
     L.fields = L.spins + (gs ? 0 : rc * n_pad);
-    L.total = L.fields + (incf ? rc * n_pad * 2 : 0);
+    L.masks = (L.fields + (incf ? rc * n_pad * 2 : 0) + 15) & ~15;
+    L.total = L.masks + mask_words * n_pad * 4;
     return L;
   }
 };
@@ -95,8 +98,25 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rc = a.rc;  // replica warps 0..rc-1, producer warps rc..rc+nprod-1
   const int n_pad = a.n_words;
-  const WinLayout L = WinLayout::make(rc, n_pad, GS, INCF);
+  const int kp = a.kp, SL = a.segl, ringN = a.rounds * kp * SL, rmask = ringN - 1;
+  const WinLayout L = WinLayout::make(rc, n_pad, GS, INCF, ringN);
   uint64_t* ring = reinterpret_cast<uint64_t*>(smem + L.ring);
+  uint32_t* jm = reinterpret_cast<uint32_t*>(smem + L.jump);
+  if (kp > 1)
+    for (int i = threadIdx.x; i < 256 * 4; i += blockDim.x)
+      reinterpret_cast<uint64_t*>(jm)[i] = __ldg(a.jump + i);
+  // window masks: a per-CTA shared-memory copy when it fits (plan), else global
+  const uint32_t* wpp = a.win_pos;
+  const uint32_t* wnp = a.win_neg;
+  if (a.masks_smem) {
+    uint32_t* wm = reinterpret_cast<uint32_t*>(smem + L.masks);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      wm[i] = __ldg(a.win_pos + i);
+      if (SIGNED) wm[n_pad + i] = __ldg(a.win_neg + i);
+    }
+    wpp = wm;
+    wnp = wm + n_pad;
+  }
   int* genpos = reinterpret_cast<int*>(smem + L.genpos);
   int* cons = reinterpret_cast<int*>(smem + L.cons);
   int* flags = reinterpret_cast<int*>(smem + L.flags);
@@ -118,31 +138,48 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const int cw = rm1 ? (warp % 4 == 3 ? -1 : warp - warp / 4) : (producer ? -1 : warp);
   if (!producer && (cw < 0 || cw >= rc)) return;  // idle padding warp
   if (producer) {
-    // ============================ producers ============================
-    // producer warp p serves replicas l = p, p + np, ... (lane = l / np): a
-    // stream costs ~25 instructions per draw, so one warp for all replicas
-    // could not keep up with the consumers
-    const int np = a.nprod, l = (rm1 ? 0 : warp - rc) + lane * np;
+    // ============================ producer ============================
+    // kp lanes per replica stream (lane = l * kp + j): the stream is cut into
+    // rounds of kp segments of SL draws, lane j generating segment j of every
+    // round and then jumping (kp-1)*SL draws ahead to its segment of the next
+    // round (Xoshiro::jump). A stream alone on one lane issues ~17 ALU
+    // instructions per draw, one warp instruction every other cycle: ~36
+    // cycles per draw, slower than a consumer visit; kp lanes side by side
+    // cut that by ~kp (minus the jump, ~10 ALU instructions per matrix column
+    // amortised over SL draws). Rounds cycle through the ring (index = draw
+    // position mod rounds*kp*SL) and are published whole; several rounds
+    // buffered absorb the warp serving the replicas' rounds at different
+    // times (a replica's round waits while others' are generated).
+    const int round = kp * SL;
+    const int l = lane / kp, j = lane % kp;
     const int r = blockIdx.x * rc + l;
     const bool act = l < rc && r < a.replicas;
     Xoshiro rng = Xoshiro::stream(act ? a.seeds[r] : 0ull, 1);  // anneal.cpp:191
-    uint64_t* my = ring + (act ? l : 0) * kRing;
+    for (int i = 0; i < j * SL; i++) rng.step();                 // to this lane's first segment
+    uint64_t* my = ring + (act ? l : 0) * ringN + j * SL;
     const unsigned gp_s = saddr(genpos + (act ? l : 0)), cs_s = saddr(cons + (act ? l : 0));
-    int gen = 0;
+    int gen = 0;  // draws published for this replica (whole rounds)
 #pragma unroll 1
     for (long long spin = 0;; spin++) {
-      const bool can = act && gen + kGen <= ld_acquire(cs_s) + kRing;
+      // one consumer position per replica group (the group's lanes must agree)
+      const int cpos = __shfl_sync(0xffffffffu, act ? ld_acquire(cs_s) : 0, lane - j);
+      const bool can = act && gen + round <= cpos + ringN;
       if (can) {
-        uint64_t* dst = my + (gen & (kRing - 1));  // batches are kGen-aligned and kGen | kRing: no wrap
+        uint64_t* dst = my + ((gen / round) & (a.rounds - 1)) * round;
+#pragma unroll 1
+        for (int b = 0; b < SL; b += 32) {
 #pragma unroll
-        for (int k = 0; k < kGen; k++) dst[k] = rng.next();
-        gen += kGen;
-        st_release(gp_s, gen);
+          for (int k = 0; k < 32; k++) dst[b + k] = rng.next();
+        }
+        if (kp > 1) rng.jump(jm);
+        gen += round;
+        __threadfence_block();  // this lane's draws before the group's release
       }
+      __syncwarp();
+      if (can && j == 0) st_release(gp_s, gen);
       if (!__any_sync(0xffffffffu, can)) {
         // ring full: a short sleep keeps this warp's polling off the issue
-        // slots the consumers need (measured: spinning, or 4 producer warps,
-        // were both slower than one sleeping producer)
+        // slots the consumers need
         if (ld_acquire(done_s) >= rc || ld_acquire(abort_s)) break;
         __nanosleep(32);
         if (spin > kWatchdog) {
@@ -215,17 +252,39 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   bool en = a.thr[0] >= 0;
   int own = 0, f = 0;
   uint32_t wp = 0u, wn = 0u;
-  const uint64_t* myring = ring + cw * kRing;
+  const uint64_t* myring = ring + cw * ringN;
   const unsigned gp_s = saddr(genpos + cw), cs_s = saddr(cons + cw);
   int gp = 0;
+  int pub = 0;                    // last published consumer position (round-aligned)
+  const int round_w = kp * SL;    // producer round (power of two)
   bool aborted = false;
+  // loop invariants through a shuffle: kept in registers instead of being
+  // re-read from the parameter bank on the step's dependency chain
+  const int nn = __shfl_sync(FULL, n, 0);
+  const int nsw = __shfl_sync(FULL, sweeps, 0);
+  // INCF deferred scatter: a spin change is scattered into the fields one step
+  // later, off the step's critical path. The next step's window is the 32
+  // vertices after the changed one, so its lanes add the change through the
+  // window masks instead (bit lane of win_pos/win_neg: the vertex 1 + lane
+  // places back is a +1/-1 neighbour); the scatter itself is applied after
+  // that step's refill loads and before the next ones. Rows of up to 128
+  // entries (four targets per lane); longer rows scatter synchronously.
+  constexpr bool defer = INCF;
+  int sd = 0;                     // pending change (0 = none)
+  int se0 = 0, se1 = 0;           // its CSR row
+  int sc[4] = {-1, -1, -1, -1}, sw[4] = {1, 1, 1, 1};
+#if K1W_PROF
   const bool prof = (a.debug & 4) != 0 && a.prof != nullptr;  // GDI_PIPE_DEBUG=4: step statistics
+  const bool nowait = (a.debug & 8) != 0;                     // timing experiment: ignore the ring
+#else
+  constexpr bool prof = false, nowait = false;
+#endif
   unsigned long long p_steps = 0, p_acc = 0, p_fill = 0, p_wait = 0, p_t0 = prof ? clock64() : 0;
 
 #pragma unroll 1
-  while (sweep < sweeps) {
+  while (sweep < nsw) {
     // refill the empty lanes [F, lim) of the window (vertex i0 + lane)
-    const int lim = min(32, n - i0);
+    const int lim = min(32, nn - i0);
     const long long p_a = prof ? clock64() : 0;
     if (lane >= F && lane < lim) {
       const int v = i0 + lane;
@@ -247,16 +306,26 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         }
         for (; k < kmax; k++) f += nbv<SIGNED>(s, __ldg(rowp + k * 32));
       }
-      if (!INCF) {
-        wp = __ldg(a.win_pos + v);
-        wn = SIGNED ? __ldg(a.win_neg + v) : 0u;
-      }
+      wp = wpp[v];
+      wn = SIGNED ? wnp[v] : 0u;
     }
     F = lim;
+    if (defer && sd != 0) {
+      // targets of the pending scatter (its row bounds were loaded at the event)
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int e = se0 + lane + 32 * q;
+        sc[q] = e < se1 ? __ldg(col + e) : -1;
+        if (SIGNED) sw[q] = e < se1 ? __ldg(wgt + e) : 0;
+      }
+      // the window misses the pending change in fld: add it through the masks
+      if ((wp >> lane) & 1u) f += sd;
+      if (SIGNED && ((wn >> lane) & 1u)) f -= sd;
+    }
     if (prof) p_fill += clock64() - p_a;
     // draws pos .. pos + F must be in the ring
     const long long p_w = prof ? clock64() : 0;
-    if (gp < pos + F + 1 && !(a.debug & 8)) {
+    if (gp < pos + F + 1 && !nowait) {
       for (long long k = 0; (gp = ld_acquire(gp_s)) < pos + F + 1; k++)
         if (k > kWatchdog || ld_acquire(abort_s)) {
           aborted = true;
@@ -266,41 +335,57 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     }
     if (prof) p_wait += clock64() - p_w;
     const bool act = lane < F;
-    const uint64_t d0 = myring[(pos + lane) & (kRing - 1)];
-    const uint64_t d1 = myring[(pos + lane + 1) & (kRing - 1)];
+    const uint64_t d0 = myring[(pos + lane) & rmask];
+    const uint64_t d1 = myring[(pos + lane + 1) & rmask];
     const int diff = UNITAB ? AG - own - f : AG - a4 * own - bb * f;
     const bool tie = diff == 0;
     const int c = diff < 0 ? 1 : diff > 0 ? -1 : (static_cast<long long>(d0) < 0 ? 1 : -1);
     const uint64_t u = tie ? d1 : d0;
     const int fin = (en && u <= tm) ? -c : c;
+    // the pending scatter: its field loads now (this step's refill loads are
+    // issued), the stores at the end of the step
+    int sv[4];
+    const int sdp = sd;
+    if (defer && sdp != 0) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) sv[q] = sc[q] >= 0 ? fld[sc[q]] : 0;
+      sd = 0;
+    }
     const unsigned m = __ballot_sync(FULL, act && (fin != own || tie));
     int adv;
+    bool wrote = defer && sdp != 0;  // shared-memory stores this step (warp-uniform)
     if (m == 0u) {
       adv = F;
       pos += F;
     } else {
       const int js = __ffs(m) - 1;
       adv = js + 1;
-      const int fs = __shfl_sync(FULL, fin, js), os = __shfl_sync(FULL, own, js);
-      const int ts = __shfl_sync(FULL, tie ? 1 : 0, js), fj = __shfl_sync(FULL, f, js);
+      int fs, os, ts, fj;
+      if (INCF) {  // |field| < 2^15: the event lane's values in one shuffle
+        const int key = __shfl_sync(FULL, (f << 3) | (fin > 0 ? 4 : 0) | (own > 0 ? 2 : 0) | (tie ? 1 : 0), js);
+        fs = (key & 4) ? 1 : -1;
+        os = (key & 2) ? 1 : -1;
+        ts = key & 1;
+        fj = key >> 3;
+      } else {
+        const int key = __shfl_sync(FULL, (fin > 0 ? 4 : 0) | (own > 0 ? 2 : 0) | (tie ? 1 : 0), js);
+        fs = (key & 4) ? 1 : -1;
+        os = (key & 2) ? 1 : -1;
+        ts = key & 1;
+        fj = __shfl_sync(FULL, f, js);
+      }
       pos += adv + ts;
       if (fs != os) {
+        wrote = true;
         if (lane == js) s[i0 + js] = static_cast<int8_t>(fs);
         const int d = fs - os;
         AG += UNITAB ? d : a4 * d;
         dcut -= (d >> 1) * fj;
-        if (INCF) {
-          // scatter the change into the neighbours' fields (a row has no
-          // repeated neighbour, so the lanes' updates never collide), then the
-          // pending lanes reload theirs
-          const int v = i0 + js;
-          const int e1 = __ldg(off + v + 1);
-          for (int e = __ldg(off + v) + lane; e < e1; e += 32) {
-            const int u = __ldg(col + e);
-            fld[u] = static_cast<int16_t>(fld[u] + (SIGNED ? __ldg(wgt + e) * d : d));
-          }
-          __syncwarp();
-          if (lane > js && lane < F) f = fld[i0 + lane];
+        if (defer) {
+          const int v = i0 + js;  // row loads in flight until the next step
+          se0 = __ldg(off + v);
+          se1 = __ldg(off + v + 1);
+          sd = d;
         } else {
           const int k = lane - js;  // pending lanes behind the event: field correction
           if (k >= 1) {
@@ -308,22 +393,49 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
             if (SIGNED && ((wn >> (k - 1)) & 1u)) f -= d;
           }
         }
-        __syncwarp();
       }
     }
-    // ring slots before pos are consumed (release: their loads are done)
-    if (lane == 0) st_release(cs_s, pos);
-    own = __shfl_down_sync(FULL, own, adv);
-    f = __shfl_down_sync(FULL, f, adv);
-    wp = __shfl_down_sync(FULL, wp, adv);
-    wn = __shfl_down_sync(FULL, wn, adv);
+    if (defer && sdp != 0) {
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        if (sc[q] >= 0) fld[sc[q]] = static_cast<int16_t>(sv[q] + (SIGNED ? sw[q] * sdp : sdp));
+    }
+    if (wrote) __syncwarp();  // this step's shared-memory stores before the next step's loads
+    // ring slots before pos are consumed (release: their loads are done);
+    // the producer works in whole rounds, so only round crossings are published
+    if ((pos & ~(round_w - 1)) != pub) {
+      if (lane == 0) st_release(cs_s, pos);
+      pub = pos & ~(round_w - 1);
+    }
+    if (INCF) {  // spin and field of the pending lanes in one shuffle
+      const int pk = __shfl_down_sync(FULL, (f << 1) | (own > 0 ? 1 : 0), adv);
+      own = (pk & 1) ? 1 : -1;
+      f = pk >> 1;
+      if (defer) {
+        wp = __shfl_down_sync(FULL, wp, adv);
+        if (SIGNED) wn = __shfl_down_sync(FULL, wn, adv);
+      }
+    } else {
+      own = __shfl_down_sync(FULL, own, adv);
+      f = __shfl_down_sync(FULL, f, adv);
+      wp = __shfl_down_sync(FULL, wp, adv);
+      if (SIGNED) wn = __shfl_down_sync(FULL, wn, adv);
+    }
     F -= adv;
     i0 += adv;
     if (prof) {
       p_steps++;
       p_acc += adv;
     }
-    if (i0 == n) {  // record_barrier (anneal.cpp:165-187)
+    if (i0 == nn) {  // record_barrier (anneal.cpp:165-187)
+      if (defer && sd != 0) {  // flush the pending scatter before the next sweep's refills
+        for (int e = se0 + lane; e < se1; e += 32) {
+          const int uu = __ldg(col + e);
+          fld[uu] = static_cast<int16_t>(fld[uu] + (SIGNED ? __ldg(wgt + e) * sd : sd));
+        }
+        sd = 0;
+        __syncwarp();
+      }
       cutv += dcut;
       dcut = 0;
       const int Gs = UNITAB ? AG : AG / a4;
@@ -336,7 +448,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       sweep++;
       i0 = 0;
       F = 0;
-      if (sweep < sweeps) {
+      if (sweep < nsw) {
         tm = a.tmask[sweep];
         en = a.thr[sweep] >= 0;
       }
@@ -377,7 +489,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
                 PipePlan* plan) {
   if (!pg.ok) return -1;
   // draw positions are 32-bit: at most one visit + one tie coin per visit
-  if (2.0 * static_cast<double>(sweeps) * st.n + 2 * kRing >= 2147483647.0) return -1;
+  if (2.0 * static_cast<double>(sweeps) * st.n + 2 * kRingMax >= 2147483647.0) return -1;
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
   while (y) {
     const long long t = x % y;
@@ -391,21 +503,41 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   rc = rc < 1 ? 1 : rc > 12 ? 12 : rc;  // block <= 512 threads (__launch_bounds__) with role padding
   const int n_pad = (st.n + 1 + 15) & ~15;
   const char* force = std::getenv("GDI_FORCE_KERNEL");
-  const bool gs = WinLayout::make(rc, n_pad, false, false).total > 200 * 1024 ||
+  // producer lanes per replica stream: the largest power of two <= 32 / rc (<= 8)
+  int kp = 1;
+  while (kp < 8 && 2 * kp * rc <= 32) kp *= 2;
+  if (const char* e = std::getenv("GDI_WINDOW_KP")) kp = std::atoi(e);  // tuning experiments
+  int nr = 4;  // rounds buffered per replica
+  if (const char* e = std::getenv("GDI_WINDOW_NR")) nr = std::atoi(e);
+  const int cap = 227 * 1024, ring_min = nr * kp * 32;  // sm_100 dynamic shared memory per CTA
+  const bool gs = WinLayout::make(rc, n_pad, false, false, ring_min).total > cap ||
                   (force && std::string(force) == "window_gmem");
   // incremental fields when they fit next to the spins (int16 bound)
-  const bool incf = !gs && st.max_abs_field < 32768 && WinLayout::make(rc, n_pad, false, true).total <= 200 * 1024 &&
+  const bool incf = !gs && st.max_abs_field < 32768 && st.max_degree <= 128 &&
+                    WinLayout::make(rc, n_pad, false, true, ring_min).total <= cap &&
                     !(force && std::string(force) == "window_masks");
+  // segment length: the longest that fits (amortises the jump over more draws)
+  int segl = 32;
+  for (int c : {256, 128, 64})
+    if (nr * kp * c <= kRingMax && WinLayout::make(rc, n_pad, gs, incf, nr * kp * c).total <= cap) {
+      segl = c;
+      break;
+    }
+  if (const char* e = std::getenv("GDI_WINDOW_SEGL")) segl = std::atoi(e);
+  // window masks in shared memory when they still fit with that segment length
+  const int mw = st.unit ? 1 : 2;
+  const bool msm = WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, mw).total <= cap;
+  plan->kp = kp;
+  plan->segl = segl;
+  plan->masks_smem = msm;
+  plan->rounds = nr;
   const bool unitab = ra == 1 && rb == 1;
   plan->fn = st.unit ? (unitab ? win_fn<false, true>(gs, incf) : win_fn<false, false>(gs, incf))
                      : (unitab ? win_fn<true, true>(gs, incf) : win_fn<true, false>(gs, incf));
   plan->prof = false;
   plan->gw = gs;
   plan->rc = rc;
-  // one producer warp: a stream costs ~36 cycles per draw on one lane (the
-  // per-warp ALU issue rate, tools/xoshiro_micro.cu), which bounds a replica
-  // at ~1 visit per ~40 cycles; more producer warps did not help (issue
-  // contention with the consumers)
+  // one producer warp, kp lanes per stream (see the kernel)
   plan->nprod = 1;
   const char* rm = std::getenv("GDI_WINDOW_ROLEMAP");  // tuning experiments
   plan->rolemap = rm ? std::atoi(rm) : 1;
@@ -416,7 +548,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
     plan->block = 32 * (rc + plan->nprod);
   }
   plan->grid = (replicas + rc - 1) / rc;
-  plan->smem = WinLayout::make(rc, n_pad, gs, incf).total;
+  plan->smem = WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, msm ? mw : 0).total;
   plan->n_words = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
@@ -441,6 +573,32 @@ cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream
   a.n_words = plan.n_words;
   a.nprod = plan.nprod;
   a.rolemap = plan.rolemap;
+  a.kp = plan.kp;
+  a.segl = plan.segl;
+  a.rounds = plan.rounds;
+  a.masks_smem = plan.masks_smem ? 1 : 0;
+  a.jump = nullptr;
+  if (plan.kp > 1) {
+    // the (kp-1)*segl-draw jump matrix, built once per device and distance
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, uint64_t*> cache;
+    int dev = 0;
+    if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
+    const int J = (plan.kp - 1) * plan.segl;
+    std::lock_guard<std::mutex> lock(mu);
+    uint64_t*& d = cache[{dev, J}];
+    if (d == nullptr) {
+      std::vector<uint64_t> h(256 * 4);
+      xoshiro_jump_matrix(static_cast<uint64_t>(J), h.data());
+      if ((err = cudaMalloc(&d, h.size() * sizeof(uint64_t))) != cudaSuccess) {
+        d = nullptr;
+        return err;
+      }
+      if ((err = cudaMemcpy(d, h.data(), h.size() * sizeof(uint64_t), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return err;
+    }
+    a.jump = d;
+  }
   const char* dbg = std::getenv("GDI_PIPE_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
   void* params[] = {&a};

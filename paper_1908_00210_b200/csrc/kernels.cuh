@@ -59,6 +59,11 @@ struct PipeArgs {
   const int32_t* wsell_off;
   int32_t nprod;                   // k1_window: RNG producer warps
   int32_t rolemap;                 // k1_window: warp role layout (see k1_window.cu)
+  int32_t kp;                      // k1_window: producer lanes per replica stream
+  int32_t segl;                    // k1_window: draws per producer segment
+  int32_t rounds;                  // k1_window: producer rounds buffered per replica (power of two)
+  int32_t masks_smem;              // k1_window: window masks copied to shared memory
+  const uint64_t* jump;            // k1_window: (kp-1)*segl-draw xoshiro jump matrix [256][4]
   int32_t sweeps;
   int32_t replicas;
   int32_t rc;                      // replicas (lanes) per CTA

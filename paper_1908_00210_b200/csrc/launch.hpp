@@ -56,6 +56,10 @@ struct PipePlan {
   int n_words = 0;  // k1_window: per-replica spin stride
   int nprod = 1;    // k1_window: RNG producer warps
   int rolemap = 1;  // k1_window: warp role layout
+  int kp = 1;       // k1_window: producer lanes per replica stream
+  int segl = 64;    // k1_window: draws per producer segment
+  int rounds = 4;   // k1_window: producer rounds buffered per replica
+  bool masks_smem = false;  // k1_window: window masks in shared memory
   const char* name = "";
 };
 
