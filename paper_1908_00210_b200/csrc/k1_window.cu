@@ -55,6 +55,15 @@ namespace {
 // Draw ring per replica: nr rounds of kp segments of L draws (kp lanes of the
 // producer warp per stream; nr, L chosen per plan to fit shared memory)
 constexpr int kRingMax = 4096;
+#ifndef K1W_SPEC
+#define K1W_SPEC 1  // draws read before the ring check
+#endif
+#ifndef K1W_LATEPK
+#define K1W_LATEPK 0  // refill loads issued before the shifted lanes are decoded
+#endif
+#ifndef K1W_MSEL
+#define K1W_MSEL 0  // masks: explicit shared/global selection (else generic pointer)
+#endif
 #ifndef K1W_PROF
 #define K1W_PROF 0  // 1: step statistics (GDI_PIPE_DEBUG=4) and the no-wait timing mode (8)
 #endif
@@ -106,17 +115,12 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     for (int i = threadIdx.x; i < 256 * 4; i += blockDim.x)
       reinterpret_cast<uint64_t*>(jm)[i] = __ldg(a.jump + i);
   // window masks: a per-CTA shared-memory copy when it fits (plan), else global
-  const uint32_t* wpp = a.win_pos;
-  const uint32_t* wnp = a.win_neg;
-  if (a.masks_smem) {
-    uint32_t* wm = reinterpret_cast<uint32_t*>(smem + L.masks);
+  uint32_t* wm = reinterpret_cast<uint32_t*>(smem + L.masks);
+  if (a.masks_smem)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       wm[i] = __ldg(a.win_pos + i);
       if (SIGNED) wm[n_pad + i] = __ldg(a.win_neg + i);
     }
-    wpp = wm;
-    wnp = wm + n_pad;
-  }
   int* genpos = reinterpret_cast<int*>(smem + L.genpos);
   int* cons = reinterpret_cast<int*>(smem + L.cons);
   int* flags = reinterpret_cast<int*>(smem + L.flags);
@@ -262,6 +266,8 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   // re-read from the parameter bank on the step's dependency chain
   const int nn = __shfl_sync(FULL, n, 0);
   const int nsw = __shfl_sync(FULL, sweeps, 0);
+  const bool msm = __shfl_sync(FULL, a.masks_smem, 0) != 0;
+  int pk = 0;  // INCF: (field << 1 | spin > 0) of the pending lanes, shifted at the end of a step
   // INCF deferred scatter: a spin change is scattered into the fields one step
   // later, off the step's critical path. The next step's window is the 32
   // vertices after the changed one, so its lanes add the change through the
@@ -286,12 +292,33 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     // refill the empty lanes [F, lim) of the window (vertex i0 + lane)
     const int lim = min(32, nn - i0);
     const long long p_a = prof ? clock64() : 0;
-    if (lane >= F && lane < lim) {
+    const bool rl = lane >= F && lane < lim;
+    int r_own = 0, r_f = 0;
+    uint32_t r_wp = 0u, r_wn = 0u;
+    if (rl) {  // loads first; the pending lanes' shifted values are decoded after
       const int v = i0 + lane;
-      own = s[v];
+      r_own = s[v];
+#if K1W_MSEL
+      r_wp = msm ? wm[v] : __ldg(a.win_pos + v);
+      if (SIGNED) r_wn = msm ? wm[n_pad + v] : __ldg(a.win_neg + v);
+#else
+      r_wp = (msm ? static_cast<const uint32_t*>(wm) : a.win_pos)[v];
+      if (SIGNED) r_wn = (msm ? static_cast<const uint32_t*>(wm) + n_pad : a.win_neg)[v];
+#endif
+      if (INCF) r_f = fld[v];
+    }
+    if (INCF && K1W_LATEPK) {
+      own = (pk & 1) ? 1 : -1;
+      f = pk >> 1;
+    }
+    if (rl) {
+      const int v = i0 + lane;
+      own = r_own;
+      wp = r_wp;
+      wn = r_wn;
       f = 0;
       if (INCF) {
-        f = fld[v];
+        f = r_f;
       } else {
         const int c = v >> 5, l = v & 31;
         const int b0 = __ldg(a.wsell_off + c), kmax = __ldg(a.wsell_off + c + 1) - b0;
@@ -306,8 +333,6 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         }
         for (; k < kmax; k++) f += nbv<SIGNED>(s, __ldg(rowp + k * 32));
       }
-      wp = wpp[v];
-      wn = SIGNED ? wnp[v] : 0u;
     }
     F = lim;
     if (defer && sd != 0) {
@@ -323,7 +348,14 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       if (SIGNED && ((wn >> lane) & 1u)) f -= sd;
     }
     if (prof) p_fill += clock64() - p_a;
-    // draws pos .. pos + F must be in the ring
+    // draws pos .. pos + F must be in the ring: read speculatively (they are
+    // when the last acquired generator position covers them) and re-read
+    // after waiting otherwise
+    uint64_t d0 = 0, d1 = 0;
+    if (K1W_SPEC) {
+      d0 = myring[(pos + lane) & rmask];
+      d1 = myring[(pos + lane + 1) & rmask];
+    }
     const long long p_w = prof ? clock64() : 0;
     if (gp < pos + F + 1 && !nowait) {
       for (long long k = 0; (gp = ld_acquire(gp_s)) < pos + F + 1; k++)
@@ -332,11 +364,17 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
           break;
         }
       if (aborted) break;
+      if (K1W_SPEC) {
+        d0 = myring[(pos + lane) & rmask];
+        d1 = myring[(pos + lane + 1) & rmask];
+      }
+    }
+    if (!K1W_SPEC) {
+      d0 = myring[(pos + lane) & rmask];
+      d1 = myring[(pos + lane + 1) & rmask];
     }
     if (prof) p_wait += clock64() - p_w;
     const bool act = lane < F;
-    const uint64_t d0 = myring[(pos + lane) & rmask];
-    const uint64_t d1 = myring[(pos + lane + 1) & rmask];
     const int diff = UNITAB ? AG - own - f : AG - a4 * own - bb * f;
     const bool tie = diff == 0;
     const int c = diff < 0 ? 1 : diff > 0 ? -1 : (static_cast<long long>(d0) < 0 ? 1 : -1);
@@ -407,10 +445,12 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       if (lane == 0) st_release(cs_s, pos);
       pub = pos & ~(round_w - 1);
     }
-    if (INCF) {  // spin and field of the pending lanes in one shuffle
-      const int pk = __shfl_down_sync(FULL, (f << 1) | (own > 0 ? 1 : 0), adv);
-      own = (pk & 1) ? 1 : -1;
-      f = pk >> 1;
+    if (INCF) {  // spin and field of the pending lanes in one shuffle (decoded next step)
+      pk = __shfl_down_sync(FULL, (f << 1) | (own > 0 ? 1 : 0), adv);
+      if (!K1W_LATEPK) {
+        own = (pk & 1) ? 1 : -1;
+        f = pk >> 1;
+      }
       if (defer) {
         wp = __shfl_down_sync(FULL, wp, adv);
         if (SIGNED) wn = __shfl_down_sync(FULL, wn, adv);
