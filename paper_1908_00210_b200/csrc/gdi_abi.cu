@@ -87,7 +87,8 @@ struct gdi_graph {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
                                 thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes +
                                 pipel.far_col.bytes + pipel.far_meta.bytes + pipel.win_pos.bytes +
-                                pipel.win_neg.bytes + pipel.wsell.bytes + pipel.wsell_off.bytes);
+                                pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
+                                pipel.wsell_off.bytes);
   }
 };
 
@@ -190,6 +191,8 @@ int ensure_pipe(gdi_graph* g) {
   g->pipe.far_meta = g->pipel.far_meta.as<int4>();
   g->pipe.win_pos = g->pipel.win_pos.as<uint32_t>();
   g->pipe.win_neg = g->pipel.win_neg.as<uint32_t>();
+  g->pipe.fwd_pos = g->pipel.fwd_pos.as<uint32_t>();
+  g->pipe.fwd_neg = g->pipel.fwd_neg.as<uint32_t>();
   g->pipe.wsell = g->pipel.wsell.as<int32_t>();
   g->pipe.wsell_off = g->pipel.wsell_off.as<int32_t>();
   g->pipe_built = true;
@@ -578,6 +581,8 @@ int gdi_session_launch(gdi_session* s) {
     a.far_meta = s->g->pipe.far_meta;
     a.win_pos = s->g->pipe.win_pos;
     a.win_neg = s->g->pipe.win_neg;
+    a.fwd_pos = s->g->pipe.fwd_pos;
+    a.fwd_neg = s->g->pipe.fwd_neg;
     a.wsell = s->g->pipe.wsell;
     a.wsell_off = s->g->pipe.wsell_off;
     a.n_words = s->g->pipe.n_words;

@@ -271,13 +271,15 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   // INCF deferred scatter: a spin change is scattered into the fields one step
   // later, off the step's critical path. The next step's window is the 32
   // vertices after the changed one, so its lanes add the change through the
-  // window masks instead (bit lane of win_pos/win_neg: the vertex 1 + lane
-  // places back is a +1/-1 neighbour); the scatter itself is applied after
-  // that step's refill loads and before the next ones. Rows of up to 128
-  // entries (four targets per lane); longer rows scatter synchronously.
+  // changed vertex's forward masks instead (bit lane of fwd_pos/fwd_neg: the
+  // vertex 1 + lane places ahead is a +1/-1 neighbour; one uniform load at the
+  // event); the scatter itself is applied after that step's refill loads and
+  // before the next ones. INCF requires rows of at most 128 entries (four
+  // targets per lane).
   constexpr bool defer = INCF;
   int sd = 0;                     // pending change (0 = none)
   int se0 = 0, se1 = 0;           // its CSR row
+  uint32_t rmv = 0u, rmn = 0u;    // its forward window masks
   int sc[4] = {-1, -1, -1, -1}, sw[4] = {1, 1, 1, 1};
 #if K1W_PROF
   const bool prof = (a.debug & 4) != 0 && a.prof != nullptr;  // GDI_PIPE_DEBUG=4: step statistics
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     if (rl) {  // loads first; the pending lanes' shifted values are decoded after
       const int v = i0 + lane;
       r_own = s[v];
+      if (!INCF) {
 #if K1W_MSEL
       r_wp = msm ? wm[v] : __ldg(a.win_pos + v);
       if (SIGNED) r_wn = msm ? wm[n_pad + v] : __ldg(a.win_neg + v);
@@ -305,6 +308,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       r_wp = (msm ? static_cast<const uint32_t*>(wm) : a.win_pos)[v];
       if (SIGNED) r_wn = (msm ? static_cast<const uint32_t*>(wm) + n_pad : a.win_neg)[v];
 #endif
+      }
       if (INCF) r_f = fld[v];
     }
     if (INCF && K1W_LATEPK) {
@@ -343,9 +347,10 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         sc[q] = e < se1 ? __ldg(col + e) : -1;
         if (SIGNED) sw[q] = e < se1 ? __ldg(wgt + e) : 0;
       }
-      // the window misses the pending change in fld: add it through the masks
-      if ((wp >> lane) & 1u) f += sd;
-      if (SIGNED && ((wn >> lane) & 1u)) f -= sd;
+      // the window misses the pending change in fld: add it through the changed
+      // vertex's forward masks (loaded at the event)
+      if ((rmv >> lane) & 1u) f += sd;
+      if (SIGNED && ((rmn >> lane) & 1u)) f -= sd;
     }
     if (prof) p_fill += clock64() - p_a;
     // draws pos .. pos + F must be in the ring: read speculatively (they are
@@ -423,6 +428,8 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
           const int v = i0 + js;  // row loads in flight until the next step
           se0 = __ldg(off + v);
           se1 = __ldg(off + v + 1);
+          rmv = __ldg(a.fwd_pos + v);
+          if (SIGNED) rmn = __ldg(a.fwd_neg + v);
           sd = d;
         } else {
           const int k = lane - js;  // pending lanes behind the event: field correction
@@ -451,10 +458,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         own = (pk & 1) ? 1 : -1;
         f = pk >> 1;
       }
-      if (defer) {
-        wp = __shfl_down_sync(FULL, wp, adv);
-        if (SIGNED) wn = __shfl_down_sync(FULL, wn, adv);
-      }
+
     } else {
       own = __shfl_down_sync(FULL, own, adv);
       f = __shfl_down_sync(FULL, f, adv);
@@ -566,7 +570,8 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   if (const char* e = std::getenv("GDI_WINDOW_SEGL")) segl = std::atoi(e);
   // window masks in shared memory when they still fit with that segment length
   const int mw = st.unit ? 1 : 2;
-  const bool msm = WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, mw).total <= cap;
+  // (the INCF variant reads only the forward masks, once per event)
+  const bool msm = !incf && WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, mw).total <= cap;
   plan->kp = kp;
   plan->segl = segl;
   plan->masks_smem = msm;

@@ -52,6 +52,8 @@ struct PipeArgs {
   const int4* far_meta;
   const uint32_t* win_pos;
   const uint32_t* win_neg;
+  const uint32_t* fwd_pos;         // k1_window: forward window masks (bit l: vertex v+1+l is a +1 neighbour)
+  const uint32_t* fwd_neg;
   int32_t n_words;                 // spin words per CTA (>= n + 1)
   uint32_t* gwords;                // [grid][n_words] global spin words, or nullptr (shared memory)
   int8_t* gspins;                  // k1_window: [R][n_words] global int8 spins, or nullptr (shared memory)

@@ -40,6 +40,8 @@ struct PipeGraph {
   int4* far_meta = nullptr;  // device
   uint32_t* win_pos = nullptr;
   uint32_t* win_neg = nullptr;
+  uint32_t* fwd_pos = nullptr;  // forward window masks (layout.cu k_fwd_masks)
+  uint32_t* fwd_neg = nullptr;
   int32_t* wsell = nullptr;  // k1_window rows
   int32_t* wsell_off = nullptr;
 };

@@ -352,6 +352,22 @@ cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout*
   return cudaStreamSynchronize(st);
 }
 
+// Forward window masks: bit l of fwd[v] = bit l of win[v + 1 + l] (vertex
+// v + 1 + l has v as a +1 / -1 neighbour at distance l + 1), so one uniform load
+// of the changed vertex's word gives the whole next window's corrections.
+__global__ void k_fwd_masks(const uint32_t* __restrict__ wpos, const uint32_t* __restrict__ wneg, int n,
+                            uint32_t* __restrict__ fpos, uint32_t* __restrict__ fneg) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  uint32_t p = 0u, q = 0u;
+  for (int l = 0; l < 32 && v + 1 + l < n; l++) {
+    p |= ((wpos[v + 1 + l] >> l) & 1u) << l;
+    q |= ((wneg[v + 1 + l] >> l) & 1u) << l;
+  }
+  fpos[v] = p;
+  fneg[v] = q;
+}
+
 cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st) {
   const int n = g.n;
   cudaError_t e;
@@ -368,6 +384,10 @@ cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStrea
   k_fill_i32<<<1, 32, 0, st>>>(L->far_col.as<int32_t>() + total, 1, n);  // never empty; index n = zero word
   k_far_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, foff.as<int32_t>(), n, win, L->far_col.as<int32_t>(),
                                        L->far_meta.as<int4>(), L->win_pos.as<uint32_t>(), L->win_neg.as<uint32_t>());
+  if ((e = cudaGetLastError())) return e;
+  if ((e = L->fwd_pos.alloc(n * sizeof(uint32_t))) || (e = L->fwd_neg.alloc(n * sizeof(uint32_t)))) return e;
+  k_fwd_masks<<<blocks(n), kB, 0, st>>>(L->win_pos.as<uint32_t>(), L->win_neg.as<uint32_t>(), n,
+                                        L->fwd_pos.as<uint32_t>(), L->fwd_neg.as<uint32_t>());
   if ((e = cudaGetLastError())) return e;
   // k1_window rows
   const int chunks = (n + 31) / 32;

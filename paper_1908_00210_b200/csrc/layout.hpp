@@ -26,7 +26,7 @@ struct ThruLayout {
 };
 
 struct PipeLayout {
-  DevBuf far_col, far_meta, win_pos, win_neg;
+  DevBuf far_col, far_meta, win_pos, win_neg, fwd_pos, fwd_neg;
   // k1_window rows: SELL-32 over the natural vertex order (chunk c = vertices
   // 32c..32c+31, entry k of lane l at (wsell_off[c] + k) * 32 + l; padding
   // index n; -1 weights in bit 31 of the index)
