@@ -385,18 +385,13 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     const int c = diff < 0 ? 1 : diff > 0 ? -1 : (static_cast<long long>(d0) < 0 ? 1 : -1);
     const uint64_t u = tie ? d1 : d0;
     const int fin = (en && u <= tm) ? -c : c;
-    // the pending scatter: its field loads now (this step's refill loads are
-    // issued), the stores at the end of the step
-    int sv[4];
+    // the pending scatter is applied at the end of the step (its target loads,
+    // issued above, come from L2)
     const int sdp = sd;
-    if (defer && sdp != 0) {
-#pragma unroll
-      for (int q = 0; q < 4; q++) sv[q] = sc[q] >= 0 ? fld[sc[q]] : 0;
-      sd = 0;
-    }
+    if (defer) sd = 0;
     const unsigned m = __ballot_sync(FULL, act && (fin != own || tie));
     int adv;
-    bool wrote = defer && sdp != 0;  // shared-memory stores this step (warp-uniform)
+    bool wrote = false;  // spin store this step (warp-uniform)
     if (m == 0u) {
       adv = F;
       pos += F;
@@ -440,11 +435,6 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
         }
       }
     }
-    if (defer && sdp != 0) {
-#pragma unroll
-      for (int q = 0; q < 4; q++)
-        if (sc[q] >= 0) fld[sc[q]] = static_cast<int16_t>(sv[q] + (SIGNED ? sw[q] * sdp : sdp));
-    }
     if (wrote) __syncwarp();  // this step's shared-memory stores before the next step's loads
     // ring slots before pos are consumed (release: their loads are done);
     // the producer works in whole rounds, so only round crossings are published
@@ -464,6 +454,12 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       f = __shfl_down_sync(FULL, f, adv);
       wp = __shfl_down_sync(FULL, wp, adv);
       if (SIGNED) wn = __shfl_down_sync(FULL, wn, adv);
+    }
+    if (defer && sdp != 0) {  // the pending scatter (after this step's refill loads, before the next)
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        if (sc[q] >= 0) fld[sc[q]] = static_cast<int16_t>(fld[sc[q]] + (SIGNED ? sw[q] * sdp : sdp));
+      __syncwarp();
     }
     F -= adv;
     i0 += adv;
