@@ -81,11 +81,12 @@ __device__ __forceinline__ int nbv(const int8_t* s, int idx) {
 
 struct WinLayout {
   int ring, jump, genpos, cons, flags, spins, fields, masks, total;
-  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, bool incf, int ring_n, int mask_words = 0) {
+  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, bool incf, int ring_n, int mask_words = 0,
+                                            bool jt2 = false) {
     WinLayout L;
     L.ring = 0;
-    L.jump = L.ring + rc * ring_n * 8;  // 256 x 32 B jump matrix
-    L.genpos = L.jump + 256 * 32;
+    L.jump = L.ring + rc * ring_n * 8;  // 256 x 32 B jump matrix, or the 128 x 4 x 32 B two-column table
+    L.genpos = L.jump + (jt2 ? 128 * 4 * 32 : 256 * 32);
     L.cons = L.genpos + 4 * 32;
     L.flags = L.cons + 4 * 32;  // [0] consumers done, [1] abort
     L.spins = L.flags + 16;
@@ -108,11 +109,12 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const int rc = a.rc;  // replica warps 0..rc-1, producer warps rc..rc+nprod-1
   const int n_pad = a.n_words;
   const int kp = a.kp, SL = a.segl, ringN = a.rounds * kp * SL, rmask = ringN - 1;
-  const WinLayout L = WinLayout::make(rc, n_pad, GS, INCF, ringN);
+  const bool jt2 = a.jump_table2 != 0;
+  const WinLayout L = WinLayout::make(rc, n_pad, GS, INCF, ringN, 0, jt2);
   uint64_t* ring = reinterpret_cast<uint64_t*>(smem + L.ring);
   uint32_t* jm = reinterpret_cast<uint32_t*>(smem + L.jump);
   if (kp > 1)
-    for (int i = threadIdx.x; i < 256 * 4; i += blockDim.x)
+    for (int i = threadIdx.x; i < (jt2 ? 2048 : 1024); i += blockDim.x)
       reinterpret_cast<uint64_t*>(jm)[i] = __ldg(a.jump + i);
   // window masks: a per-CTA shared-memory copy when it fits (plan), else global
   uint32_t* wm = reinterpret_cast<uint32_t*>(smem + L.masks);
@@ -175,7 +177,12 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
 #pragma unroll
           for (int k = 0; k < 32; k++) dst[b + k] = rng.next();
         }
-        if (kp > 1) rng.jump(jm);
+        if (kp > 1) {
+          if (jt2)
+            xoshiro_jump2(rng, jm);
+          else
+            rng.jump(jm);
+        }
         gen += round;
         __threadfence_block();  // this lane's draws before the group's release
       }
@@ -568,6 +575,10 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   const int mw = st.unit ? 1 : 2;
   // (the INCF variant reads only the forward masks, once per event)
   const bool msm = !incf && WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, mw).total <= cap;
+  // the two-column jump table (half the jump's ALU work) when its extra 8 KB fit
+  bool jt2 = kp > 1 && WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, msm ? mw : 0, true).total <= cap;
+  if (const char* e = std::getenv("GDI_WINDOW_JT2")) jt2 = kp > 1 && std::atoi(e) != 0;
+  plan->jt2 = jt2;
   plan->kp = kp;
   plan->segl = segl;
   plan->masks_smem = msm;
@@ -589,7 +600,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
     plan->block = 32 * (rc + plan->nprod);
   }
   plan->grid = (replicas + rc - 1) / rc;
-  plan->smem = WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, msm ? mw : 0).total;
+  plan->smem = WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, msm ? mw : 0, jt2).total;
   plan->n_words = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
@@ -618,6 +629,7 @@ cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream
   a.segl = plan.segl;
   a.rounds = plan.rounds;
   a.masks_smem = plan.masks_smem ? 1 : 0;
+  a.jump_table2 = plan.jt2 ? 1 : 0;
   a.jump = nullptr;
   if (plan.kp > 1) {
     // the (kp-1)*segl-draw jump matrix, built once per device and distance
@@ -627,10 +639,15 @@ cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream
     if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
     const int J = (plan.kp - 1) * plan.segl;
     std::lock_guard<std::mutex> lock(mu);
-    uint64_t*& d = cache[{dev, J}];
+    uint64_t*& d = cache[{dev, plan.jt2 ? -J : J}];
     if (d == nullptr) {
       std::vector<uint64_t> h(256 * 4);
       xoshiro_jump_matrix(static_cast<uint64_t>(J), h.data());
+      if (plan.jt2) {
+        std::vector<uint64_t> t(128 * 4 * 4);
+        xoshiro_jump_table2(h.data(), t.data());
+        h.swap(t);
+      }
       if ((err = cudaMalloc(&d, h.size() * sizeof(uint64_t))) != cudaSuccess) {
         d = nullptr;
         return err;

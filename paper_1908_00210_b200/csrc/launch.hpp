@@ -62,6 +62,7 @@ struct PipePlan {
   int segl = 64;    // k1_window: draws per producer segment
   int rounds = 4;   // k1_window: producer rounds buffered per replica
   bool masks_smem = false;  // k1_window: window masks in shared memory
+  bool jt2 = false;         // k1_window: two-column jump table
   const char* name = "";
 };
 

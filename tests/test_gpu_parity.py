@@ -224,3 +224,13 @@ def test_m1_million_vertices_bit_exact(kernel_variant):
         pytest.skip("k1_exact keeps spins in shared memory: 1M does not fit (capacity)")
     out = check_batch_against_golden("M1")
     assert out["cut"][0] == 1252631 and out["imbalance"][0] == 0
+
+
+@pytest.mark.parametrize("jt2", ["0", "1"])
+def test_window_jump_forms_bit_exact(jt2, kernel_variant, monkeypatch):
+    """k1_window's producer jump as the plain bit matrix (configs whose shared
+    memory is full) and as the two-column table: same draws, same anneal."""
+    if kernel_variant != "auto":
+        pytest.skip("default kernel only")
+    monkeypatch.setenv("GDI_WINDOW_JT2", jt2)
+    check_batch_against_golden("G22", count=64)
