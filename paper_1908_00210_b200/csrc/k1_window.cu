@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <string>
 #include <utility>
 #include <vector>
@@ -81,7 +82,8 @@ __device__ __forceinline__ int nbv(const int8_t* s, int idx) {
 
 struct WinLayout {
   int ring, jump, genpos, cons, flags, spins, fields, masks, total;
-  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, bool incf, int ring_n, int mask_words = 0,
+  // fb: bytes per exact field (0 = no INCF fields, 1 = int8, 2 = int16)
+  __host__ __device__ static WinLayout make(int rc, int n_pad, bool gs, int fb, int ring_n, int mask_words = 0,
                                             bool jt2 = false) {
     WinLayout L;
     L.ring = 0;
@@ -91,17 +93,17 @@ struct WinLayout {
     L.flags = L.cons + 4 * 32;  // [0] consumers done, [1] abort
     L.spins = L.flags + 16;
     L.fields = L.spins + (gs ? 0 : rc * n_pad);
-    L.masks = (L.fields + (incf ? rc * n_pad * 2 : 0) + 15) & ~15;
+    L.masks = (L.fields + rc * n_pad * fb + 15) & ~15;
     L.total = L.masks + mask_words * n_pad * 4;
     return L;
   }
 };
 
-// INCF: every vertex's field kept exact in shared memory (int16; scattered on
+// INCF: every vertex's field kept exact in shared memory (int8 or int16; scattered on
 // each spin change, ~2% of visits) so a window refill is two shared loads
 // instead of a row gather; else rows are gathered from the natural-order
 // SELL layout and pending lanes are corrected through the window masks.
-template <bool SIGNED, bool UNITAB, bool GS, bool INCF>
+template <bool SIGNED, bool UNITAB, bool GS, int INCF>  // INCF: bytes per exact field (0 = gathered rows)
 __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.g.n;
@@ -211,7 +213,8 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   }
   const size_t rs = static_cast<size_t>(r);
   int8_t* s = GS ? a.gspins + rs * n_pad : reinterpret_cast<int8_t*>(smem + L.spins) + cw * n_pad;
-  int16_t* fld = reinterpret_cast<int16_t*>(smem + L.fields) + cw * n_pad;  // INCF only
+  using FT = typename std::conditional<INCF == 1, int8_t, int16_t>::type;  // exact field type
+  FT* fld = reinterpret_cast<FT*>(smem + L.fields) + cw * n_pad;  // INCF only
   const int32_t* __restrict__ off = a.g.off;
   const int32_t* __restrict__ col = a.g.col;
   const int32_t* __restrict__ wgt = a.g.w;
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       int acc = 0;
       const int e1 = __ldg(off + v + 1);
       for (int e = __ldg(off + v); e < e1; e++) acc += SIGNED ? __ldg(wgt + e) * s[__ldg(col + e)] : s[__ldg(col + e)];
-      fld[v] = static_cast<int16_t>(acc);
+      fld[v] = static_cast<FT>(acc);
     }
     __syncwarp();
   }
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   // event); the scatter itself is applied after that step's refill loads and
   // before the next ones. INCF requires rows of at most 128 entries (four
   // targets per lane).
-  constexpr bool defer = INCF;
+  constexpr bool defer = INCF != 0;
   int sd = 0;                     // pending change (0 = none)
   int se0 = 0, se1 = 0;           // its CSR row
   uint32_t rmv = 0u, rmn = 0u;    // its forward window masks
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     if (defer && sdp != 0) {  // the pending scatter (after this step's refill loads, before the next)
 #pragma unroll
       for (int q = 0; q < 4; q++)
-        if (sc[q] >= 0) fld[sc[q]] = static_cast<int16_t>(fld[sc[q]] + (SIGNED ? sw[q] * sdp : sdp));
+        if (sc[q] >= 0) fld[sc[q]] = static_cast<FT>(fld[sc[q]] + (SIGNED ? sw[q] * sdp : sdp));
       __syncwarp();
     }
     F -= adv;
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       if (defer && sd != 0) {  // flush the pending scatter before the next sweep's refills
         for (int e = se0 + lane; e < se1; e += 32) {
           const int uu = __ldg(col + e);
-          fld[uu] = static_cast<int16_t>(fld[uu] + (SIGNED ? __ldg(wgt + e) * sd : sd));
+          fld[uu] = static_cast<FT>(fld[uu] + (SIGNED ? __ldg(wgt + e) * sd : sd));
         }
         sd = 0;
         __syncwarp();
@@ -524,10 +527,11 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
 }
 
 template <bool S, bool U>
-const void* win_fn(bool gs, bool incf) {
-  if (gs) return reinterpret_cast<const void*>(&k1_window<S, U, true, false>);
-  return incf ? reinterpret_cast<const void*>(&k1_window<S, U, false, true>)
-              : reinterpret_cast<const void*>(&k1_window<S, U, false, false>);
+const void* win_fn(bool gs, int fb) {
+  if (gs) return reinterpret_cast<const void*>(&k1_window<S, U, true, 0>);
+  if (fb == 1) return reinterpret_cast<const void*>(&k1_window<S, U, false, 1>);
+  if (fb == 2) return reinterpret_cast<const void*>(&k1_window<S, U, false, 2>);
+  return reinterpret_cast<const void*>(&k1_window<S, U, false, 0>);
 }
 
 }  // namespace
@@ -561,22 +565,42 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
                   (force && std::string(force) == "window_gmem");
   // incremental fields when they fit next to the spins (int16 bound)
   const bool incf = !gs && st.max_abs_field < 32768 && st.max_degree <= 128 &&
-                    WinLayout::make(rc, n_pad, false, true, ring_min).total <= cap &&
+                    WinLayout::make(rc, n_pad, false, st.max_abs_field <= 127 ? 1 : 2, ring_min).total <= cap &&
                     !(force && std::string(force) == "window_masks");
-  // segment length: the longest that fits (amortises the jump over more draws)
-  int segl = 32;
-  for (int c : {256, 128, 64})
-    if (nr * kp * c <= kRingMax && WinLayout::make(rc, n_pad, gs, incf, nr * kp * c).total <= cap) {
-      segl = c;
-      break;
-    }
-  if (const char* e = std::getenv("GDI_WINDOW_SEGL")) segl = std::atoi(e);
-  // window masks in shared memory when they still fit with that segment length
+  // shared-memory budget after the spins: segment length (the longest that
+  // fits amortises the jump over more draws), window masks (the INCF variant
+  // reads only the forward masks, once per event), the two-column jump table
   const int mw = st.unit ? 1 : 2;
-  // (the INCF variant reads only the forward masks, once per event)
-  const bool msm = !incf && WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, mw).total <= cap;
-  // the two-column jump table (half the jump's ALU work) when its extra 8 KB fit
-  bool jt2 = kp > 1 && WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, msm ? mw : 0, true).total <= cap;
+  struct Fit {
+    int segl;
+    bool msm, jt2;
+  };
+  auto fit = [&](int fb) {
+    Fit f{32, false, false};
+    for (int c : {256, 128, 64})
+      if (nr * kp * c <= kRingMax && WinLayout::make(rc, n_pad, gs, fb, nr * kp * c).total <= cap) {
+        f.segl = c;
+        break;
+      }
+    if (const char* e = std::getenv("GDI_WINDOW_SEGL")) f.segl = std::atoi(e);
+    f.msm = fb == 0 && WinLayout::make(rc, n_pad, gs, fb, nr * kp * f.segl, mw).total <= cap;
+    f.jt2 = kp > 1 && WinLayout::make(rc, n_pad, gs, fb, nr * kp * f.segl, f.msm ? mw : 0, true).total <= cap;
+    return f;
+  };
+  // exact field type: int16, or int8 (|field| <= 127) when that frees room for a
+  // longer segment or the jump table (int8 fields were measured slower on their own)
+  int fb = incf ? 2 : 0;
+  Fit ft = fit(fb);
+  if (incf && st.max_abs_field <= 127) {
+    const Fit f8 = fit(1);
+    if (f8.segl > ft.segl || (f8.jt2 && !ft.jt2)) {
+      fb = 1;
+      ft = f8;
+    }
+  }
+  const int segl = ft.segl;
+  const bool msm = ft.msm;
+  bool jt2 = ft.jt2;
   if (const char* e = std::getenv("GDI_WINDOW_JT2")) jt2 = kp > 1 && std::atoi(e) != 0;
   plan->jt2 = jt2;
   plan->kp = kp;
@@ -584,8 +608,8 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   plan->masks_smem = msm;
   plan->rounds = nr;
   const bool unitab = ra == 1 && rb == 1;
-  plan->fn = st.unit ? (unitab ? win_fn<false, true>(gs, incf) : win_fn<false, false>(gs, incf))
-                     : (unitab ? win_fn<true, true>(gs, incf) : win_fn<true, false>(gs, incf));
+  plan->fn = st.unit ? (unitab ? win_fn<false, true>(gs, fb) : win_fn<false, false>(gs, fb))
+                     : (unitab ? win_fn<true, true>(gs, fb) : win_fn<true, false>(gs, fb));
   plan->prof = false;
   plan->gw = gs;
   plan->rc = rc;
@@ -600,7 +624,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
     plan->block = 32 * (rc + plan->nprod);
   }
   plan->grid = (replicas + rc - 1) / rc;
-  plan->smem = WinLayout::make(rc, n_pad, gs, incf, nr * kp * segl, msm ? mw : 0, jt2).total;
+  plan->smem = WinLayout::make(rc, n_pad, gs, fb, nr * kp * segl, msm ? mw : 0, jt2).total;
   plan->n_words = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
