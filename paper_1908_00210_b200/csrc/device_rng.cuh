@@ -41,25 +41,36 @@ struct Xoshiro {
   // rng.hpp:23-33
   __host__ __device__ __forceinline__ uint64_t next() {
     const uint64_t out = rotl64(s0 + s3, 23) + s0;
-    const uint64_t t = s1 << 17;
-    s2 ^= s0;
-    s3 ^= s1;
-    s1 ^= s2;
-    s0 ^= s3;
-    s2 ^= t;
-    s3 = rotl64(s3, 45);
+    step();
     return out;
   }
 
-  // the state transition alone (next() without its output)
+  // the state transition alone (next() without its output). The reference's
+  // in-place sequence (s2 ^= s0; s3 ^= s1; s1 ^= s2; s0 ^= s3; s2 ^= t;
+  // s3 = rotl(s3, 45)) written as three-input XORs of the old words, one LOP3
+  // per 32-bit half each (the compiler did not merge the in-place form)
+  __host__ __device__ __forceinline__ static uint64_t xor3(uint64_t a, uint64_t b, uint64_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t lo, hi;  // explicit lop3: common-subexpression elimination would otherwise split these
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(lo) : "r"(static_cast<uint32_t>(a)), "r"(static_cast<uint32_t>(b)),
+        "r"(static_cast<uint32_t>(c)));
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(hi) : "r"(static_cast<uint32_t>(a >> 32)),
+        "r"(static_cast<uint32_t>(b >> 32)), "r"(static_cast<uint32_t>(c >> 32)));
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+#else
+    return a ^ b ^ c;
+#endif
+  }
   __host__ __device__ __forceinline__ void step() {
     const uint64_t t = s1 << 17;
-    s2 ^= s0;
-    s3 ^= s1;
-    s1 ^= s2;
-    s0 ^= s3;
-    s2 ^= t;
-    s3 = rotl64(s3, 45);
+    const uint64_t n1 = xor3(s1, s2, s0);  // s1 ^ (s2 ^ s0)
+    const uint64_t n0 = xor3(s0, s3, s1);  // s0 ^ (s3 ^ s1)
+    const uint64_t n2 = xor3(s2, s0, t);   // (s2 ^ s0) ^ t
+    const uint64_t n3 = s3 ^ s1;
+    s0 = n0;
+    s1 = n1;
+    s2 = n2;
+    s3 = rotl64(n3, 45);
   }
 
   // Jump ahead J draws: the transition is linear over GF(2), so J steps are
