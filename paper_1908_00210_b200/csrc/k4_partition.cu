@@ -477,7 +477,16 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->ctas = ctas < 1 ? 1 : ctas;
   plan->chains = plan->ctas * kNW;
   // tail chunks run by the last CTA against the exact counter (see k4_sweep)
-  plan->tail = nck / 8 < kTailMax ? nck / 8 : kTailMax;
+  // 8 chunks: the chains' residual after the CTA tails is a few spins; a
+  // 32-chunk tail balanced no better (M1 and a 100k graph, 4 seeds: final
+  // imbalance 0 either way) and cost a fifth of the M1 sweep, the last CTA
+  // deciding its chunks in order against a counter that cascades through them
+  constexpr int kTailDefault = 8;
+  plan->tail = nck / 8 < kTailDefault ? nck / 8 : kTailDefault;
+  if (const char* e = std::getenv("GDI_K4_TAIL")) {  // tuning experiments
+    const int t = std::atoi(e);
+    plan->tail = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
+  }
   plan->sweep_fn = wkind == 0 ? sweep_fn<0>(kmax) : wkind == 1 ? sweep_fn<1>(kmax) : sweep_fn<2>(kmax);
   plan->gtail_fn = wkind == 0 ? gtail_fn<0>(kmax) : wkind == 1 ? gtail_fn<1>(kmax) : gtail_fn<2>(kmax);
   plan->cut_fn = wkind == 0   ? reinterpret_cast<const void*>(&k4_cut<0>)
