@@ -56,7 +56,10 @@ namespace gdi {
 namespace {
 
 constexpr int kNW = 16;  // warps per CTA
-constexpr int kDefer = 2;     // chunks per chain deferred to the CTA tail
+#ifndef K4_DEFER
+#define K4_DEFER 2
+#endif
+constexpr int kDefer = K4_DEFER;  // chunks per chain deferred to the CTA tail
 constexpr int kTailMax = 32;  // global tail chunks (= kDefer * kNW: shares stage[])
 constexpr int kPackBlock = 256;
 constexpr int kCutBlock = 512;
