@@ -59,12 +59,6 @@ constexpr int kRingMax = 4096;
 #ifndef K1W_SPEC
 #define K1W_SPEC 1  // draws read before the ring check
 #endif
-#ifndef K1W_LATEPK
-#define K1W_LATEPK 0  // refill loads issued before the shifted lanes are decoded
-#endif
-#ifndef K1W_MSEL
-#define K1W_MSEL 0  // masks: explicit shared/global selection (else generic pointer)
-#endif
 #ifndef K1W_PROF
 #define K1W_PROF 0  // 1: step statistics (GDI_PIPE_DEBUG=4) and the no-wait timing mode (8)
 #endif
@@ -277,7 +271,6 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const int nn = __shfl_sync(FULL, n, 0);
   const int nsw = __shfl_sync(FULL, sweeps, 0);
   const bool msm = __shfl_sync(FULL, a.masks_smem, 0) != 0;
-  int pk = 0;  // INCF: (field << 1 | spin > 0) of the pending lanes, shifted at the end of a step
   // INCF deferred scatter: a spin change is scattered into the fields one step
   // later, off the step's critical path. The next step's window is the 32
   // vertices after the changed one, so its lanes add the change through the
@@ -307,23 +300,16 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     const bool rl = lane >= F && lane < lim;
     int r_own = 0, r_f = 0;
     uint32_t r_wp = 0u, r_wn = 0u;
-    if (rl) {  // loads first; the pending lanes' shifted values are decoded after
+    if (rl) {  // loads into temporaries, then the refilled lanes take them
       const int v = i0 + lane;
       r_own = s[v];
       if (!INCF) {
-#if K1W_MSEL
-      r_wp = msm ? wm[v] : __ldg(a.win_pos + v);
-      if (SIGNED) r_wn = msm ? wm[n_pad + v] : __ldg(a.win_neg + v);
-#else
-      r_wp = (msm ? static_cast<const uint32_t*>(wm) : a.win_pos)[v];
-      if (SIGNED) r_wn = (msm ? static_cast<const uint32_t*>(wm) + n_pad : a.win_neg)[v];
-#endif
+        // one generic pointer for shared or global masks (measured faster than
+        // selecting an explicit shared or global load per step)
+        r_wp = (msm ? static_cast<const uint32_t*>(wm) : a.win_pos)[v];
+        if (SIGNED) r_wn = (msm ? static_cast<const uint32_t*>(wm) + n_pad : a.win_neg)[v];
       }
       if (INCF) r_f = fld[v];
-    }
-    if (INCF && K1W_LATEPK) {
-      own = (pk & 1) ? 1 : -1;
-      f = pk >> 1;
     }
     if (rl) {
       const int v = i0 + lane;
@@ -453,11 +439,9 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       pub = pos & ~(round_w - 1);
     }
     if (INCF) {  // spin and field of the pending lanes in one shuffle (decoded next step)
-      pk = __shfl_down_sync(FULL, (f << 1) | (own > 0 ? 1 : 0), adv);
-      if (!K1W_LATEPK) {
-        own = (pk & 1) ? 1 : -1;
-        f = pk >> 1;
-      }
+      const int pk = __shfl_down_sync(FULL, (f << 1) | (own > 0 ? 1 : 0), adv);
+      own = (pk & 1) ? 1 : -1;
+      f = pk >> 1;
 
     } else {
       own = __shfl_down_sync(FULL, own, adv);

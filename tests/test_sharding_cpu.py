@@ -135,6 +135,45 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+class _RecSession:
+    """Stands in for a PartSession: records the driver's call order."""
+
+    def __init__(self, log, name):
+        self.log, self.name = log, name
+
+    def init(self):
+        self.log.append(("init", self.name))
+
+    def sweep(self, k, send):
+        self.log.append(("sweep", self.name, k))
+
+    def finish(self, k, recv):
+        self.log.append(("finish", self.name, k))
+
+    def fetch(self):
+        return {}
+
+
+def test_run_partitioned_fused_barrier_order():
+    """Fused exchange (sweep kernels store into the other ranks' spin copies):
+    no rank may start sweep 0 before every rank initialised its copy, nor
+    sweep k+1 before every rank finished sweep k (tail replay, cut) on its
+    copy. run_partitioned calls the barrier after init and between sweeps."""
+    log = []
+    ss = [_RecSession(log, r) for r in range(2)]
+    sh.run_partitioned(ss, 3, lambda: log.append(("exchange",)), lambda i: (0, 0),
+                       barrier=lambda: log.append(("barrier",)))
+    kinds = [e[0] for e in log]
+    assert kinds == ["init", "init", "barrier",
+                     "sweep", "sweep", "exchange", "finish", "finish", "barrier",
+                     "sweep", "sweep", "exchange", "finish", "finish", "barrier",
+                     "sweep", "sweep", "exchange", "finish", "finish"]
+    # unfused: no barrier at all
+    log.clear()
+    sh.run_partitioned(ss, 2, lambda: log.append(("exchange",)), lambda i: (0, 0))
+    assert ("barrier",) not in log and [e[0] for e in log].count("sweep") == 4
+
+
 def test_gloo_world2_sharding_and_partition_exchange():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
