@@ -135,6 +135,22 @@ int gdi_graph_query(const gdi_graph* g, gdi_graph_info* info);
 int gdi_anneal_batch(const gdi_graph* g, const gdi_params* p, const uint64_t* seeds,
                      int32_t replicas, gdi_outputs* out);
 
+/* The trace in column form (what array-oriented bindings such as pyising
+ * return): hcut_imb[(r*sweeps + k)*3 + {0,1,2}] = {hamiltonian_scaled, cut,
+ * imbalance}, seconds[r*sweeps + k], flip_probability[k]. Any pointer may be
+ * NULL. */
+typedef struct {
+  int64_t* hcut_imb;
+  double* seconds;
+  double* flip_probability;
+} gdi_trace_columns;
+
+/* gdi_anneal_batch with the trace written as columns (out->trace and
+ * out->counters are ignored): one conversion pass instead of records and a
+ * second pass in the binding. */
+int gdi_anneal_batch_columns(const gdi_graph* g, const gdi_params* p, const uint64_t* seeds, int32_t replicas,
+                             gdi_outputs* out, const gdi_trace_columns* trace);
+
 /* Fused exact evaluation (cut, imbalance, H) of R host spin vectors. */
 int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,
                        int64_t b_num, int64_t denom, gdi_score* scores);

@@ -481,6 +481,99 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
 }  // namespace
 
 extern "C" {
+static int check_watchdog(gdi_session* s);  // defined with the session entry points below
+}
+
+namespace {
+
+// gdi_session_fetch, with the trace optionally in column form (cols)
+int fetch_impl(gdi_session* s, gdi_outputs* out, const gdi_trace_columns* cols) {
+  if (!s || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
+  if (!s->launched) return fail(GDI_ERR_CONFIG, "session has not been launched");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  GDI_CUDA(cudaStreamSynchronize(s->stream));
+  if (int rc = check_watchdog(s)) return rc;
+  const size_t R = s->replicas, n = s->g->st.n, S = s->p.sweeps;
+  const long long A = s->p.a_num, B = s->p.b_num;
+  const double denom = static_cast<double>(s->p.denom);
+  float ms = 0.f;
+  GDI_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  out->seconds = ms * 1e-3;
+  if (out->spins)
+    GDI_CUDA(cudaMemcpy(out->spins, s->spins.p, R * n, cudaMemcpyDeviceToHost));
+  if (out->scores) {
+    std::vector<DevTrace> fin(R);
+    GDI_CUDA(cudaMemcpy(fin.data(), s->final_out.p, R * sizeof(DevTrace), cudaMemcpyDeviceToHost));
+    for (size_t r = 0; r < R; r++) {
+      const long long sum = fin[r].sum, cut = fin[r].cut;
+      gdi_score& sc = out->scores[r];
+      sc.cut = cut;
+      sc.imbalance = sum < 0 ? -sum : sum;
+      sc.hamiltonian_scaled = A * sum * sum + B * cut;
+      sc.hamiltonian = static_cast<double>(sc.hamiltonian_scaled) / denom;
+      sc.balance_counter = fin[r].counter;
+    }
+  }
+  const bool want_cols = cols != nullptr && (cols->hcut_imb || cols->seconds || cols->flip_probability);
+  if (want_cols && cols->flip_probability)
+    for (size_t k = 0; k < S; k++) cols->flip_probability[k] = s->pf[k];
+  if (out->trace || out->counters || (want_cols && (cols->hcut_imb || cols->seconds))) {
+    if (!(s->p.flags & GDI_FLAG_TRACE))
+      return fail(GDI_ERR_CONFIG, "trace requested but the session was created without GDI_FLAG_TRACE");
+    // pinned staging: the trace is the bulk of a batch's
+    // result (24 B per sweep per replica + a timestamp), pageable copies of it
+    // cost more than the conversion
+    const size_t tb = R * S * sizeof(DevTrace), sb = R * (S + 1) * sizeof(unsigned long long);
+    // (one buffer per host thread, reused across sessions: one-shot batches
+    // create a session per call)
+    PinnedBuf& stage = trace_stage();
+    if (!s->host_trace) {  // else the kernels wrote the records there already
+      GDI_CUDA(stage.ensure(tb + sb));
+      GDI_CUDA(cudaMemcpyAsync(stage.p, s->trace.p, tb, cudaMemcpyDeviceToHost, s->stream));
+      GDI_CUDA(cudaMemcpyAsync(stage.as<char>() + tb, s->stamps.p, sb, cudaMemcpyDeviceToHost, s->stream));
+      GDI_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    const DevTrace* tr = stage.as<DevTrace>();
+    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(stage.as<char>() + tb);
+    parallel_rows(R, 64 * 1024 / (S + 1) + 1, [&](size_t r0, size_t r1) {
+    for (size_t r = r0; r < r1; r++)
+      for (size_t k = 0; k < S; k++) {
+        const DevTrace& d = tr[r * S + k];
+        if (out->counters) out->counters[r * S + k] = d.counter;
+        if (want_cols) {
+          const long long hs = A * d.sum * d.sum + B * d.cut;
+          if (cols->hcut_imb) {
+            int64_t* c3 = cols->hcut_imb + 3 * (r * S + k);
+            c3[0] = hs;
+            c3[1] = d.cut;
+            c3[2] = d.sum < 0 ? -d.sum : d.sum;
+          }
+          if (cols->seconds)
+            cols->seconds[r * S + k] = static_cast<double>(st[r * (S + 1) + k + 1] - st[r * (S + 1) + k]) * 1e-9;
+        }
+        if (out->trace) {
+          gdi_trace_rec& t = out->trace[r * S + k];
+          t.cut = d.cut;
+          t.imbalance = d.sum < 0 ? -d.sum : d.sum;
+          t.hamiltonian_scaled = A * d.sum * d.sum + B * d.cut;
+          t.hamiltonian = static_cast<double>(t.hamiltonian_scaled) / denom;
+          t.flip_probability = s->pf[k];
+          t.seconds = static_cast<double>(st[r * (S + 1) + k + 1] - st[r * (S + 1) + k]) * 1e-9;
+        }
+      }
+    });
+  }
+  if (out->snapshots) {
+    if (!(s->p.flags & GDI_FLAG_SNAPSHOTS))
+      return fail(GDI_ERR_CONFIG, "snapshots requested but the session was created without GDI_FLAG_SNAPSHOTS");
+    GDI_CUDA(cudaMemcpy(out->snapshots, s->snaps.p, R * (S + 1) * n, cudaMemcpyDeviceToHost));
+  }
+  return GDI_OK;
+}
+
+}  // namespace
+
+extern "C" {
 
 int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
   if (!s || !seeds) return fail(GDI_ERR_CONFIG, "NULL argument");
@@ -679,75 +772,7 @@ int gdi_session_sync(gdi_session* s) {
   return check_watchdog(s);
 }
 
-int gdi_session_fetch(gdi_session* s, gdi_outputs* out) {
-  if (!s || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
-  if (!s->launched) return fail(GDI_ERR_CONFIG, "session has not been launched");
-  GDI_CUDA(cudaSetDevice(s->g->device));
-  GDI_CUDA(cudaStreamSynchronize(s->stream));
-  if (int rc = check_watchdog(s)) return rc;
-  const size_t R = s->replicas, n = s->g->st.n, S = s->p.sweeps;
-  const long long A = s->p.a_num, B = s->p.b_num;
-  const double denom = static_cast<double>(s->p.denom);
-  float ms = 0.f;
-  GDI_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
-  out->seconds = ms * 1e-3;
-  if (out->spins)
-    GDI_CUDA(cudaMemcpy(out->spins, s->spins.p, R * n, cudaMemcpyDeviceToHost));
-  if (out->scores) {
-    std::vector<DevTrace> fin(R);
-    GDI_CUDA(cudaMemcpy(fin.data(), s->final_out.p, R * sizeof(DevTrace), cudaMemcpyDeviceToHost));
-    for (size_t r = 0; r < R; r++) {
-      const long long sum = fin[r].sum, cut = fin[r].cut;
-      gdi_score& sc = out->scores[r];
-      sc.cut = cut;
-      sc.imbalance = sum < 0 ? -sum : sum;
-      sc.hamiltonian_scaled = A * sum * sum + B * cut;
-      sc.hamiltonian = static_cast<double>(sc.hamiltonian_scaled) / denom;
-      sc.balance_counter = fin[r].counter;
-    }
-  }
-  if (out->trace || out->counters) {
-    if (!(s->p.flags & GDI_FLAG_TRACE))
-      return fail(GDI_ERR_CONFIG, "trace requested but the session was created without GDI_FLAG_TRACE");
-    // pinned staging: the trace is the bulk of a batch's
-    // result (24 B per sweep per replica + a timestamp), pageable copies of it
-    // cost more than the conversion
-    const size_t tb = R * S * sizeof(DevTrace), sb = R * (S + 1) * sizeof(unsigned long long);
-    // (one buffer per host thread, reused across sessions: one-shot batches
-    // create a session per call)
-    PinnedBuf& stage = trace_stage();
-    if (!s->host_trace) {  // else the kernels wrote the records there already
-      GDI_CUDA(stage.ensure(tb + sb));
-      GDI_CUDA(cudaMemcpyAsync(stage.p, s->trace.p, tb, cudaMemcpyDeviceToHost, s->stream));
-      GDI_CUDA(cudaMemcpyAsync(stage.as<char>() + tb, s->stamps.p, sb, cudaMemcpyDeviceToHost, s->stream));
-      GDI_CUDA(cudaStreamSynchronize(s->stream));
-    }
-    const DevTrace* tr = stage.as<DevTrace>();
-    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(stage.as<char>() + tb);
-    parallel_rows(R, 64 * 1024 / (S + 1) + 1, [&](size_t r0, size_t r1) {
-    for (size_t r = r0; r < r1; r++)
-      for (size_t k = 0; k < S; k++) {
-        const DevTrace& d = tr[r * S + k];
-        if (out->counters) out->counters[r * S + k] = d.counter;
-        if (out->trace) {
-          gdi_trace_rec& t = out->trace[r * S + k];
-          t.cut = d.cut;
-          t.imbalance = d.sum < 0 ? -d.sum : d.sum;
-          t.hamiltonian_scaled = A * d.sum * d.sum + B * d.cut;
-          t.hamiltonian = static_cast<double>(t.hamiltonian_scaled) / denom;
-          t.flip_probability = s->pf[k];
-          t.seconds = static_cast<double>(st[r * (S + 1) + k + 1] - st[r * (S + 1) + k]) * 1e-9;
-        }
-      }
-    });
-  }
-  if (out->snapshots) {
-    if (!(s->p.flags & GDI_FLAG_SNAPSHOTS))
-      return fail(GDI_ERR_CONFIG, "snapshots requested but the session was created without GDI_FLAG_SNAPSHOTS");
-    GDI_CUDA(cudaMemcpy(out->snapshots, s->snaps.p, R * (S + 1) * n, cudaMemcpyDeviceToHost));
-  }
-  return GDI_OK;
-}
+int gdi_session_fetch(gdi_session* s, gdi_outputs* out) { return fetch_impl(s, out, nullptr); }
 
 int gdi_session_launch_count(const gdi_session* s, int32_t* count) {
   if (!s || !count) return fail(GDI_ERR_CONFIG, "NULL argument");
@@ -773,9 +798,16 @@ int gdi_session_destroy(gdi_session* s) {
 
 int gdi_anneal_batch(const gdi_graph* g, const gdi_params* p, const uint64_t* seeds,
                      int32_t replicas, gdi_outputs* out) {
-  if (!seeds || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
+  return gdi_anneal_batch_columns(g, p, seeds, replicas, out, nullptr);
+}
+
+int gdi_anneal_batch_columns(const gdi_graph* g, const gdi_params* p, const uint64_t* seeds, int32_t replicas,
+                             gdi_outputs* out, const gdi_trace_columns* cols) {
+  if (!seeds || !out || !p) return fail(GDI_ERR_CONFIG, "NULL argument");
   gdi_params q = *p;
-  if (out->trace || out->counters) q.flags |= GDI_FLAG_TRACE;
+  gdi_outputs o = *out;
+  if (cols) o.trace = nullptr, o.counters = nullptr;  // the columns replace the records
+  if (o.trace || o.counters || (cols && (cols->hcut_imb || cols->seconds))) q.flags |= GDI_FLAG_TRACE;
   if (out->snapshots) q.flags |= GDI_FLAG_SNAPSHOTS;
   gdi_session* s = nullptr;
   // trace written by the kernels straight into pinned host memory (fetched from there below)
@@ -785,7 +817,9 @@ int gdi_anneal_batch(const gdi_graph* g, const gdi_params* p, const uint64_t* se
   if ((rc = gdi_session_set_seeds(s, seeds))) return rc;
   if ((rc = gdi_session_launch(s))) return rc;
   if ((rc = gdi_session_sync(s))) return rc;
-  return gdi_session_fetch(s, out);
+  rc = fetch_impl(s, &o, cols);
+  out->seconds = o.seconds;
+  return rc;
 }
 
 int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,

@@ -485,14 +485,26 @@ PYBIND11_MODULE(pyising, m) {
          py::array_t<std::uint64_t, py::array::c_style | py::array::forcecast> seeds, bool trace) {
         // End-to-end C-ABI path with host buffers and no device caching:
         // CSR upload (gdi_graph_create), seeds H2D, kernel, spins + scores
-        // (+ trace) D2H, device buffers released — every call.
+        // (+ trace) D2H, device buffers released — every call. The trace is
+        // written by the library straight into the returned numpy columns
+        // (gdi_anneal_batch_columns: one conversion pass).
         const AnnealParams params = params_in.validated();
         const Graph& g = problem.graph();
         const std::size_t R = static_cast<std::size_t>(seeds.size());
         const std::size_t n = static_cast<std::size_t>(g.num_nodes()), S = static_cast<std::size_t>(params.sweeps);
         std::vector<std::int8_t> sp(R * n);
         std::vector<gdi_score> sc(R);
-        gdi_trace_rec* tr = trace ? trace_scratch(R * S) : nullptr;
+        py::array_t<std::int64_t> t3;
+        py::array_t<double> secs_a, pf_a;
+        gdi_trace_columns cols{};
+        if (trace) {
+          t3 = py::array_t<std::int64_t>({static_cast<py::ssize_t>(R), static_cast<py::ssize_t>(S), py::ssize_t{3}});
+          secs_a = py::array_t<double>({static_cast<py::ssize_t>(R), static_cast<py::ssize_t>(S)});
+          pf_a = py::array_t<double>({static_cast<py::ssize_t>(S)});
+          cols.hcut_imb = t3.mutable_data();
+          cols.seconds = secs_a.mutable_data();
+          cols.flip_probability = pf_a.mutable_data();
+        }
         double secs = 0.0;
         std::vector<std::uint64_t> sd(seeds.data(), seeds.data() + R);
         {
@@ -511,13 +523,19 @@ PYBIND11_MODULE(pyising, m) {
           gdi_outputs out{};
           out.spins = sp.data();
           out.scores = sc.data();
-          out.trace = tr;
-          const int rc = gdi_anneal_batch(dg, &q, sd.data(), static_cast<std::int32_t>(R), &out);
+          const int rc = gdi_anneal_batch_columns(dg, &q, sd.data(), static_cast<std::int32_t>(R), &out,
+                                                  trace ? &cols : nullptr);
           gdi_graph_destroy(dg);
           check_abi(rc);
           secs = out.seconds;
         }
-        return Session::pack(std::move(sp), sc, tr, R, n, trace ? S : 0, secs, true, trace);
+        py::dict d = Session::pack(std::move(sp), sc, nullptr, R, n, 0, secs, true, false);
+        if (trace) {
+          d["trace"] = t3;
+          d["trace_seconds"] = secs_a;
+          d["flip_probability"] = pf_a;
+        }
+        return d;
       },
       py::arg("problem"), py::arg("params"), py::arg("seeds"), py::arg("trace") = true);
 

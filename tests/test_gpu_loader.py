@@ -60,3 +60,30 @@ def test_device_validation_statistics_weighted(lib):
     # weights given but all 1: recognised as unit
     info1, _ = query(lib, pi.random_graph(500, 2000, 1), weighted=True)
     assert info1.all_unit_weights == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode_workers", [1, 8])
+def test_one_shot_trace_columns_match_records(mode_workers):
+    """anneal_batch_fresh (gdi_anneal_batch_columns: the trace written straight
+    into numpy columns) returns what anneal_batch (records, then columns)
+    does: same spins, scores, trace and flip probabilities; positive sweep
+    times. Exact mode and the pooled mode."""
+    from tests.helpers import golden_configs, product_graph
+
+    g = product_graph(golden_configs()["G22"]["recipe"])
+    prob = pi.MinCutProblem.with_default_coefficients(g)
+    p = pi.AnnealParams()
+    p.sweeps = 50
+    p.workers = mode_workers
+    p.deterministic = mode_workers == 1
+    seeds = np.arange(1, 33, dtype=np.uint64)
+    a = pi.anneal_batch(prob, p, seeds, True)
+    b = pi.anneal_batch_fresh(prob, p, seeds, True)
+    assert np.array_equal(a["spins"], b["spins"])  # the pooled mode is run-to-run reproducible here too (K2)
+    assert np.array_equal(a["cut"], b["cut"]) and np.array_equal(a["imbalance"], b["imbalance"])
+    assert np.array_equal(a["trace"], b["trace"])
+    assert np.array_equal(a["flip_probability"], b["flip_probability"])
+    assert b["trace_seconds"].shape == (32, 50) and (b["trace_seconds"] > 0).all()
+    c = pi.anneal_batch_fresh(prob, p, seeds, False)
+    assert "trace" not in c and np.array_equal(c["spins"], b["spins"])
