@@ -53,8 +53,9 @@ namespace gdi {
 
 namespace {
 
-// Draw ring per replica: nr rounds of kp segments of L draws (kp lanes of the
-// producer warp per stream; nr, L chosen per plan to fit shared memory)
+// Draw ring per replica: a power of two of draws holding more than two rounds
+// of kp segments of L draws (kp lanes of the producer warp per stream; ring
+// and L chosen per plan to fit shared memory)
 constexpr int kRingMax = 4096;
 #ifndef K1W_SPEC
 #define K1W_SPEC 1  // draws read before the ring check
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rc = a.rc;  // replica warps 0..rc-1, producer warps rc..rc+nprod-1
   const int n_pad = a.n_words;
-  const int kp = a.kp, SL = a.segl, ringN = a.rounds * kp * SL, rmask = ringN - 1;
+  const int kp = a.kp, SL = a.segl, ringN = a.ring_n, rmask = ringN - 1;
   const bool jt2 = a.jump_table2 != 0;
   const WinLayout L = WinLayout::make(rc, n_pad, GS, INCF, ringN, 0, jt2);
   uint64_t* ring = reinterpret_cast<uint64_t*>(smem + L.ring);
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     // cycles per draw, slower than a consumer visit; kp lanes side by side
     // cut that by ~kp (minus the jump, ~10 ALU instructions per matrix column
     // amortised over SL draws). Rounds cycle through the ring (index = draw
-    // position mod rounds*kp*SL) and are published whole; several rounds
+    // position mod the ring size) and are published whole; several rounds
     // buffered absorb the warp serving the replicas' rounds at different
     // times (a replica's round waits while others' are generated).
     const int round = kp * SL;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     const bool act = l < rc && r < a.replicas;
     Xoshiro rng = Xoshiro::stream(act ? a.seeds[r] : 0ull, 1);  // anneal.cpp:191
     for (int i = 0; i < j * SL; i++) rng.step();                 // to this lane's first segment
-    uint64_t* my = ring + (act ? l : 0) * ringN + j * SL;
+    uint64_t* my = ring + (act ? l : 0) * ringN;
     const unsigned gp_s = saddr(genpos + (act ? l : 0)), cs_s = saddr(cons + (act ? l : 0));
     int gen = 0;  // draws published for this replica (whole rounds)
 #pragma unroll 1
@@ -167,11 +168,13 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       const int cpos = __shfl_sync(0xffffffffu, act ? ld_acquire(cs_s) : 0, lane - j);
       const bool can = act && gen + round <= cpos + ringN;
       if (can) {
-        uint64_t* dst = my + ((gen / round) & (a.rounds - 1)) * round;
+        // 32-draw batches start at multiples of 32, so none straddles the
+        // ring's end (rounds need not divide the ring)
 #pragma unroll 1
         for (int b = 0; b < SL; b += 32) {
+          uint64_t* dst = my + ((gen + j * SL + b) & rmask);
 #pragma unroll
-          for (int k = 0; k < 32; k++) dst[b + k] = rng.next();
+          for (int k = 0; k < 32; k++) dst[k] = rng.next();
         }
         if (kp > 1) {
           if (jt2)
@@ -263,8 +266,7 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
   const uint64_t* myring = ring + cw * ringN;
   const unsigned gp_s = saddr(genpos + cw), cs_s = saddr(cons + cw);
   int gp = 0;
-  int pub = 0;                    // last published consumer position (round-aligned)
-  const int round_w = kp * SL;    // producer round (power of two)
+  int pub = 0;                    // last published consumer position (256-aligned)
   bool aborted = false;
   // loop invariants through a shuffle: kept in registers instead of being
   // re-read from the parameter bank on the step's dependency chain
@@ -433,10 +435,10 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     }
     if (wrote) __syncwarp();  // this step's shared-memory stores before the next step's loads
     // ring slots before pos are consumed (release: their loads are done);
-    // the producer works in whole rounds, so only round crossings are published
-    if ((pos & ~(round_w - 1)) != pub) {
+    // the producer works in whole rounds, so publishing every 256 draws is enough
+    if ((pos & ~255) != pub) {
       if (lane == 0) st_release(cs_s, pos);
-      pub = pos & ~(round_w - 1);
+      pub = pos & ~255;
     }
     if (INCF) {  // spin and field of the pending lanes in one shuffle (decoded next step)
       const int pk = __shfl_down_sync(FULL, (f << 1) | (own > 0 ? 1 : 0), adv);
@@ -542,8 +544,8 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   int kp = 1;
   while (kp < 8 && 2 * kp * rc <= 32) kp *= 2;
   if (const char* e = std::getenv("GDI_WINDOW_KP")) kp = std::atoi(e);  // tuning experiments
-  int nr = 4;  // rounds buffered per replica
-  if (const char* e = std::getenv("GDI_WINDOW_NR")) nr = std::atoi(e);
+  const int nr = 4;  // (minimum ring for the layout checks: nr * kp * 32 draws)
+  const char* ring_env = std::getenv("GDI_WINDOW_RING");  // tuning: ring size (power of two)
   const int cap = 227 * 1024, ring_min = nr * kp * 32;  // sm_100 dynamic shared memory per CTA
   const bool gs = WinLayout::make(rc, n_pad, false, false, ring_min).total > cap ||
                   (force && std::string(force) == "window_gmem");
@@ -558,17 +560,25 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   struct Fit {
     int segl;
     bool msm, jt2;
+    int ring;
   };
   auto fit = [&](int fb) {
-    Fit f{32, false, false};
-    for (int c : {256, 128, 64})
-      if (nr * kp * c <= kRingMax && WinLayout::make(rc, n_pad, gs, fb, nr * kp * c).total <= cap) {
-        f.segl = c;
+    Fit f{32, false, false, 256};
+    // the largest power-of-two ring that fits; segments as long as a round of
+    // kp segments stays within 3/8 of the ring (more than two rounds buffered:
+    // 192 draws for kp = 4 in 2048, measured best of 128..256)
+    for (int rn : {2048, 1024, 512, 256})
+      if (WinLayout::make(rc, n_pad, gs, fb, rn).total <= cap) {
+        f.ring = rn;
         break;
       }
+    f.segl = (f.ring * 3 / 8 / kp) / 32 * 32;
+    f.segl = f.segl < 32 ? 32 : f.segl > 256 ? 256 : f.segl;
     if (const char* e = std::getenv("GDI_WINDOW_SEGL")) f.segl = std::atoi(e);
-    f.msm = fb == 0 && WinLayout::make(rc, n_pad, gs, fb, nr * kp * f.segl, mw).total <= cap;
-    f.jt2 = kp > 1 && WinLayout::make(rc, n_pad, gs, fb, nr * kp * f.segl, f.msm ? mw : 0, true).total <= cap;
+    if (ring_env) f.ring = std::atoi(ring_env);
+    const int rn = f.ring;
+    f.msm = fb == 0 && WinLayout::make(rc, n_pad, gs, fb, rn, mw).total <= cap;
+    f.jt2 = kp > 1 && WinLayout::make(rc, n_pad, gs, fb, rn, f.msm ? mw : 0, true).total <= cap;
     return f;
   };
   // exact field type: int16, or int8 (|field| <= 127) when that frees room for a
@@ -577,7 +587,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   Fit ft = fit(fb);
   if (incf && st.max_abs_field <= 127) {
     const Fit f8 = fit(1);
-    if (f8.segl > ft.segl || (f8.jt2 && !ft.jt2)) {
+    if (f8.ring > ft.ring || f8.segl > ft.segl || (f8.jt2 && !ft.jt2)) {
       fb = 1;
       ft = f8;
     }
@@ -591,6 +601,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
   plan->segl = segl;
   plan->masks_smem = msm;
   plan->rounds = nr;
+  plan->ring_n = ft.ring;
   const bool unitab = ra == 1 && rb == 1;
   plan->fn = st.unit ? (unitab ? win_fn<false, true>(gs, fb) : win_fn<false, false>(gs, fb))
                      : (unitab ? win_fn<true, true>(gs, fb) : win_fn<true, false>(gs, fb));
@@ -608,7 +619,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
     plan->block = 32 * (rc + plan->nprod);
   }
   plan->grid = (replicas + rc - 1) / rc;
-  plan->smem = WinLayout::make(rc, n_pad, gs, fb, nr * kp * segl, msm ? mw : 0, jt2).total;
+  plan->smem = WinLayout::make(rc, n_pad, gs, fb, plan->ring_n, msm ? mw : 0, jt2).total;
   plan->n_words = n_pad;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
@@ -636,6 +647,7 @@ cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream
   a.kp = plan.kp;
   a.segl = plan.segl;
   a.rounds = plan.rounds;
+  a.ring_n = plan.ring_n;
   a.masks_smem = plan.masks_smem ? 1 : 0;
   a.jump_table2 = plan.jt2 ? 1 : 0;
   a.jump = nullptr;

@@ -64,6 +64,7 @@ struct PipeArgs {
   int32_t kp;                      // k1_window: producer lanes per replica stream
   int32_t segl;                    // k1_window: draws per producer segment
   int32_t rounds;                  // k1_window: producer rounds buffered per replica (power of two)
+  int32_t ring_n;                  // k1_window: draws per replica ring (power of two, multiple of 32)
   int32_t masks_smem;              // k1_window: window masks copied to shared memory
   int32_t jump_table2;             // k1_window: jump is the two-column table (xoshiro_jump2)
   const uint64_t* jump;            // k1_window: (kp-1)*segl-draw xoshiro jump matrix [256][4]

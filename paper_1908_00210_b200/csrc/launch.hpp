@@ -61,6 +61,7 @@ struct PipePlan {
   int kp = 1;       // k1_window: producer lanes per replica stream
   int segl = 64;    // k1_window: draws per producer segment
   int rounds = 4;   // k1_window: producer rounds buffered per replica
+  int ring_n = 2048;  // k1_window: draws per replica ring
   bool masks_smem = false;  // k1_window: window masks in shared memory
   bool jt2 = false;         // k1_window: two-column jump table
   const char* name = "";
