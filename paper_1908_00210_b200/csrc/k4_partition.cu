@@ -480,15 +480,18 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->ctas = ctas < 1 ? 1 : ctas;
   plan->chains = plan->ctas * kNW;
   // tail chunks run by the last CTA against the exact counter (see k4_sweep)
-  // 8 chunks: the chains' residual after the CTA tails is a few spins; a
-  // 32-chunk tail balanced no better (M1 and a 100k graph, 4 seeds: final
-  // imbalance 0 either way) and cost a fifth of the M1 sweep, the last CTA
-  // deciding its chunks in order against a counter that cascades through them
+  // one device: 8 chunks. The chains' residual after the CTA tails is a few
+  // spins; a 32-chunk tail balanced no better (M1 and a 100k graph, 4 seeds:
+  // final imbalance 0 either way) and cost a fifth of the M1 sweep (the last
+  // CTA decides its chunks in order against a counter that cascades through
+  // them). Partitioned over ranks the residuals of every rank's chains add
+  // up: 8 chunks left a fused W=4 run imbalanced, so 32 there.
   constexpr int kTailDefault = 8;
   plan->tail = nck / 8 < kTailDefault ? nck / 8 : kTailDefault;
+  plan->tail_multi = nck / 8 < kTailMax ? nck / 8 : kTailMax;
   if (const char* e = std::getenv("GDI_K4_TAIL")) {  // tuning experiments
     const int t = std::atoi(e);
-    plan->tail = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
+    plan->tail = plan->tail_multi = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
   }
   plan->sweep_fn = wkind == 0 ? sweep_fn<0>(kmax) : wkind == 1 ? sweep_fn<1>(kmax) : sweep_fn<2>(kmax);
   plan->gtail_fn = wkind == 0 ? gtail_fn<0>(kmax) : wkind == 1 ? gtail_fn<1>(kmax) : gtail_fn<2>(kmax);
@@ -516,7 +519,7 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   PartArgs a = args;
   a.a4 = plan.a4;
   a.b = plan.b;
-  a.tail = plan.tail;
+  a.tail = a.world == 1 ? plan.tail : plan.tail_multi;
   a.tail_ticket = a.world == 1 ? 1 : 0;  // ranks > 1: k4_gtail after the exchange
   const char* dbg = std::getenv("GDI_K4_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;

@@ -95,7 +95,8 @@ struct PartPlan {
   int32_t a4 = 4, b = 4;
   int ctas = 1;        // per replica
   int chains = 16;     // per replica (one per warp)
-  int tail = 0;        // tail chunks (exact counter) per sweep
+  int tail = 0;        // tail chunks (exact counter) per sweep, one device
+  int tail_multi = 0;  // the same when the graph is partitioned over ranks
   int block = 512;
   int pack_grid = 148, cut_grid = 148;
   const char* name = "";
