@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -230,7 +231,17 @@ namespace {
 // graph.cpp:47-61 invariants on the host, before any device work, so that a
 // bad CSR is a domain error on every machine (the statistics come from the
 // device pass). Rows are split over host threads for large graphs.
-int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int stride) {
+// Host validation of the caller's CSR (domain errors come before any device
+// work). With stage != nullptr the same row-parallel pass copies offsets,
+// adjacency (stride 1 or 2 int32 per entry) and weights into the pinned
+// staging buffer (layout: offsets | adjacency | weights), so the upload runs
+// at link speed instead of the driver's pageable staging.
+int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int stride, const int32_t* weights = nullptr,
+                  char* stage = nullptr) {
+  const int64_t nnz = offsets[n];
+  int64_t* st_off = reinterpret_cast<int64_t*>(stage);
+  int32_t* st_adj = stage ? reinterpret_cast<int32_t*>(stage + (static_cast<size_t>(n) + 1) * 8) : nullptr;
+  int32_t* st_w = stage ? st_adj + static_cast<size_t>(nnz) * stride : nullptr;
   auto rows = [&](int32_t lo, int32_t hi) -> int {
     for (int32_t i = lo; i < hi; i++) {
       const int64_t o0 = offsets[i], o1 = offsets[i + 1];
@@ -241,10 +252,16 @@ int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int str
         if (v == i) return 3;
       }
     }
+    if (stage) {  // rows valid, so offsets[lo] <= offsets[hi] <= nnz
+      const int64_t e0 = offsets[lo], e1 = offsets[hi];
+      std::memcpy(st_off + lo, offsets + lo, static_cast<size_t>(hi - lo + (hi == n ? 1 : 0)) * 8);
+      std::memcpy(st_adj + e0 * stride, nbr + e0 * stride, static_cast<size_t>(e1 - e0) * stride * 4);
+      if (weights) std::memcpy(st_w + e0, weights + e0, static_cast<size_t>(e1 - e0) * 4);
+    }
     return 0;
   };
   // rows are split evenly; below ~1M adjacency entries one thread does it all
-  const size_t min_rows = offsets[n] < (1 << 20) ? static_cast<size_t>(n) + 1 : 0;
+  const size_t min_rows = nnz < (1 << 20) ? static_cast<size_t>(n) + 1 : 0;
   std::vector<int> codes(16, 0);
   std::atomic<unsigned> slot{0};
   parallel_rows(static_cast<size_t>(n), min_rows, [&](size_t lo, size_t hi) {
@@ -270,8 +287,30 @@ int create_graph(int device, int32_t n, const int64_t* offsets, const int32_t* n
     return fail(GDI_ERR_DOMAIN, "offsets must start at 0 and hold an even entry count");
   if (nnz > 0x7fffffffLL) return fail(GDI_ERR_CAPACITY, "more than 2^31-1 adjacency entries");
   if (nnz > 0 && !(pairs ? pairs : nbr)) return fail(GDI_ERR_DOMAIN, "adjacency is NULL");
-  int rc = validate_host(n, offsets, pairs ? pairs : nbr, pairs ? 2 : 1);
+  const bool timing = std::getenv("GDI_TIMING") != nullptr;  // phase times on stderr (tuning)
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  // large graphs: validated and staged into pinned memory in one pass
+  // (pinned allocation is host-only; the device is touched after validation)
+  const int stride = pairs ? 2 : 1;
+  const size_t stage_bytes = (static_cast<size_t>(n) + 1) * 8 + static_cast<size_t>(nnz) * stride * 4 +
+                             (weights && !pairs ? static_cast<size_t>(nnz) * 4 : 0);
+  thread_local PinnedBuf upload_stage;
+  char* stage = nullptr;
+  if (nnz >= (1 << 20) && upload_stage.ensure(stage_bytes) == cudaSuccess) stage = upload_stage.as<char>();
+  int rc = validate_host(n, offsets, pairs ? pairs : nbr, stride, pairs ? nullptr : weights, stage);
   if (rc) return rc;
+  if (stage) {  // upload from the staged copy
+    const int64_t* so = reinterpret_cast<const int64_t*>(stage);
+    const int32_t* sa = reinterpret_cast<const int32_t*>(stage + (static_cast<size_t>(n) + 1) * 8);
+    offsets = so;
+    if (pairs)
+      pairs = sa;
+    else
+      nbr = sa;
+    if (weights && !pairs) weights = sa + static_cast<size_t>(nnz);
+  }
+  const double t_val = ms();
 
   auto g = std::make_unique<gdi_graph>();
   g->device = device;
@@ -282,9 +321,13 @@ int create_graph(int device, int32_t n, const int64_t* offsets, const int32_t* n
   GraphScan scan{};
   cudaStream_t st = nullptr;
   GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const double t_dev = ms();
   const cudaError_t ue = upload_and_scan(offsets, nbr, weights, pairs, n, nnz, g->off, g->col, g->w, &scan, st);
   cudaStreamDestroy(st);
   GDI_CUDA(ue);
+  if (timing)
+    std::fprintf(stderr, "[gdi_graph_create] validate %.2f ms, device setup %.2f ms, upload+scan %.2f ms\n", t_val,
+                 t_dev - t_val, ms() - t_dev);
   if (scan.bad & 1u) return fail(GDI_ERR_DOMAIN, "offsets not monotone");
   if (scan.bad & 2u) return fail(GDI_ERR_DOMAIN, "edge endpoint out of range");
   if (scan.bad & 4u) return fail(GDI_ERR_DOMAIN, "self-loop");
