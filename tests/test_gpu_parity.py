@@ -234,3 +234,19 @@ def test_window_jump_forms_bit_exact(jt2, kernel_variant, monkeypatch):
         pytest.skip("default kernel only")
     monkeypatch.setenv("GDI_WINDOW_JT2", jt2)
     check_batch_against_golden("G22", count=64)
+
+
+@pytest.mark.parametrize("big", [600, 1800])
+def test_exact_results_independent_of_batch_size(big, kernel_variant):
+    """Exact mode: a replica's anneal depends on its seed only. Large batches
+    change the kernel's shape (replicas per CTA 5 and 13 -> 12, producer lanes
+    per stream 4 and 2, more CTAs than SMs at 1800) but not a single spin."""
+    if kernel_variant != "auto":
+        pytest.skip("default kernel only")
+    g = product_graph(golden_configs()["G1"]["recipe"])
+    prob = pi.MinCutProblem.with_default_coefficients(g)
+    p = det_params(sweeps=200)
+    small = pi.anneal_batch(prob, p, np.arange(1, 65, dtype=np.uint64), True)
+    large = pi.anneal_batch(prob, p, np.arange(1, big + 1, dtype=np.uint64), True)
+    assert np.array_equal(small["spins"], large["spins"][:64])
+    assert np.array_equal(small["trace"], large["trace"][:64])
