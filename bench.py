@@ -246,11 +246,13 @@ def run_partition_bench(args, pi, torch, dist, world, rank, local, dev, recipe, 
             "config": {"workload": f"M1: {' '.join(recipe)}, one replica vertex-partitioned over {world} GPUs, "
                                    f"{sweeps} sweeps, pooled throughput mode",
                        "n": n, "m": m, "replicas": 1, "sweeps": sweeps,
-                       "parallelism": f"vertex partition x{world}: chunks c = rank (mod {world}), "
-                                      "1 packed spin all-gather per sweep (NCCL)",
+                       "parallelism": f"vertex partition x{world}: chunks c = rank (mod {world}); spin changes "
+                                      "stored into the other ranks' copies over peer memory during the sweep "
+                                      "(CUDA IPC), per sweep a 16-byte counter all-gather + a barrier all-reduce",
                        "l2": "flushed between steps (256 MB write)", "kernel": "k4_sweep (partitioned)"},
             "clocks": clocks.summary(),
-            "gpu_launches": args.steps * (1 + 5 * sweeps),
+            # per sweep: k4_sweep, xpack, xunpack, global tail, pack, cut (+ init once)
+            "gpu_launches": args.steps * (1 + 6 * sweeps),
             "result": {"cut": out["cut"], "imbalance": out["imbalance"]},
         }
         print(json.dumps(line), flush=True)
