@@ -57,10 +57,14 @@ namespace {
 
 constexpr int kNW = 16;  // warps per CTA
 #ifndef K4_DEFER
-#define K4_DEFER 2
+#define K4_DEFER 1
 #endif
-constexpr int kDefer = K4_DEFER;  // chunks per chain deferred to the CTA tail
-constexpr int kTailMax = 32;  // global tail chunks (= kDefer * kNW: shares stage[])
+// chunks per chain deferred to the CTA tail: warp 0 decides the CTA's 16 *
+// kDefer tail chunks in order while the other warps wait, ~30% of an M1 sweep
+// with 2 (1.74 -> 1.53 ms per 20 sweeps with 1, balance unchanged; 0 leaves
+// sweeps imbalanced)
+constexpr int kDefer = K4_DEFER;
+constexpr int kTailMax = 32;  // global tail chunks (>= kDefer * kNW: shares stage[])
 constexpr int kPackBlock = 256;
 constexpr int kCutBlock = 512;
 
