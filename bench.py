@@ -206,6 +206,31 @@ def run_reference_arm(args):
     return 0
 
 
+def topology_only(args):
+    """Process-group plumbing of the multi-rank bench without any GPU work:
+    every rank joins (BENCH_DIST_BACKEND, default nccl), rank 0 prints the
+    world it saw (tests/test_bench_launch.py runs this with gloo on CPU)."""
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if world > 1:
+        dist.init_process_group(backend)
+        import torch
+
+        t = torch.tensor([rank], dtype=torch.int64)
+        dist.all_reduce(t)
+        ranks_sum = int(t.item())
+        dist.destroy_process_group()
+    else:
+        ranks_sum = 0
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "ranks_sum": ranks_sum, "requested": args.gpus,
+                          "backend": backend if world > 1 else None}), flush=True)
+    return 0
+
+
 def run_partition_bench(args, pi, torch, dist, world, rank, local, dev, recipe, g, prob, params):
     """BASELINE configs[4] on N GPUs: ONE replica of the 1M-vertex graph,
     vertex-partitioned (sharding.anneal_partitioned: K4 chains per rank, one
@@ -260,6 +285,35 @@ def run_partition_bench(args, pi, torch, dist, world, rank, local, dev, recipe, 
     return 0
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(nproc: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run, one rank per GPU on this node (rendezvous on
+    127.0.0.1), and return its exit code. Rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    return "unknown"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -273,8 +327,15 @@ def main():
     ap.add_argument("--no-throughput", action="store_true")
     ap.add_argument("--mode", default="exact", choices=["exact", "throughput"],
                     help="headline mode: exact (bit-exact, default) or throughput (pooled racy mode)")
+    ap.add_argument("--topology-only", action="store_true",
+                    help="initialise the ranks, print the rank/world line and exit (launcher test)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # the driver runs `bench.py --gpus N` directly: launch N ranks here
+        return spawn_ranks(args.gpus)
+    if args.topology_only:
+        return topology_only(args)
     if args.impl == "reference":
         return run_reference_arm(args)
 

@@ -205,6 +205,12 @@ int gdi_part_destroy(gdi_part* s);
 int gdi_part_ipc_handle(const gdi_part* s, void* handle);
 int gdi_part_attach_peers(gdi_part* s, const void* handles);
 int gdi_part_attach_local(gdi_part* s, gdi_part* const* parts);
+/* Teardown order for the fused exchange: every rank calls gdi_part_detach
+ * (waits for its stream, closes the peers' IPC mappings), then the ranks
+ * synchronise (a process-group barrier), then gdi_part_destroy frees this
+ * rank's exported copy. Destroying an exporter while a peer still has its
+ * copy open is undefined behaviour in CUDA. */
+int gdi_part_detach(gdi_part* s);
 
 /* Measurement utility (not a reference interface): sustained read bandwidth
  * in GB/s of an L2-resident buffer of `bytes` bytes re-read `iters` times on

@@ -245,7 +245,9 @@ int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int str
   auto rows = [&](int32_t lo, int32_t hi) -> int {
     for (int32_t i = lo; i < hi; i++) {
       const int64_t o0 = offsets[i], o1 = offsets[i + 1];
-      if (o1 < o0) return 1;
+      // bounds before any adjacency read or staging copy: a monotone prefix
+      // that overshoots nnz must not read past the caller's arrays
+      if (o1 < o0 || o0 < 0 || o1 > nnz) return 1;
       for (int64_t e = o0; e < o1; e++) {
         const int32_t v = nbr[e * stride];
         if (v < 0 || v >= n) return 2;
@@ -1123,6 +1125,18 @@ int gdi_part_fetch(gdi_part* s, gdi_outputs* out) {
       t.seconds = static_cast<double>(st[k + 1] - st[k]) * 1e-9;
     }
   }
+  return GDI_OK;
+}
+
+int gdi_part_detach(gdi_part* s) {
+  if (!s) return fail(GDI_ERR_CONFIG, "NULL argument");
+  GDI_CUDA(cudaSetDevice(s->g->device));
+  if (s->stream) GDI_CUDA(cudaStreamSynchronize(s->stream));
+  for (void* q : s->ipc_opened) GDI_CUDA(cudaIpcCloseMemHandle(q));
+  s->ipc_opened.clear();
+  for (int q = 0; q < 7; q++) s->args.peer[q] = nullptr;
+  s->args.npeer = 0;
+  s->peer = false;
   return GDI_OK;
 }
 

@@ -482,8 +482,9 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
     const unsigned genpos_s = saddr(genpos + lane), cons_s = saddr(cons + lane), done_s = saddr(done);
     int gen = 0;
     long long p_t0 = PROF ? clock64() : 0, p_wait = 0;
+    long long idle = 0;  // consecutive polls without progress (watchdog)
 #pragma unroll 1
-    for (long long spins = 0;; spins++) {
+    for (;;) {
       const int c = ld_acquire(cons_s);
       const bool can = gen + 8 <= c + kRing;
       if (can) {
@@ -492,12 +493,14 @@ __global__ void __launch_bounds__(32 * kNW, 1) k1_pipe(const PipeArgs a) {
         gen += 8;
         st_release(genpos_s, gen);
       }
-      if (!__any_sync(0xffffffffu, can)) {
+      if (__any_sync(0xffffffffu, can)) {
+        idle = 0;
+      } else {
         if (ld_acquire(done_s) || ld_acquire(abort_s)) break;
         const long long p_a = PROF ? clock64() : 0;
         __nanosleep(64);
         if (PROF) p_wait += clock64() - p_a;
-        if (spins > kWatchdog) {
+        if (++idle > kWatchdog) {
           watchdog(a, abort_s, 3, gen, c);
           break;
         }

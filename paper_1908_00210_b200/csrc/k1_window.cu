@@ -162,8 +162,9 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
     uint64_t* my = ring + (act ? l : 0) * ringN;
     const unsigned gp_s = saddr(genpos + (act ? l : 0)), cs_s = saddr(cons + (act ? l : 0));
     int gen = 0;  // draws published for this replica (whole rounds)
+    long long idle = 0;  // consecutive polls without a round to generate (watchdog)
 #pragma unroll 1
-    for (long long spin = 0;; spin++) {
+    for (;;) {
       // one consumer position per replica group (the group's lanes must agree)
       const int cpos = __shfl_sync(0xffffffffu, act ? ld_acquire(cs_s) : 0, lane - j);
       const bool can = act && gen + round <= cpos + ringN;
@@ -187,12 +188,14 @@ __global__ void __launch_bounds__(512, 1) k1_window(const PipeArgs a) {
       }
       __syncwarp();
       if (can && j == 0) st_release(gp_s, gen);
-      if (!__any_sync(0xffffffffu, can)) {
+      if (__any_sync(0xffffffffu, can)) {
+        idle = 0;
+      } else {
         // ring full: a short sleep keeps this warp's polling off the issue
         // slots the consumers need
         if (ld_acquire(done_s) >= rc || ld_acquire(abort_s)) break;
         __nanosleep(32);
-        if (spin > kWatchdog) {
+        if (++idle > kWatchdog) {  // no consumer progress for ~2^28 polls
           st_release(abort_s, 1);
           if (a.watchdog != nullptr) atomicCAS(a.watchdog, 0, 30);
           break;

@@ -227,6 +227,7 @@ public:
     const std::string hs = handles;
     check_abi(gdi_part_attach_peers(sess_, hs.data()));
   }
+  void detach() { check_abi(gdi_part_detach(sess_)); }
   void attach_local(const std::vector<PartSession*>& parts) {
     std::vector<gdi_part*> ps;
     for (PartSession* q : parts) ps.push_back(q->sess_);
@@ -633,6 +634,8 @@ PYBIND11_MODULE(pyising, m) {
       .def("ipc_handle", &PartSession::ipc_handle, "this rank's spin copy as a CUDA IPC handle (bytes)")
       .def("attach_peers", &PartSession::attach_peers, py::arg("handles"),
            "fused exchange: every rank's ipc_handle(), rank-major, concatenated")
+      .def("detach", &PartSession::detach,
+           "close the peers' IPC mappings (call on every rank, then barrier, before dropping the session)")
       .def("attach_local", &PartSession::attach_local, py::arg("parts"),
            "fused exchange between partitions of this process on one device (testing)")
       .def("sweep", &PartSession::sweep, py::arg("k"), py::arg("send"))

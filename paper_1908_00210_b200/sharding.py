@@ -174,7 +174,14 @@ def anneal_partitioned(problem, params, seed: int, dist, device: int, stream=Non
         dist.all_reduce(t)
         return t.cpu().numpy()
 
-    return combine(res, all_reduce_sum)
+    out = combine(res, all_reduce_sum)
+    if fused and world > 1:
+        # teardown order (gdi.h gdi_part_detach): close the peers' mappings on
+        # every rank, barrier, and only then free the exported copies
+        ps.detach()
+        dist.barrier()
+    del ps
+    return out
 
 
 def emulate_partitioned(problem, params, seed: int, world: int, device: int = 0, fused: bool = False) -> dict:
