@@ -100,9 +100,11 @@ struct gdi_session {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ExactPlan plan;
+  BlockPlan bplan;
   PipePlan pplan;
   ThruPlan tplan;
   PartPlan kplan;
+  bool use_block = false;  // k1_block (exact mode default)
   bool use_pipe = false;
   bool use_win = false;  // the pipe plan is a k1_window plan
   bool use_thru = false;
@@ -337,6 +339,7 @@ int create_graph(int device, int32_t n, const int64_t* offsets, const int32_t* n
   g->st.max_abs_field = static_cast<long long>(scan.max_abs_field);
   g->st.max_degree = scan.max_degree;
   g->wkind = g->st.unit ? 0 : (!scan.non_pm1 ? 1 : 2);
+  g->st.pm1 = g->wkind <= 1;
   // k1_pipe eligibility (every |w| == 1, n >= 2L); its layout is built lazily
   g->pipe.ok = n >= 2 * pipe_window() && (g->st.unit || !scan.non_pm1);
   g->pipe.n_words = (n + 1 + 3) & ~3;
@@ -446,11 +449,18 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   else if (thru_ok && force != "part" &&
            thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
     s->use_thru = true;
-  // exact mode: k1_window (speculative visit windows) by default; k1_pipe on
-  // request (GDI_FORCE_KERNEL=pipe|pipe_gmem); k1_exact for everything else
+  // exact mode: k1_block (fixed-point windows) by default; k1_window
+  // (speculative windows) where k1_block does not fit; k1_pipe on request
+  // (GDI_FORCE_KERNEL=pipe|pipe_gmem); k1_exact for everything else
   const bool want_pipe = force == "pipe" || force == "pipe_gmem";
   bool pipe_ok = false;
-  if (!s->use_thru && force != "exact" && !want_pipe &&
+  if (!s->use_thru && (force.empty() || force == "auto" || force == "block") &&
+      block_plan(g->st, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->bplan) == 0)
+    s->use_block = true;
+  if (force == "block" && !s->use_block)
+    return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=block but k1_block does not apply");
+  if (s->use_block) {
+  } else if (!s->use_thru && force != "exact" && !want_pipe &&
       window_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0) {
     pipe_ok = true;
     s->use_win = true;
@@ -461,7 +471,7 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
     return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=window but k1_window does not apply");
   if ((force == "pipe" || force == "pipe_gmem") && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
   s->use_pipe = pipe_ok;
-  if (!s->use_thru && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
+  if (!s->use_thru && !s->use_block && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
   gdi_graph* gm = const_cast<gdi_graph*>(g);  // layouts are a lazily built cache
   if (s->use_thru && (rc = ensure_thru(gm))) return rc;
@@ -755,6 +765,7 @@ int gdi_session_launch(gdi_session* s) {
   a.replicas = s->replicas;
   a.seeds = s->seeds.as<uint64_t>();
   a.thr = s->thr_d.as<long long>();
+  a.tmask = s->tmask_d.as<unsigned long long>();
   a.a4 = 4 * s->p.a_num;
   a.b = s->p.b_num;
   a.spins_out = s->spins.as<int8_t>();
@@ -763,7 +774,7 @@ int gdi_session_launch(gdi_session* s) {
   a.snaps = s->snaps.as<int8_t>();
   a.final_out = s->final_out.as<DevTrace>();
   GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
-  GDI_CUDA(exact_launch(s->plan, a, s->stream));
+  GDI_CUDA(s->use_block ? block_launch(s->bplan, a, s->stream) : exact_launch(s->plan, a, s->stream));
   GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
   s->launched = true;
   return GDI_OK;
@@ -829,6 +840,7 @@ const char* gdi_session_kernel(const gdi_session* s) {
   if (!s) return "";
   if (s->use_part) return s->kplan.name;
   if (s->use_thru) return s->tplan.name;
+  if (s->use_block) return s->bplan.name;
   return s->use_pipe ? s->pplan.name : s->plan.name;
 }
 

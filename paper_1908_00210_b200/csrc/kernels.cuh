@@ -32,6 +32,7 @@ struct ExactArgs {
   int32_t replicas;
   const uint64_t* seeds;  // [R]
   const long long* thr;   // [sweeps] flip threshold on (x >> 11); -1 = never
+  const unsigned long long* tmask;  // [sweeps] thr*2^11 + 2047 (k1_block)
   long long a4;           // 4 * a_num
   long long b;            // b_num
   int8_t* spins_out;      // [R][n]

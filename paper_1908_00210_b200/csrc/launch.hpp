@@ -14,6 +14,7 @@ struct GraphStats {
   int64_t m = 0;
   int32_t max_degree = 0;
   bool unit = true;
+  bool pm1 = false;             // every |w| == 1 (unit or +-1)
   long long max_abs_field = 0;  // max_i sum_j |w_ij|
 };
 
@@ -76,6 +77,17 @@ cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t
 int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b,
                 int32_t sweeps, PipePlan* plan);
 cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);
+
+// k1_block (aligned windows resolved to a fixed point, per-warp draws)
+struct BlockPlan {
+  const void* fn = nullptr;
+  int32_t a4 = 4, b = 4;  // coefficients reduced by gcd(4A, B)
+  int rc = 1;             // replica warps per CTA
+  int block = 32, grid = 1, smem = 0, nnz = 0;
+  const char* name = "";
+};
+int block_plan(const GraphStats& st, int32_t replicas, int64_t a4, int64_t b, int32_t sweeps, BlockPlan* plan);
+cudaError_t block_launch(const BlockPlan& plan, const ExactArgs& args, cudaStream_t stream);
 
 struct ThruPlan {
   const void* fn = nullptr;

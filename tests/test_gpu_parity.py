@@ -16,10 +16,11 @@ from tests.helpers import fnv_rows, golden_configs, product_graph, small_cases
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "exact"])
+@pytest.fixture(autouse=True, params=["auto", "legacy", "exact"])
 def kernel_variant(request, monkeypatch):
-    """Run every parity test on both exact-mode kernels: the warp-specialised
-    pipe kernel (chosen automatically where it applies) and k1_exact."""
+    """Run every parity test on the exact-mode kernels: k1_block (chosen
+    automatically where it fits), k1_window (GDI_FORCE_KERNEL=legacy: the
+    automatic choice where k1_block does not fit) and k1_exact."""
     monkeypatch.setenv("GDI_FORCE_KERNEL", request.param)
     return request.param
 
@@ -173,7 +174,8 @@ def test_session_device_resident_matches_batch(kernel_variant):
     assert np.array_equal(got["spins"], ref["spins"])
     assert np.array_equal(got["trace"], ref["trace"])
     assert s.launch_count >= 1 and s.kernel
-    assert ("window" in s.kernel) == (kernel_variant == "auto")
+    assert ("block" in s.kernel) == (kernel_variant == "auto")
+    assert ("window" in s.kernel) == (kernel_variant == "legacy")
 
 
 def test_pipe_window_edge_cases_match_oracle():
@@ -220,7 +222,7 @@ def test_forced_exact_variants_bit_exact(name, count, variant, kernel_variant, m
 
 
 def test_m1_million_vertices_bit_exact(kernel_variant):
-    if kernel_variant != "auto":
+    if kernel_variant == "exact":
         pytest.skip("k1_exact keeps spins in shared memory: 1M does not fit (capacity)")
     out = check_batch_against_golden("M1")
     assert out["cut"][0] == 1252631 and out["imbalance"][0] == 0
@@ -230,8 +232,8 @@ def test_m1_million_vertices_bit_exact(kernel_variant):
 def test_window_jump_forms_bit_exact(jt2, kernel_variant, monkeypatch):
     """k1_window's producer jump as the plain bit matrix (configs whose shared
     memory is full) and as the two-column table: same draws, same anneal."""
-    if kernel_variant != "auto":
-        pytest.skip("default kernel only")
+    if kernel_variant != "legacy":
+        pytest.skip("k1_window only")
     monkeypatch.setenv("GDI_WINDOW_JT2", jt2)
     check_batch_against_golden("G22", count=64)
 
@@ -241,8 +243,8 @@ def test_exact_results_independent_of_batch_size(big, kernel_variant):
     """Exact mode: a replica's anneal depends on its seed only. Large batches
     change the kernel's shape (replicas per CTA 5 and 13 -> 12, producer lanes
     per stream 4 and 2, more CTAs than SMs at 1800) but not a single spin."""
-    if kernel_variant != "auto":
-        pytest.skip("default kernel only")
+    if kernel_variant == "exact":
+        pytest.skip("k1_block and k1_window only")
     g = product_graph(golden_configs()["G1"]["recipe"])
     prob = pi.MinCutProblem.with_default_coefficients(g)
     p = det_params(sweeps=200)
