@@ -110,15 +110,48 @@ class ClockSampler:
 
 
 def measured_traffic(config: str, kernel: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/roofline_traffic.json), or None."""
+    """Per-launch traffic of the dominant kernel from the committed ncu
+    --set full capture (profiles/roofline_traffic.json): DRAM bytes
+    (dram__bytes_read.sum + dram__bytes_write.sum), L2 bytes (lts__t_bytes.sum)
+    and shared-memory wavefronts, or None when no capture of this kernel is
+    committed."""
     try:
         with open(os.path.join(REPO, "profiles", "roofline_traffic.json")) as f:
             doc = json.load(f)
     except OSError:
         return None
-    rec = doc.get(f"{config}:{kernel}")
-    return rec["dram_bytes_per_launch"] if rec else None
+    return doc.get(f"{config}:{kernel}")
+
+
+def roofline(bpu: float, updates: float, ms: float, l2: float, hbm: float, peaks_src: str,
+             traffic, working_set: int, l2_size: int, note: str):
+    """SURVEY.md 8(d) accounting: achieved = updates/s x B_logical against the
+    peak of the level that holds the working set (L2 when the CSR + spins fit
+    in L2, HBM otherwise)."""
+    achieved = bpu * updates / (ms * 1e-3) / 1e9
+    in_l2 = working_set <= l2_size
+    peak = l2 if in_l2 else hbm
+    rec = {"bound": "l2" if in_l2 else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": achieved / peak,
+           "traffic": None, "bytes_per_update": bpu, "working_set_bytes": working_set,
+           "l2_bytes": l2_size,
+           "peak_source": ("live L2 read probe (probe.cu: 16-byte __ldcg loads of a 48 MB L2-resident "
+                           "buffer, 4 CTAs/SM x 512 threads, 50 passes; profiles/l2_peak.json)") if in_l2
+                          else peaks_src,
+           "hbm_peak_gbs": hbm, "frac_of_hbm": achieved / hbm, "l2_peak_gbs": l2, "note": note}
+    if traffic:
+        units = traffic.get("updates_per_launch")
+        lps = traffic.get("launches_per_step", 1)
+        # per step, like `achieved` (M1: one k4_sweep launch per sweep)
+        rec["traffic"] = traffic["dram_bytes_per_launch"] * lps if traffic.get("dram_bytes_per_launch") else None
+        if traffic.get("lts_bytes_per_launch"):
+            rec["l2_traffic"] = traffic["lts_bytes_per_launch"] * lps
+        rec["traffic_source"] = traffic.get("source")
+        if units:
+            rec["measured_per_update"] = {
+                k: traffic[k] / units for k in ("dram_bytes_per_launch", "lts_bytes_per_launch",
+                                                "smem_wavefronts_per_launch") if traffic.get(k) is not None}
+    return rec
 
 
 def l2_probe_gbs(pi) -> float:
@@ -153,6 +186,10 @@ def cpu_port_bench(recipe, sweeps, replicas, seed0=1):
     return {"seconds": s, "updates_per_s": replicas * g.n * sweeps / s, "threads": 1, "replicas": replicas}
 
 
+def host_cpu():
+    return {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
+
+
 def cpu_baseline(recipe, n, sweeps):
     threads = os.cpu_count() or 1
     # bounded sample: ~20 CPU-seconds of reference work (one G22 replica is
@@ -162,12 +199,12 @@ def cpu_baseline(recipe, n, sweeps):
     res = cpu_reference_bench(recipe, sweeps, reps, threads)
     if res is not None:
         return {"value": res["updates_per_s"], "unit": "spin-updates/s", "cores": res["threads"],
-                "kind": "reference",
+                "kind": "reference", **host_cpu(),
                 "sample": f"{reps} deterministic single-worker anneals ({sweeps} sweeps) on a "
                           f"{res['threads']}-thread pool, oracle/_ref/ref_tool (bench.cpp:158-175 scheduling)"}
     reps = 2
     res = cpu_port_bench(recipe, sweeps, reps)
-    return {"value": res["updates_per_s"], "unit": "spin-updates/s", "cores": 1, "kind": "port",
+    return {"value": res["updates_per_s"], "unit": "spin-updates/s", "cores": 1, "kind": "port", **host_cpu(),
             "sample": f"{reps} anneals ({sweeps} sweeps) with the C restatement, 1 core"}
 
 
@@ -199,7 +236,7 @@ def run_reference_arm(args):
         "config": {"workload": f"{args.config}: {' '.join(recipe)}, deterministic replicas, {sweeps} sweeps",
                    "replicas_per_step": reps if kind == "reference" else 1},
         "cpu_baseline": {"value": value, "unit": "spin-updates/s", "cores": threads if kind == "reference" else 1,
-                         "kind": kind, "sample": f"{reps if kind == 'reference' else 1} replicas per step"},
+                         "kind": kind, **host_cpu(), "sample": f"{reps if kind == 'reference' else 1} replicas per step"},
         "e2e": {"value": value, "unit": "spin-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -439,7 +476,6 @@ def main():
     if rank == 0:
         weighted = not g.all_unit_weights
         bpu = algorithmic_bytes_per_update(n, m, weighted)
-        achieved = bpu * R * n * sweeps / (step_ms * 1e-3) / 1e9
         peaks = {}
         try:
             with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -447,7 +483,19 @@ def main():
         except OSError:
             pass
         hbm = peaks.get("hbm_gbs", 6650.0)
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
         l2 = l2_probe_gbs(pi)
+        l2_size = torch.cuda.get_device_properties(dev).L2_cache_size
+        ws = (n + 1) * 4 + 2 * m * 4 + (2 * m if weighted else 0) + R * n  # compact CSR + int8 spins
+        clk = clocks.summary()
+        rl = roofline(bpu, R * n * sweeps, step_ms, l2, hbm, hbm_src, measured_traffic(args.config, sess.kernel),
+                      ws, l2_size,
+                      ("exact mode: each replica is one serial decision chain (SURVEY 8(d): K1 is latency-bound, "
+                       "see cycles_per_visit); " if args.mode == "exact" else "") +
+                      "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident")
+        if args.mode == "exact" and clk.get("sm_mhz"):
+            # SM cycles per visit of one replica chain (all chains run concurrently)
+            rl["cycles_per_visit"] = step_ms * 1e-3 * clk["sm_mhz"] * 1e6 / (n * sweeps)
         line = {
             "metric": METRIC, "value": value, "unit": "spin-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
@@ -461,14 +509,8 @@ def main():
                                else "throughput (reference pooled racy mode, statistically equivalent)",
                        "parallelism": f"replicas x{world} (weak)", "l2": "flushed between steps (256 MB write)",
                        "kernel": sess.kernel},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": measured_traffic(args.config, sess.kernel),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                         "bytes_per_update": bpu, "l2_peak_gbs": l2, "frac_of_l2": achieved / l2,
-                         "note": ("exact mode is bound by the serial per-replica decision chain, not bandwidth; "
-                                  if args.mode == "exact" else "") +
-                                 "logical bytes per SURVEY 8(d); CSR and spins are L1/L2/smem resident"},
-            "clocks": clocks.summary(),
+            "roofline": rl,
+            "clocks": clk,
             "gpu_launches": args.steps * sess.launch_count,
             "wall_s_timed": t_wall,
             "result": best,
@@ -498,7 +540,6 @@ def main():
         tres = tsess.fetch(spins=False, trace=False)
         if rank == 0:
             tbal = tres["imbalance"] <= n % 2
-            t_ach = bpu * R * n * sweeps / (t_ms * 1e-3) / 1e9
             line["throughput_mode"] = {
                 "value": updates_per_step / (float(tt.item()) * 1e-3), "unit": "spin-updates/s",
                 "ms_per_step": float(tt.item()), "kernel": tsess.kernel,
@@ -506,9 +547,9 @@ def main():
                 "best_balanced_cut": int(tres["cut"][tbal].min()) if tbal.any() else None,
                 "mean_cut": float(tres["cut"].mean()), "frac_balanced": float(tbal.mean()),
                 "gpu_launches": args.steps * tsess.launch_count,
-                "roofline": {"bound": "hbm", "achieved": t_ach, "peak": hbm, "unit": "GB/s", "frac": t_ach / hbm,
-                             "l2_peak_gbs": l2, "frac_of_l2": t_ach / l2, "bytes_per_update": bpu,
-                             "note": "logical bytes (SURVEY 8(d)); CSR and spins are L1/L2/smem resident"}}
+                "roofline": roofline(bpu, R * n * sweeps, t_ms, l2, hbm, hbm_src,
+                                     measured_traffic(args.config, tsess.kernel), ws, l2_size,
+                                     "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident")}
         del tsess
 
     # e2e: the public batched call with host buffers (fresh CSR upload, seeds
