@@ -79,14 +79,15 @@ struct gdi_graph {
   int wkind = 0;  // 0 unit, 1 +-1 (sign bit), 2 general
   // kernel layouts, built on the device the first time a session needs one
   std::mutex mu;
-  bool thru_built = false, pipe_built = false;
+  bool thru_built = false, pipe_built = false, part_built = false;
   ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
+  DevBuf psell, pdeg;  // K4: the SELL rows over visit-order positions, degree by position
   PipeLayout pipel;  // k1_pipe: far lists + window masks
   PipeGraph pipe;    // k1_pipe view (ok = eligible; pointers once built)
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
-                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes +
+                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes +
                                 pipel.far_col.bytes + pipel.far_meta.bytes + pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
                                 pipel.wsell_off.bytes);
@@ -109,12 +110,12 @@ struct gdi_session {
   bool use_win = false;  // the pipe plan is a k1_window plan
   bool use_thru = false;
   bool use_part = false;
-  cudaGraphExec_t part_exec = nullptr;  // k4: 1 + 3M launches replayed as one graph
+  cudaGraphExec_t part_exec = nullptr;  // k4: 1 + 2M launches replayed as one graph
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
   DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords, gspins;
-  DevBuf live, gsum, gdelta, acc, done, finished, bits;  // k4 state
+  DevBuf live, gsum, gdelta, acc, done, finished;  // k4 state (live: position-space spin words)
   DevTrace* tr = nullptr;              // trace records: s->trace, or pinned host memory
   unsigned long long* st = nullptr;    // sweep timestamps: s->stamps, or pinned host memory
   bool host_trace = false;             // one-shot batch: kernels write the trace straight to the host
@@ -179,6 +180,21 @@ int ensure_thru(gdi_graph* g) {
   if (e == cudaErrorInvalidValue) return fail(GDI_ERR_CAPACITY, "SELL layout exceeds 2^31 entries");
   GDI_CUDA(e);
   g->thru_built = true;
+  return GDI_OK;
+}
+
+// K4 rows over positions (after ensure_thru)
+int ensure_part(gdi_graph* g) {
+  int rc = ensure_thru(g);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(g->mu);
+  if (g->part_built) return GDI_OK;
+  cudaStream_t st = nullptr;
+  GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const cudaError_t e = build_part_layout(g->csr(), g->thru, g->psell, g->pdeg, st);
+  cudaStreamDestroy(st);
+  GDI_CUDA(e);
+  g->part_built = true;
   return GDI_OK;
 }
 
@@ -475,6 +491,7 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
   gdi_graph* gm = const_cast<gdi_graph*>(g);  // layouts are a lazily built cache
   if (s->use_thru && (rc = ensure_thru(gm))) return rc;
+  if (s->use_part && (rc = ensure_part(gm))) return rc;
   if (s->use_pipe && (rc = ensure_pipe(gm))) return rc;
 
   if (stream) {
@@ -516,13 +533,12 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   }
   if (p->flags & GDI_FLAG_SNAPSHOTS) GDI_CUDA(s->snaps.alloc(R * (S + 1) * n));
   if (s->use_part) {
-    GDI_CUDA(s->live.alloc(R * part_stride(g->st.n)));
+    GDI_CUDA(s->live.alloc(R * part_words(g->st.n) * sizeof(uint32_t)));
     GDI_CUDA(s->gsum.alloc(R * sizeof(long long)));
     GDI_CUDA(s->gdelta.alloc(R * sizeof(long long)));
     GDI_CUDA(s->acc.alloc(2 * R * sizeof(unsigned long long)));
     GDI_CUDA(s->done.alloc(R * sizeof(unsigned int)));
     GDI_CUDA(s->finished.alloc(R * sizeof(unsigned int)));
-    GDI_CUDA(s->bits.alloc(R * ((n + 31) / 32) * sizeof(uint32_t)));
   }
   GDI_CUDA(cudaMemcpyAsync(s->thr_d.p, s->thr.data(), S * sizeof(long long),
                            cudaMemcpyHostToDevice, s->stream));
@@ -646,13 +662,10 @@ int gdi_session_launch(gdi_session* s) {
       PartArgs a{};
       a.g = s->g->csr();
       a.order = s->g->thru.order.as<int32_t>();
-      a.sell = s->g->thru.sell.as<int4>();
+      a.psell = s->g->psell.as<int4>();
+      a.pdeg = s->g->pdeg.as<int32_t>();
       a.sell_off = s->g->thru.sell_off.as<int32_t>();
       a.sell_w = s->g->thru.sell_w.as<int4>();
-      a.edges = s->g->thru.edges.as<int2>();
-      a.edge_w = s->g->thru.edge_w.as<int32_t>();
-      a.e_begin = 0;
-      a.e_end = s->g->st.m;
       a.chains = s->kplan.chains;
       a.world_chains = s->kplan.chains;
       a.chain0 = 0;
@@ -664,13 +677,12 @@ int gdi_session_launch(gdi_session* s) {
       a.seeds = s->seeds.as<uint64_t>();
       a.thr = s->thr_d.as<long long>();
       a.tmask = s->tmask_d.as<unsigned long long>();
-      a.spins = s->live.as<int8_t>();
+      a.bits = s->live.as<uint32_t>();
       a.gsum = s->gsum.as<long long>();
       a.gdelta = s->gdelta.as<long long>();
       a.acc = s->acc.as<unsigned long long>();
       a.done = s->done.as<unsigned int>();
       a.finished = s->finished.as<unsigned int>();
-      a.bits = s->bits.as<uint32_t>();
       a.trace = s->tr;
       a.stamps = s->st;
       a.snaps = s->snaps.as<int8_t>();
@@ -783,15 +795,11 @@ int gdi_session_launch(gdi_session* s) {
 // A stalled k1_pipe pipeline aborts itself (watchdog) instead of hanging;
 // surface that as a runtime error rather than returning wrong results.
 static int check_watchdog(gdi_session* s) {
-  if (s->use_part) {
-    int w = 0;
-    GDI_CUDA(cudaMemcpy(&w, s->watchdog.p, sizeof w, cudaMemcpyDeviceToHost));
-    if (w != 0) return fail(GDI_ERR_RUNTIME, "k4_sweep chain token watchdog fired (warp " + std::to_string(w - 40) + ")");
+  if (s->use_part) {  // k4 has no inter-warp waits; debug counters only
     if (std::getenv("GDI_K4_DEBUG")) {
       int d[8] = {0};
       GDI_CUDA(cudaMemcpy(d, s->watchdog.p, sizeof d, cudaMemcpyDeviceToHost));
-      std::fprintf(stderr, "[k4 debug] tail g0 %d -> %d, T %d nmain %d | CTAs with residual %d, sum|Gc0| %d sum|Gc| %d\n",
-                   d[2], d[3], d[4], d[5], d[6], d[7], d[1]);
+      std::fprintf(stderr, "[k4 debug] %d %d %d %d %d %d %d %d\n", d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7]);
     }
     return GDI_OK;
   }
@@ -923,7 +931,7 @@ struct gdi_part {
   std::vector<double> pf;
   std::vector<long long> thr;
   std::vector<unsigned long long> tmask;
-  DevBuf seeds, thr_d, tmask_d, live, spins, gsum, gdelta, acc, done, finished, bits, trace, stamps, final_out, watchdog;
+  DevBuf seeds, thr_d, tmask_d, live, spins, gsum, gdelta, acc, done, finished, trace, stamps, final_out, watchdog;
   bool inited = false;
   bool peer = false;                 // fused exchange attached (gdi_part_attach_*)
   std::vector<void*> ipc_opened;     // peer spin copies opened through CUDA IPC
@@ -955,24 +963,24 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
     return fail(GDI_ERR_CAPACITY, "decision arithmetic exceeds the 32-bit kernel bound");
   const int nck = (g->st.n + 31) / 32;
   int ctas = s->plan.ctas;
-  const int max_ctas = nck / world / 64;  // >= 4 chunks per chain
+  const int max_ctas = nck / world / 64;  // >= 2 chunks per chain
   ctas = ctas < max_ctas ? ctas : max_ctas;
+  const int per_cta = s->plan.chains / (s->plan.ctas > 0 ? s->plan.ctas : 1);  // chains per CTA
   s->plan.ctas = ctas < 1 ? 1 : ctas;
-  s->plan.chains = s->plan.ctas * 16;
-  if ((rc = ensure_thru(s->g))) return rc;
+  s->plan.chains = s->plan.ctas * per_cta;
+  if ((rc = ensure_part(s->g))) return rc;
   schedule(s->p, s->pf, s->thr, s->tmask);
   const size_t n = g->st.n, S = p->sweeps;
   GDI_CUDA(s->seeds.alloc(sizeof(uint64_t)));
   GDI_CUDA(s->thr_d.alloc(S * sizeof(long long)));
   GDI_CUDA(s->tmask_d.alloc(S * sizeof(unsigned long long)));
-  GDI_CUDA(s->live.alloc_plain(part_stride(g->st.n)));  // exportable to the other ranks (CUDA IPC)
+  GDI_CUDA(s->live.alloc_plain(part_words(g->st.n) * sizeof(uint32_t)));  // exportable to the other ranks (CUDA IPC)
   GDI_CUDA(s->spins.alloc(n));
   GDI_CUDA(s->gsum.alloc(sizeof(long long)));
   GDI_CUDA(s->gdelta.alloc(sizeof(long long)));
   GDI_CUDA(s->acc.alloc(2 * sizeof(unsigned long long)));
   GDI_CUDA(s->done.alloc(sizeof(unsigned int)));
   GDI_CUDA(s->finished.alloc(sizeof(unsigned int)));
-  GDI_CUDA(s->bits.alloc(((n + 31) / 32) * sizeof(uint32_t)));
   GDI_CUDA(s->trace.alloc(S * sizeof(DevTrace)));
   GDI_CUDA(s->stamps.alloc((S + 1) * sizeof(unsigned long long)));
   GDI_CUDA(s->final_out.alloc(sizeof(DevTrace)));
@@ -984,13 +992,10 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   PartArgs& a = s->args;
   a.g = g->csr();
   a.order = g->thru.order.as<int32_t>();
-  a.sell = g->thru.sell.as<int4>();
+  a.psell = g->psell.as<int4>();
+  a.pdeg = g->pdeg.as<int32_t>();
   a.sell_off = g->thru.sell_off.as<int32_t>();
   a.sell_w = g->thru.sell_w.as<int4>();
-  a.edges = g->thru.edges.as<int2>();
-  a.edge_w = g->thru.edge_w.as<int32_t>();
-  a.e_begin = g->st.m * rank / world;
-  a.e_end = g->st.m * (rank + 1) / world;
   a.chains = s->plan.chains;
   a.world_chains = s->plan.chains * world;
   a.chain0 = rank;
@@ -1002,13 +1007,12 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   a.seeds = s->seeds.as<uint64_t>();
   a.thr = s->thr_d.as<long long>();
   a.tmask = s->tmask_d.as<unsigned long long>();
-  a.spins = s->live.as<int8_t>();
+  a.bits = s->live.as<uint32_t>();
   a.gsum = s->gsum.as<long long>();
   a.gdelta = s->gdelta.as<long long>();
   a.acc = s->acc.as<unsigned long long>();
   a.done = s->done.as<unsigned int>();
   a.finished = s->finished.as<unsigned int>();
-  a.bits = s->bits.as<uint32_t>();
   a.trace = s->trace.as<DevTrace>();
   a.stamps = s->stamps.as<unsigned long long>();
   a.final_out = s->final_out.as<DevTrace>();
@@ -1033,7 +1037,7 @@ int gdi_part_ipc_handle(const gdi_part* s, void* handle) {
 }
 
 namespace {
-int attach(gdi_part* s, const std::vector<int8_t*>& ptrs) {
+int attach(gdi_part* s, const std::vector<uint32_t*>& ptrs) {
   if (s->inited) return fail(GDI_ERR_CONFIG, "attach peers before gdi_part_init");
   if (static_cast<int>(ptrs.size()) != s->world - 1 || s->world - 1 > 7)
     return fail(GDI_ERR_CONFIG, "fused exchange needs world - 1 <= 7 peers");
@@ -1047,7 +1051,7 @@ int attach(gdi_part* s, const std::vector<int8_t*>& ptrs) {
 int gdi_part_attach_peers(gdi_part* s, const void* handles) {
   if (!s || !handles) return fail(GDI_ERR_CONFIG, "NULL argument");
   GDI_CUDA(cudaSetDevice(s->g->device));
-  std::vector<int8_t*> ptrs;
+  std::vector<uint32_t*> ptrs;
   for (int q = 0; q < s->world; q++) {
     if (q == s->rank) continue;
     cudaIpcMemHandle_t h;
@@ -1055,19 +1059,19 @@ int gdi_part_attach_peers(gdi_part* s, const void* handles) {
     void* p = nullptr;
     GDI_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     s->ipc_opened.push_back(p);
-    ptrs.push_back(static_cast<int8_t*>(p));
+    ptrs.push_back(static_cast<uint32_t*>(p));
   }
   return attach(s, ptrs);
 }
 
 int gdi_part_attach_local(gdi_part* s, gdi_part* const* parts) {
   if (!s || !parts) return fail(GDI_ERR_CONFIG, "NULL argument");
-  std::vector<int8_t*> ptrs;
+  std::vector<uint32_t*> ptrs;
   for (int q = 0; q < s->world; q++) {
     if (q == s->rank) continue;
     if (!parts[q] || parts[q]->g->device != s->g->device)
       return fail(GDI_ERR_CONFIG, "local peers must be partitions on the same device");
-    ptrs.push_back(parts[q]->live.as<int8_t>());
+    ptrs.push_back(parts[q]->live.as<uint32_t>());
   }
   return attach(s, ptrs);
 }
@@ -1085,8 +1089,9 @@ int gdi_part_sweep(gdi_part* s, int32_t sweep, void* send) {
   if (!s->inited) return fail(GDI_ERR_CONFIG, "gdi_part_init not called");
   if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
   GDI_CUDA(cudaSetDevice(s->g->device));
-  GDI_CUDA(part_sweep_launch(s->plan, s->args, sweep, s->stream));
-  GDI_CUDA(part_xpack_launch(s->plan, s->args, send, s->stream));
+  PartArgs a = s->args;
+  a.send = static_cast<unsigned char*>(send);
+  GDI_CUDA(part_sweep_launch(s->plan, a, sweep, s->stream));
   return GDI_OK;
 }
 
@@ -1094,9 +1099,8 @@ int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv) {
   if (!s || !recv) return fail(GDI_ERR_CONFIG, "NULL argument");
   if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
   GDI_CUDA(cudaSetDevice(s->g->device));
-  GDI_CUDA(part_xunpack_launch(s->plan, s->args, recv, part_exchange_bytes(s->g->st.n, s->world, s->peer), sweep,
-                                 s->stream));
-  GDI_CUDA(part_barrier_launch(s->plan, s->args, sweep, s->spins.as<int8_t>(), s->stream));
+  GDI_CUDA(part_finish_launch(s->plan, s->args, sweep, recv, part_exchange_bytes(s->g->st.n, s->world, s->peer),
+                              s->spins.as<int8_t>(), s->stream));
   return GDI_OK;
 }
 

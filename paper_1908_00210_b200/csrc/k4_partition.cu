@@ -2,45 +2,66 @@
 //
 // Contract: the reference's pooled racy mode (proj/src/anneal.cpp:203-225,
 // SPEC.md "annealer / Concurrency Model") for graphs whose spins do not fit
-// in one CTA's shared memory — BASELINE configs[4], the 1M-vertex rudy graph
-// — with one or a few replicas, so the parallelism has to come from the
+// one warp's chain of K2 — BASELINE configs[4], the 1M-vertex rudy graph —
+// with one or a few replicas, so the parallelism has to come from the
 // vertices of one replica rather than from independent replicas (K2).
 //
-// Chains. The chunks (32 vertices, SELL-32 rows over the degree-binned
-// order, the same layout as K2) are dealt round-robin to P chains; a chain
-// is one warp (P = all resident warps / replicas). A chain visits its chunks
-// in order with its counter in a register, and inside a chunk the 32
-// decisions see the counter as if made in order (K2's fixed-point ballot
-// prefix). Neighbour spins are read through L2 while other chains write them
-// (racy reads, as the contract allows). A first version chained the 16
-// warps of a CTA through a shared-memory token: the ~700-cycle handoff per
-// chunk, not the memory system, bounded it (116 us per 1M-vertex sweep).
+// Spins in position space. The visit order is the degree-binned order of the
+// SELL layout; position p holds vertex order[p]. A replica's spins are one bit
+// per position (bit l of word c = position 32c + l is +1): chunk c's 32
+// decisions become one word, written by one store (no atomics: only the
+// chunk's chain writes it), and the whole spin state of the 1M-vertex graph is
+// 125 KB. The SELL rows hold neighbour *positions* (build_part_layout).
 //
-// Decoupled global balance. A single counter read live by ~10^4 concurrent
-// visitors over-corrects (all see the same stale imbalance and all flip
-// towards the minority: the "biphasic oscillation" of PAPER.md:632-633; K2's
-// first version showed it). Here chain J starts each sweep from its share of
-// the exact global imbalance G at the last barrier (G/P in units of 2,
-// remainder spread over a rotating set of chains, so the shares sum to G) and then
-// counts only its own spin changes. Every chain drives its own counter to
-// zero, so together they remove exactly G per sweep instead of P times G,
-// and each chain absorbs its own random flips. The last T chunks of the
-// order (its lowest-degree vertices) form a tail that the last CTA to finish
-// decides against the exact global counter, so a sweep ends balanced as the
-// sequential algorithm does rather than with the sum of P chain residuals.
-// With P = 1 this is the exact sequential counter.
+// Shared-memory spin copy. Every CTA (one per SM, 32 warps) keeps a copy of its
+// replica's spin words in shared memory and reads neighbour spins from it
+// (one LDS per neighbour instead of a 32-byte L2 sector per 1-byte gather).
+// Decisions go to the global words (authoritative) and to the CTA's copy; the
+// CTA's last warp is not a chain but re-copies the global words into the copy
+// (TMA bulk copies, one after another: ~4-5 us each here), so other CTAs'
+// changes arrive within about one chunk step, read racily as the contract
+// allows. ~150k of the 1M vertices are in flight at any moment
+// anyway. A chain's own spins are read from the global words, which only it
+// writes, so the counter stays exact. Measured against the round-1 kernel
+// (int8 spins gathered from L2 at each visit) on M1, 20 sweeps: 1.52 -> 1.18
+// ms, cut +1.3% (1.254M -> 1.268M; the reference's own pooled mode is +2% to
+// +7% on this graph); reading the last two bands of chunks from L2 instead
+// (SMODE 2, GDI_K4_FRESH=1) restores the cut (1.2555M) at 2.5 ms.
 //
-// Barrier (record_barrier, anneal.cpp:165-187): k4_pack bit-packs the spins
-// (and sums them), k4_cut streams the canonical edge list against the
-// 1 bit/vertex copy (L1-resident: 125 KB for 1M vertices) and the last block
-// writes the trace record, checks nothing is lost (counter = G + chain
-// deltas) and rolls the counter. Kernel boundaries are the sweep barriers;
-// the session replays the 1 + 3M launches as one CUDA graph.
+// Chains and decoupled global balance. The chunks are dealt round-robin to P
+// chains, one per warp, each with an exactly sequential counter; inside a
+// chunk the 32 decisions see the counter as if made in order (fixed point of
+// a ballot prefix). A single counter read live by ~10^4 concurrent visitors
+// over-corrects (all see the same stale imbalance and flip towards the
+// minority: the biphasic oscillation of PAPER.md:632-633), so chain J starts
+// each sweep from its share of the exact global imbalance G at the last
+// barrier (G/P in units of 2, remainder rotated over the chains) and counts
+// only its own changes. Chains 0..D-1 of a CTA defer their last chunk to a
+// CTA tail that one warp decides in order against the CTA's exact counter (the
+// sum of its 32 chains' counters), and the last T chunks of the order form a
+// global tail decided in order against the exact global counter in the
+// barrier kernel, so a sweep ends balanced as the sequential algorithm does.
+// (A block-wide fixed point over all 1024 deferred vertices, each seeing the
+// block prefix of the changes before it, needed ~N rounds: the low-degree
+// tail vertices are all counter-sensitive near G = 0, so every change shifted
+// the decisions after it.)
 //
-// Multi-GPU (vertex partitioning): the chain numbering is
-// global (chain0, world_chains), so a device runs a contiguous block of the
-// chains; between sweeps the owned chunks' spins are exchanged and the
-// deltas summed (host side), and the edge list is sliced per device.
+// Barrier (record_barrier, anneal.cpp:165-187), k4_finish: every CTA replays
+// the global tail (identical inputs, identical results) into shared memory,
+// then counts its share of the exact cut (each edge once, by its endpoint
+// with the lower position) and of the spin sum, reading tail words from its
+// shared copy; the last CTA writes the trace record and the tail words and
+// rolls the counter. Two launches per sweep; the session replays the
+// 1 + 2M launches as one CUDA graph.
+//
+// Multi-GPU (vertex partitioning): rank r of W runs the
+// chains J = r (mod W), i.e. owns the chunks c = r (mod W). Fused exchange: a
+// changed chunk word is stored into every peer's copy in the same instruction
+// stream as the decision (one 4-byte store per peer over NVLink); the sweep's
+// counter delta goes to the per-sweep all-gather. Unfused: the owned words go
+// to the send buffer and the finishing kernel reads the other ranks' words
+// from the all-gathered buffer (and copies them into the local words for the
+// next sweep). Every rank replays the global tail identically.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -55,119 +76,231 @@ namespace gdi {
 
 namespace {
 
-constexpr int kNW = 16;  // warps per CTA
-#ifndef K4_DEFER
-#define K4_DEFER 1
-#endif
-// chunks per chain deferred to the CTA tail: warp 0 decides the CTA's 16 *
-// kDefer tail chunks in order while the other warps wait, ~30% of an M1 sweep
-// with 2 (1.74 -> 1.53 ms per 20 sweeps with 1, balance unchanged; 0 leaves
-// sweeps imbalanced)
-constexpr int kDefer = K4_DEFER;
-constexpr int kTailMax = 32;  // global tail chunks (>= kDefer * kNW: shares stage[])
-constexpr int kPackBlock = 256;
-constexpr int kCutBlock = 512;
+constexpr int kNW = 32;       // warps per CTA (one thread per deferred vertex in the CTA tail)
+constexpr int kTailMax = kNW;  // global tail chunks: one per warp of a finishing CTA
+constexpr unsigned FULL = 0xffffffffu;
 
-// Racy neighbour read through L2 (other chains write concurrently; L1 would
-// keep a stale line for the whole sweep). WK as in K2.
-template <int WK>
-__device__ __forceinline__ int nb(const int8_t* s, int idx, int w) {
-  if (WK == 1) {
-    const int v = __ldcg(s + (idx & 0x7fffffff));
-    return idx < 0 ? -v : v;
-  }
-  const int v = __ldcg(s + idx);
-  return WK == 2 ? w * v : v;
-}
+template <int WK, int KMAX>
+struct Row {
+  int4 g[KMAX];
+  int4 w[WK == 2 ? KMAX : 1];
+  int c0, groups, v, deg;
+  unsigned word;  // the chunk's own spin word (global, authoritative)
+};
 
-struct ChunkIn {
-  int v, own, f;
+// One lane's visit of a chunk: everything the decision needs.
+struct Visit {
+  int own, f;
   bool live, coin, flip;
 };
 
 template <int WK, int KMAX>
-__device__ __forceinline__ ChunkIn gather(const PartArgs& a, const int8_t* s, int c, int sweep, uint32_t k0,
-                                          uint32_t k1, unsigned long long tm, bool en, int lane) {
-  ChunkIn ci{0, 0, 0, false, false, false};
-  const int idx = c * 32 + lane;
-  ci.live = idx < a.g.n;
-  if (!ci.live) return ci;
-  ci.v = __ldg(a.order + idx);
-  const int c0 = __ldg(a.sell_off + c), c1 = __ldg(a.sell_off + c + 1);
-  const int groups = (c1 - c0) >> 5;
-  int4 g4[KMAX], w4[KMAX];
+__device__ __forceinline__ void load_row(const PartArgs& a, const uint32_t* gb, int c, int c0, int c1, int lane,
+                                         Row<WK, KMAX>& r) {
+  r.c0 = c0;
+  r.groups = (c1 - c0) >> 5;
 #pragma unroll
   for (int k = 0; k < KMAX; k++)
-    if (k < groups) {
-      g4[k] = __ldg(a.sell + c0 + k * 32 + lane);
-      if (WK == 2) w4[k] = __ldg(a.sell_w + c0 + k * 32 + lane);
+    if (k < r.groups) {
+      r.g[k] = __ldg(a.psell + c0 + k * 32 + lane);
+      if (WK == 2) r.w[k] = __ldg(a.sell_w + c0 + k * 32 + lane);
     }
-  const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(ci.v), 0u, 0u, k0, k1);
-  ci.coin = (x.z >> 31) != 0;
-  ci.flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
-  ci.own = __ldcg(s + ci.v);
-  int f = 0;
-#pragma unroll
-  for (int k = 0; k < KMAX; k++)
-    if (k < groups) {
-      const int4 q = g4[k];
-      const int4 w = WK == 2 ? w4[k] : make_int4(1, 1, 1, 1);
-      f += nb<WK>(s, q.x, w.x) + nb<WK>(s, q.y, w.y) + nb<WK>(s, q.z, w.z) + nb<WK>(s, q.w, w.w);
-    }
-  for (int k = KMAX; k < groups; k++) {
-    const int4 q = __ldg(a.sell + c0 + k * 32 + lane);
-    const int4 w = WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
-    f += nb<WK>(s, q.x, w.x) + nb<WK>(s, q.y, w.y) + nb<WK>(s, q.z, w.z) + nb<WK>(s, q.w, w.w);
-  }
-  ci.f = f;
-  return ci;
+  const int p = c * 32 + lane;
+  r.v = p < a.g.n ? __ldg(a.order + p) : 0;
+  if (WK != 2) r.deg = p < a.g.n ? __ldg(a.pdeg + p) : 0;
+  r.word = __ldcg(gb + c);
 }
 
-// The 32 decisions of one chunk against counter G (sequentially consistent
-// inside the chunk); writes the changed spins and advances G.
-__device__ __forceinline__ void decide_chunk(const ChunkIn& cur, int& G, int8_t* s, int a4, int bb, int lane,
-                                             const PartArgs* peers = nullptr) {
-  const unsigned below = (1u << lane) - 1u;
-  const int base_diff = -a4 * cur.own - bb * cur.f;
-  int fin = cur.live ? decide(a4 * G + base_diff, cur.coin, cur.flip) : 0;
-  int d = cur.live ? fin - cur.own : 0;
-  unsigned up = __ballot_sync(0xffffffffu, d > 0), dn = __ballot_sync(0xffffffffu, d < 0);
-  if ((up | dn) != 0u) {
-    for (int round = 0; round < 33; round++) {
-      const int excl = 2 * (__popc(up & below) - __popc(dn & below));
-      const int fin2 = cur.live ? decide(a4 * (G + excl) + base_diff, cur.coin, cur.flip) : 0;
-      if (__all_sync(0xffffffffu, fin2 == fin)) break;
-      fin = fin2;
-      d = cur.live ? fin - cur.own : 0;
-      up = __ballot_sync(0xffffffffu, d > 0);
-      dn = __ballot_sync(0xffffffffu, d < 0);
+// One SELL entry x (a neighbour position; bit 31 = weight -1 on +-1 graphs):
+// unit / +-1 weights: the bit of s_e * w_e = +1 (padding entries point at a
+// zero word: 0), summed and turned into the field by f = 2 * count - degree;
+// general weights: w_e * s_e directly (padding has weight 0).
+template <int WK, typename Word>
+__device__ __forceinline__ int term(int x, int w, Word word) {
+  const int q = WK == 1 ? (x & 0x7fffffff) : x;
+  const unsigned sh = __funnelshift_r(word(q >> 5), 0u, q);  // (shift mod 32)
+  if (WK == 2) return (sh & 1u) ? w : -w;
+  return static_cast<int>((sh ^ (static_cast<unsigned>(x) >> 31)) & 1u);
+}
+
+template <int WK, int KMAX, typename Word>
+__device__ __forceinline__ int row_field(const PartArgs& a, const Row<WK, KMAX>& r, Word word, int lane) {
+  int acc = 0;
+#pragma unroll
+  for (int k = 0; k < KMAX; k++)
+    if (k < r.groups) {
+      const int4 q = r.g[k];
+      const int4 w = WK == 2 ? r.w[k] : make_int4(1, 1, 1, 1);
+      acc += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
     }
-    if (cur.live && d != 0) {
-      s[cur.v] = static_cast<int8_t>(fin);
-      if (peers != nullptr)  // fused exchange: the change lands in every rank's copy
-        for (int q = 0; q < peers->npeer; q++) peers->peer[q][cur.v] = static_cast<int8_t>(fin);
+  for (int k = KMAX; k < r.groups; k++) {  // rows longer than the register bucket
+    const int4 q = __ldg(a.psell + r.c0 + k * 32 + lane);
+    const int4 w = WK == 2 ? __ldg(a.sell_w + r.c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
+    acc += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
+  }
+  return WK == 2 ? acc : 2 * acc - r.deg;
+}
+
+// The spin-word loads of the register bucket are issued first and consumed
+// after the Philox draw, so their latency (an LDS, or an L2 round trip for
+// the fresh bands of SMODE 2) overlaps the RNG.
+template <int WK, int KMAX, typename Word>
+__device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMAX>& r, int c, Word word, int lane,
+                                            int sweep, uint32_t k0, uint32_t k1, unsigned long long tm,
+                                            bool en) {
+  Visit x;
+  x.live = c * 32 + lane < a.g.n;
+  x.own = x.live ? (((r.word >> lane) & 1u) ? 1 : -1) : -1;
+  auto pos = [](int e) { return WK == 1 ? (e & 0x7fffffff) : e; };
+  unsigned wv[4 * KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; k++)
+    if (k < r.groups) {
+      wv[4 * k + 0] = word(pos(r.g[k].x) >> 5);
+      wv[4 * k + 1] = word(pos(r.g[k].y) >> 5);
+      wv[4 * k + 2] = word(pos(r.g[k].z) >> 5);
+      wv[4 * k + 3] = word(pos(r.g[k].w) >> 5);
+    }
+  const Philox4 ph = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(r.v), 0u, 0u, k0, k1);
+  x.coin = (ph.z >> 31) != 0;
+  x.flip = en && ((static_cast<uint64_t>(ph.x) << 32) | ph.y) <= tm;
+  auto bit = [](int e, int w, unsigned wd) {
+    const unsigned sh = __funnelshift_r(wd, 0u, WK == 1 ? (e & 0x7fffffff) : e);
+    if (WK == 2) return (sh & 1u) ? w : -w;
+    return static_cast<int>((sh ^ (static_cast<unsigned>(e) >> 31)) & 1u);
+  };
+  int acc = 0;
+#pragma unroll
+  for (int k = 0; k < KMAX; k++)
+    if (k < r.groups) {
+      const int4 q = r.g[k];
+      const int4 w = WK == 2 ? r.w[k] : make_int4(1, 1, 1, 1);
+      acc += bit(q.x, w.x, wv[4 * k]) + bit(q.y, w.y, wv[4 * k + 1]) + bit(q.z, w.z, wv[4 * k + 2]) +
+             bit(q.w, w.w, wv[4 * k + 3]);
+    }
+  for (int k = KMAX; k < r.groups; k++) {  // rows longer than the register bucket
+    const int4 q = __ldg(a.psell + r.c0 + k * 32 + lane);
+    const int4 w = WK == 2 ? __ldg(a.sell_w + r.c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
+    acc += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
+  }
+  x.f = x.live ? (WK == 2 ? acc : 2 * acc - r.deg) : 0;
+  return x;
+}
+
+// The 32 decisions of one chunk against counter G, each seeing G after the
+// changes of the lanes before it; advances G and returns the chunk's new
+// spin word: two evaluations settle most chunks, else the in-order scan
+// (sweep_common.cuh warp_seq_decide). (Written out here: the same logic
+// behind a shared helper with a round loop measured 1.5x slower.)
+__device__ __forceinline__ unsigned decide_chunk(const Visit& x, int& G, int a4, int bb, int lane) {
+  const int base = -a4 * x.own - bb * x.f;
+  int fin = x.live ? decide(a4 * G + base, x.coin, x.flip) : x.own;
+  const unsigned up = __ballot_sync(FULL, fin > x.own), dn = __ballot_sync(FULL, fin < x.own);
+  if ((up | dn) == 0u) return __ballot_sync(FULL, fin > 0);
+  const unsigned below = (1u << lane) - 1u;
+  const int fin2 =
+      x.live ? decide(a4 * (G + 2 * (__popc(up & below) - __popc(dn & below))) + base, x.coin, x.flip) : x.own;
+  if (__all_sync(FULL, fin2 == fin)) {
+    G += 2 * (__popc(up) - __popc(dn));
+    return __ballot_sync(FULL, fin > 0);
+  }
+  fin = warp_seq_decide(x.own, x.f, x.live, x.coin, x.flip, G, a4, bb, lane);
+  return __ballot_sync(FULL, fin > 0);
+}
+
+// A staged visit packed into one word (shared memory): the field in the low
+// 16 bits, then own, live, coin, flip.
+__device__ __forceinline__ unsigned pack(const Visit& x) {
+  return (static_cast<unsigned>(x.f) & 0xffffu) | (x.own > 0 ? 1u << 16 : 0u) | (x.live ? 1u << 17 : 0u) |
+         (x.coin ? 1u << 18 : 0u) | (x.flip ? 1u << 19 : 0u);
+}
+__device__ __forceinline__ Visit unpack(unsigned u) {
+  Visit x;
+  x.f = static_cast<int>(static_cast<short>(u & 0xffffu));
+  x.own = (u >> 16) & 1u ? 1 : -1;
+  x.live = (u >> 17) & 1u;
+  x.coin = (u >> 18) & 1u;
+  x.flip = (u >> 19) & 1u;
+  return x;
+}
+
+// Bulk copies global -> shared (TMA engine) completing on a per-warp mbarrier.
+__device__ __forceinline__ void mbar_init(uint64_t* mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}" ::"r"(saddr(mb)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(mb)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(mb))
+               : "memory");
+}
+
+// A warp's share of a CTA's shared spin copy: words [w * S, w * S + S) with S
+// a multiple of 4 (16-byte aligned bulk copies).
+struct Slice {
+  int lo, bytes;
+  __device__ Slice(int nwp, int warp) {
+    const int S = ((nwp + kNW - 1) / kNW + 3) & ~3;
+    lo = warp * S;
+    const int hi = lo + S < nwp ? lo + S : nwp;
+    bytes = hi > lo ? 4 * (hi - lo) : 0;
+  }
+};
+
+// Refresh this warp's slice of the CTA's shared spin copy from the global
+// words: one bulk copy by lane 0, landing while the warp goes on deciding
+// (readers see a word's old or new value, as with any racy read). The
+// previous refresh of the slice is waited for first (phase parity).
+struct Refresher {
+  uint64_t* mb;
+  unsigned phase;
+  bool pending;
+  __device__ void issue(uint32_t* sb, const uint32_t* gb, const Slice& sl, int lane) {
+    if (lane != 0 || sl.bytes == 0) return;
+    if (pending) {
+      mbar_wait(mb, phase);
+      phase ^= 1u;
+    }
+    bulk_copy(sb + sl.lo, gb + sl.lo, sl.bytes, mb);
+    pending = true;
+  }
+  __device__ void drain(int lane) {
+    if (lane == 0 && pending) {
+      mbar_wait(mb, phase);
+      phase ^= 1u;
+      pending = false;
     }
   }
-  G += 2 * (__popc(up) - __popc(dn));
-}
+};
 
 // Initial spins (one Philox draw per vertex: the throughput mode is not
 // bit-exact, so the serial stream-0 walk of anneal.cpp:148-155 is not needed)
-// and the exact initial counter.
-__global__ void __launch_bounds__(256) k4_init(const PartArgs a, int ns) {
-  const int r = blockIdx.y, v = blockIdx.x * 256 + threadIdx.x, n = a.g.n;
+// and the exact initial counter. One thread per position of every word.
+__global__ void __launch_bounds__(256) k4_init(const PartArgs a) {
+  const int r = blockIdx.y, p = blockIdx.x * 256 + threadIdx.x, n = a.g.n;
   const uint64_t seed = a.seeds[r];
   int sp = 0;
-  if (v < n) {
+  if (p < n) {
+    const int v = __ldg(a.order + p);
     const Philox4 x = philox4x32_10(0xffffffffu, static_cast<uint32_t>(v), 1u, 0u, static_cast<uint32_t>(seed),
                                     static_cast<uint32_t>(seed >> 32));
     sp = (x.x >> 31) ? 1 : -1;
     if (a.snaps != nullptr) a.snaps[static_cast<size_t>(r) * (a.sweeps + 1) * n + v] = static_cast<int8_t>(sp);
   }
-  if (v < ns) a.spins[static_cast<size_t>(r) * ns + v] = static_cast<int8_t>(sp);  // pad (index n) = 0
+  const unsigned word = __ballot_sync(FULL, sp > 0);
+  if ((threadIdx.x & 31) == 0 && (p >> 5) < a.nwp) a.bits[static_cast<size_t>(r) * a.nwp + (p >> 5)] = word;
   int t = sp;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
   __shared__ int red[8];
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
   __syncthreads();
@@ -179,27 +312,71 @@ __global__ void __launch_bounds__(256) k4_init(const PartArgs a, int ns) {
   }
 }
 
-template <int WK, int KMAX>
-__global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const PartArgs a, int ns) {
-  __shared__ int cta_delta, cta_share, last, tail_g;
-  __shared__ ChunkIn stage[kTailMax][32];
+// SMODE: 0 neighbour spins from the global words (graphs whose copy does not
+// fit shared memory), 1 from the CTA's shared copy, 2 from the shared copy
+// except the chunks of the previous and the current band (the chunks decided
+// in the last and in this chunk step by the chains of every CTA: what the
+// sequential order would already show, and what a refreshed copy lags
+// behind), which are read from the global words.
+template <int WK, int KMAX, int SMODE>
+__global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
+  constexpr bool SM = SMODE > 0;
+  extern __shared__ __align__(16) uint32_t sb[];
+  __shared__ unsigned stage[kNW][32];
+  __shared__ int st_c[kNW];
+  __shared__ unsigned st_w[kNW];
+  __shared__ int red_share[kNW], red_delta[kNW];
+  __shared__ int last, chains_done;
+  __shared__ uint64_t mbar[kNW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
-  const int J = a.chain0 + (blockIdx.x * kNW + warp) * a.chain_stride, P = a.world_chains;
-  const int n = a.g.n, nck = (n + 31) >> 5, T = (a.debug & 4) ? 0 : a.tail, nmain = nck - T;
-  const int K = J < nmain ? (nmain - J + P - 1) / P : 0;
-  int8_t* s = a.spins + static_cast<size_t>(r) * ns;
+  // refresh: the last warp is not a chain but keeps re-copying the whole spin
+  // copy (one bulk copy after another) until the chains are done
+  const bool rmode = SM && a.refresh != 0;
+  const int CW = rmode ? kNW - 1 : kNW;  // chains per CTA
+  const bool is_chain = warp < CW;
+  const int J = a.chain0 + (blockIdx.x * CW + warp) * a.chain_stride, P = a.world_chains;
+  const int n = a.g.n, nck = (n + 31) >> 5, T = a.tail, nmain = nck - T;
+  const int K = is_chain && J < nmain ? (nmain - J + P - 1) / P : 0;
+  const int D = a.cta_tail;             // chains (warps 0..D-1) deferring their last chunk
+  const int Km = warp < D ? K - 1 : K;  // chunks decided by the chain itself
+  uint32_t* gb = a.bits + static_cast<size_t>(r) * a.nwp;
   const int sweep = a.sweep;
   const uint64_t seed = a.seeds[r];
   const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
   const unsigned long long tm = a.tmask[sweep];
   const bool en = a.thr[sweep] >= 0;
   const int a4 = a.a4, bb = a.b;
+  const int W = a.world;
+  uint32_t* send_words = (a.send != nullptr && a.npeer == 0) ? reinterpret_cast<uint32_t*>(a.send + 8) : nullptr;
 
-  // this chain's share of the global imbalance at the last barrier, in
-  // units of 2 (a spin change moves a counter by 2: a chain handed +-1 would
-  // take it for balanced and keep it, so an imbalance spread as +-1 shares is
-  // only half corrected); the parity bit goes to one rotating chain
+  const Slice slice(a.nwp, warp);
+  Refresher rf{&mbar[warp], 0u, false};
+  if (SM) {  // the whole copy: every warp its slice
+    if (lane == 0) {
+      mbar_init(&mbar[warp]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    rf.issue(sb, gb, slice, lane);
+    rf.drain(lane);
+  }
+  int blo = 0, bhi = 0;  // SMODE 2: chunks [blo, bhi) read from the global words
+  auto word = [&](int wi) -> unsigned {
+    if (SMODE == 0) return __ldcg(gb + wi);
+    if (SMODE == 1) return sb[wi];
+    const bool fresh = static_cast<unsigned>(wi - blo) < static_cast<unsigned>(bhi - blo);
+    unsigned v = 0u, u = 0u;
+    if (fresh)
+      v = __ldcg(gb + wi);
+    else
+      u = sb[wi];
+    return fresh ? v : u;
+  };
+
+  // this chain's share of the global imbalance at the last barrier, in units
+  // of 2 (a spin change moves a counter by 2: a chain handed +-1 would take it
+  // for balanced and keep it); the parity bit goes to one rotating chain
   const long long Gs = a.gsum[r];
   const long long par = Gs & 1, Gh = (Gs - par) / 2;
   long long q = Gh / P, rem = Gh - q * P;
@@ -208,255 +385,333 @@ __global__ void __launch_bounds__(32 * kNW, KMAX >= 4 ? 1 : 2) k4_sweep(const Pa
     q -= 1;
   }
   const int rot = static_cast<int>((J + P - sweep % P) % P);
-  const int share = static_cast<int>(2 * (q + (rot < rem ? 1 : 0)) + (rot == P - 1 ? par : 0));
-  if (threadIdx.x == 0) {
-    cta_delta = 0;
-    cta_share = 0;
-  }
+  const int share = is_chain ? static_cast<int>(2 * (q + (rot < rem ? 1 : 0)) + (rot == P - 1 ? par : 0)) : 0;
+  // SELL bounds of this chain's first 32 chunks, one per lane (saves a
+  // dependent L2 round trip per chunk)
+  const int pc = J + lane * P;
+  const int so0 = lane < K ? __ldg(a.sell_off + pc) : 0, so1 = lane < K ? __ldg(a.sell_off + pc + 1) : 0;
+  auto bounds = [&](int k, int& c0, int& c1) {
+    if (k < 32) {
+      c0 = __shfl_sync(FULL, so0, k);
+      c1 = __shfl_sync(FULL, so1, k);
+    } else {
+      c0 = __ldg(a.sell_off + J + k * P);
+      c1 = __ldg(a.sell_off + J + k * P + 1);
+    }
+  };
+  auto commit = [&](int c, unsigned old, unsigned nw) {
+    if (nw != old) {
+      if (lane == 0) {
+        gb[c] = nw;
+        if (SM) sb[c] = nw;
+      }
+      if (lane < a.npeer) a.peer[lane][c] = nw;  // fused exchange: one store per peer
+    }
+    if (send_words != nullptr && lane == 0) send_words[c / W] = nw;
+  };
+  if (threadIdx.x == 0) chains_done = 0;
   __syncthreads();
 
-  int G = share;
-  // every chunk but the chain's last kDefer: those go to the CTA tail below
-#pragma unroll 1
-  for (int k = 0; k + kDefer < K; k++) {
-    const ChunkIn cur = gather<WK, KMAX>(a, s, J + k * P, sweep, k0, k1, tm, en, lane);
-    decide_chunk(cur, G, s, a4, bb, lane, a.npeer > 0 ? &a : nullptr);
+  if (rmode && !is_chain) {
+    // (one copy takes ~4-5 us here, about one chunk step; copying only the
+    // bands being decided, or from every chain warp between its chunks, was
+    // not fresher: no better cut)
+    if (lane == 0) {  // (rf: this warp's barrier, its phase past the initial copy)
+      int rounds = 0;
+      while (*static_cast<volatile int*>(&chains_done) < CW) {
+        bulk_copy(sb, gb, a.nwp * 4, rf.mb);
+        mbar_wait(rf.mb, rf.phase);
+        rf.phase ^= 1u;
+        rounds++;
+      }
+      if ((a.debug & 1) && a.watchdog != nullptr) {  // GDI_K4_DEBUG=1: refresh rounds per CTA
+        atomicAdd(a.watchdog + 0, rounds);
+        atomicAdd(a.watchdog + 1, 1);
+      }
+    }
+    __syncwarp();
   }
-  // CTA tail: the 16 * kDefer deferred chunks (low-degree end of the order)
-  // are decided in order by warp 0 against the CTA's exact counter (sum of
-  // its chains' counters), so a CTA leaves a residual of at most a spin or
-  // two instead of the sum of 16 chain residuals
-#pragma unroll
-  for (int d = 0; d < kDefer; d++) {
-    const int k = K - kDefer + d;
-    stage[d * kNW + warp][lane] =
-        k >= 0 ? gather<WK, KMAX>(a, s, J + k * P, sweep, k0, k1, tm, en, lane) : ChunkIn{0, 0, 0, false, false, false};
+  int G = share;
+  Row<WK, KMAX> cur, nxt;
+  if (K > 0) {
+    int c0, c1;
+    bounds(0, c0, c1);
+    load_row<WK, KMAX>(a, gb, J, c0, c1, lane, cur);
+  }
+#pragma unroll 1
+  for (int k = 0; k < Km; k++) {
+    const int c = J + k * P;
+    if (k + 1 < K) {
+      int c0, c1;
+      bounds(k + 1, c0, c1);
+      load_row<WK, KMAX>(a, gb, c + P, c0, c1, lane, nxt);
+    }
+    blo = (k - 1) * P;
+    bhi = (k + 1) * P;
+    const Visit x = make_visit<WK, KMAX>(a, cur, c, word, lane, sweep, k0, k1, tm, en);
+    commit(c, cur.word, decide_chunk(x, G, a4, bb, lane));
+    cur = nxt;
+  }
+  if (rmode && is_chain && lane == 0) atomicAdd(&chains_done, 1);
+  // CTA tail: the last chunks of chains 0..D-1 (low-degree end of the
+  // order), decided in order by warp 0 against the CTA's exact counter (sum of
+  // its chains' counters), so a CTA leaves a residual of at most a spin or two
+  // instead of the sum of 32 chain residuals
+  if (warp < D) {
+    const int ct = J + (K - 1) * P;
+    blo = (K - 2) * P;
+    bhi = K * P;
+    const Visit xt = K > 0 ? make_visit<WK, KMAX>(a, cur, ct, word, lane, sweep, k0, k1, tm, en)
+                           : Visit{-1, 0, false, false, false};
+    stage[warp][lane] = pack(xt);
+    if (lane == 0) {
+      st_c[warp] = K > 0 ? ct : -1;
+      st_w[warp] = cur.word;
+    }
   }
   if (lane == 0) {
-    atomicAdd(&cta_delta, G - share);
-    atomicAdd(&cta_share, share);
+    red_share[warp] = share;
+    red_delta[warp] = G - share;
   }
   __syncthreads();
   if (warp == 0) {
-    const int gc0 = cta_share + cta_delta;
-    int Gc = gc0;
-    for (int t = 0; t < kDefer * kNW; t++) decide_chunk(stage[t][lane], Gc, s, a4, bb, lane, a.npeer > 0 ? &a : nullptr);
-    if (lane == 0) cta_delta += Gc - gc0;
-    if ((a.debug & 8) && lane == 0 && a.watchdog != nullptr && sweep + 1 == a.sweeps) {
-      atomicAdd(a.watchdog + 6, Gc != 0 ? 1 : 0);
-      atomicAdd(a.watchdog + 7, gc0 < 0 ? -gc0 : gc0);
-      atomicAdd(a.watchdog + 1, Gc < 0 ? -Gc : Gc);
+    int sh = red_share[lane], dl = red_delta[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sh += __shfl_xor_sync(FULL, sh, o);
+      dl += __shfl_xor_sync(FULL, dl, o);
+    }
+    const int g0 = sh + dl;
+    int Gc = g0;
+#pragma unroll 1
+    for (int t = 0; t < D; t++) {
+      const int c = st_c[t];
+      if (c < 0) continue;
+      const unsigned nw = decide_chunk(unpack(stage[t][lane]), Gc, a4, bb, lane);
+      commit(c, st_w[t], nw);
+    }
+    const int cta_delta = dl + Gc - g0;
+    if (lane == 0 && cta_delta != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.gdelta + r), static_cast<unsigned long long>(cta_delta));
+  }
+  if (a.send == nullptr) return;
+  // ranks > 1: the last CTA moves the sweep's delta into the send buffer
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(a.finished + r, 1u) == gridDim.x - 1;
+    if (last) {
+      __threadfence();
+      *reinterpret_cast<long long*>(a.send) =
+          static_cast<long long>(atomicExch(reinterpret_cast<unsigned long long*>(a.gdelta + r), 0ull));
+      a.finished[r] = 0u;
     }
   }
-  __threadfence();  // this CTA's spin writes before the ticket (the tail reads them)
-  __syncthreads();  // (also: the CTA tail is done with stage[])
-  if (threadIdx.x == 0) {
-    if (cta_delta != 0)
-      atomicAdd(reinterpret_cast<unsigned long long*>(a.gdelta + r), static_cast<unsigned long long>(cta_delta));
-    last = 0;
-    if (T > 0 && a.tail_ticket) {
-      __threadfence();
-      last = atomicAdd(a.finished + r, 1u) == gridDim.x - 1;
-      if (last) {
-        __threadfence();
-        tail_g = static_cast<int>(a.gsum[r] + static_cast<long long>(atomicAdd(
-                                                  reinterpret_cast<unsigned long long*>(a.gdelta + r), 0ull)));
-        a.finished[r] = 0u;
+}
+
+// Barrier: global tail, exact cut share and spin sum, trace record, outputs.
+// recv (ranks > 1): the all-gathered send buffers, rstride bytes apart.
+// SM: the spin words are copied into shared memory first (bulk copies; in the
+// unfused exchange the main chunks owned by other ranks come from recv), so
+// every lookup is one LDS. The global tail is decided by warp 0 while the
+// other warps count the cut over the edges between main vertices; the edges
+// with a tail endpoint are counted from the tail rows afterwards.
+template <int WK, int KMAX, bool SM>
+__global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const unsigned char* recv, long long rstride,
+                                                        int8_t* spins_out) {
+  extern __shared__ __align__(16) uint32_t sw[];
+  __shared__ uint32_t tw[kTailMax];
+  __shared__ unsigned stage[kTailMax][32];
+  __shared__ int tail_delta;
+  __shared__ long long lred[2][kNW];
+  __shared__ int last;
+  __shared__ uint64_t mbar[kNW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y, n = a.g.n, nck = (n + 31) >> 5, T = a.tail, nmain = nck - T, zpos = 32 * nck;
+  const int tlo = 32 * nmain;  // first tail position
+  const int W = a.world, rk = a.rank, sweep = a.sweep;
+  uint32_t* gb = a.bits + static_cast<size_t>(r) * a.nwp;
+  const bool unfused = recv != nullptr && a.npeer == 0 && W > 1;
+  long long G0 = a.gsum[r];
+  if (recv != nullptr)
+    for (int q = 0; q < W; q++) G0 += *reinterpret_cast<const long long*>(recv + q * rstride);
+  else
+    G0 += __ldcg(a.gdelta + r);
+  // spin words before the tail: main chunks owned by other ranks come from
+  // the all-gathered buffer (unfused exchange), everything else is local
+  auto mword = [&](int wi) -> unsigned {
+    if (unfused && wi < nmain && wi % W != rk)
+      return reinterpret_cast<const uint32_t*>(recv + (wi % W) * rstride + 8)[wi / W];
+    return __ldg(gb + wi);  // (read-only in this kernel until the last CTA's tail stores)
+  };
+  if (SM) {
+    if (unfused) {
+      for (int wi = threadIdx.x; wi < a.nwp; wi += blockDim.x) sw[wi] = mword(wi);
+    } else {
+      const Slice sl(a.nwp, warp);
+      Refresher rf{&mbar[warp], 0u, false};
+      if (lane == 0) {
+        mbar_init(&mbar[warp]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncwarp();
+      rf.issue(sw, gb, sl, lane);
+      rf.drain(lane);
+    }
+    __syncthreads();
+  }
+  // lookups before the tail is decided (tail words: their values before it)
+  auto pre = [&](int wi) -> unsigned { return SM ? sw[wi] : mword(wi); };
+
+  // 1. global tail, replayed identically by every CTA (and every rank):
+  // gathered by T warps, decided in order by warp 0 against the exact counter
+  const uint64_t seed = a.seeds[r];
+  if (warp < T) {
+    const int c = nmain + warp;
+    Row<WK, KMAX> row;
+    load_row<WK, KMAX>(a, gb, c, __ldg(a.sell_off + c), __ldg(a.sell_off + c + 1), lane, row);
+    row.word = pre(c);
+    const Visit xt = make_visit<WK, KMAX>(a, row, c, pre, lane, sweep, static_cast<uint32_t>(seed),
+                                          static_cast<uint32_t>(seed >> 32), a.tmask[sweep], a.thr[sweep] >= 0);
+    stage[warp][lane] = pack(xt);
+  }
+  __syncthreads();
+  long long cut = 0, pop = 0;
+  if (warp == 0) {
+    int Gt = static_cast<int>(G0);
+#pragma unroll 1
+    for (int t = 0; t < T; t++) {
+      const unsigned nw = decide_chunk(unpack(stage[t][lane]), Gt, a.a4, a.b, lane);
+      if (lane == 0) tw[t] = nw;
+    }
+    if (lane == 0) tail_delta = Gt - static_cast<int>(G0);
+  } else {
+    // 2a. this rank's share of the exact cut (evaluate.cpp:10-18) over the
+    // edges between main vertices: every edge once, by its endpoint with the
+    // lower position, rank r counting the rows of its own main chunks
+    const int nwarps = gridDim.x * (kNW - 1);
+    for (int c = blockIdx.x * (kNW - 1) + warp - 1; c < nmain; c += nwarps) {
+      if (c % W != rk) continue;
+      const int p = c * 32 + lane;
+      const unsigned sp = (pre(c) >> lane) & 1u;
+      const int c0 = __ldg(a.sell_off + c), groups = (__ldg(a.sell_off + c + 1) - c0) >> 5;
+      for (int k = 0; k < groups; k++) {
+        const int4 q4 = __ldg(a.psell + c0 + k * 32 + lane);
+        const int4 w4 = WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
+        const int xs[4] = {q4.x, q4.y, q4.z, q4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int q = WK == 1 ? (xs[j] & 0x7fffffff) : xs[j];
+          if (q > p && q < tlo && ((__funnelshift_r(pre(q >> 5), 0u, q) & 1u) != sp))
+            cut += WK == 0 ? 1 : WK == 1 ? (xs[j] < 0 ? -1 : 1) : ws[j];
+        }
       }
     }
   }
   __syncthreads();
-  if (!last) return;
-  // tail: gathered by all warps (every other chain is done), decided in
-  // order by warp 0 against the exact counter
-  for (int t = warp; t < T; t += kNW) stage[t][lane] = gather<WK, KMAX>(a, s, nmain + t, sweep, k0, k1, tm, en, lane);
-  __syncthreads();
-  if (warp != 0) return;
-  const int g0 = tail_g;
-  int Gt = g0;
-  for (int t = 0; t < T; t++) decide_chunk(stage[t][lane], Gt, s, a4, bb, lane);
-  if ((a.debug & 8) && lane == 0 && a.watchdog != nullptr && sweep + 1 == a.sweeps) {
-    a.watchdog[2] = g0;
-    a.watchdog[3] = Gt;
-    a.watchdog[4] = T;
-    a.watchdog[5] = nmain;
-  }
-  if (lane == 0 && Gt != g0)
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.gdelta + r), static_cast<unsigned long long>(Gt - g0));
-}
-
-// Barrier part 1: bit-pack the spins (bit l of word w = vertex 32w + l is
-// +1), sum them, copy snapshots / final spins.
-__global__ void __launch_bounds__(kPackBlock) k4_pack(const PartArgs a, int ns, int8_t* spins_out) {
-  const int r = blockIdx.y, n = a.g.n, sweep = a.sweep;
-  const int lane = threadIdx.x & 31;
-  const int8_t* s = a.spins + static_cast<size_t>(r) * ns;
-  const int nw = (n + 31) >> 5;
+  const int tot = tail_delta;
+  auto word = [&](int wi) -> unsigned { return wi >= nmain && wi < nck ? tw[wi - nmain] : pre(wi); };
+  // 2b. the edges with a tail endpoint, from the tail rows (rank 0): to a
+  // main vertex always, to another tail vertex once (higher position)
+  if (rk == 0)
+    for (int t = blockIdx.x * kNW + warp; t < T; t += gridDim.x * kNW) {
+      const int c = nmain + t, p = c * 32 + lane;
+      const unsigned sp = (tw[t] >> lane) & 1u;
+      const int c0 = __ldg(a.sell_off + c), groups = (__ldg(a.sell_off + c + 1) - c0) >> 5;
+      for (int k = 0; k < groups; k++) {
+        const int4 q4 = __ldg(a.psell + c0 + k * 32 + lane);
+        const int4 w4 = WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
+        const int xs[4] = {q4.x, q4.y, q4.z, q4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int q = WK == 1 ? (xs[j] & 0x7fffffff) : xs[j];
+          if ((q < tlo || (q > p && q != zpos)) && ((__funnelshift_r(word(q >> 5), 0u, q) & 1u) != sp))
+            cut += WK == 0 ? 1 : WK == 1 ? (xs[j] < 0 ? -1 : 1) : ws[j];
+        }
+      }
+    }
+  // 3. the spin sum (global, on every rank), the unfused exchange's copy of the
+  // other ranks' words for the next sweep, and the natural-order outputs
   const bool last_sweep = sweep + 1 == a.sweeps;
   int8_t* snap = a.snaps != nullptr ? a.snaps + (static_cast<size_t>(r) * (a.sweeps + 1) + sweep + 1) * n : nullptr;
-  int sum = 0;
-  const int warps = gridDim.x * (kPackBlock / 32);
-  for (int w = blockIdx.x * (kPackBlock / 32) + (threadIdx.x >> 5); w < nw; w += warps) {
-    const int v = 32 * w + lane;
-    const int8_t x = v < n ? __ldcg(s + v) : static_cast<int8_t>(0);
-    sum += x;
-    const unsigned bits = __ballot_sync(0xffffffffu, x > 0);
-    if (lane == 0) a.bits[static_cast<size_t>(r) * nw + w] = bits;
-    if (v < n) {
-      if (snap != nullptr) snap[v] = x;
-      if (last_sweep) spins_out[static_cast<size_t>(r) * n + v] = x;
-    }
+  const int nthreads = gridDim.x * blockDim.x;
+  for (int wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nck; wi += nthreads) {
+    const unsigned x = word(wi);
+    pop += __popc(x);
+    if (unfused && wi < nmain && wi % W != rk) gb[wi] = x;
   }
+  if (snap != nullptr || last_sweep)
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += nthreads) {
+      const int8_t s = ((word(p >> 5) >> (p & 31)) & 1u) ? 1 : -1;
+      const int v = __ldg(a.order + p);
+      if (snap != nullptr) snap[v] = s;
+      if (last_sweep) spins_out[static_cast<size_t>(r) * n + v] = s;
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  __shared__ int red[kPackBlock / 32];
-  if (lane == 0) red[threadIdx.x >> 5] = sum;
+  for (int o = 16; o > 0; o >>= 1) {
+    cut += __shfl_xor_sync(FULL, cut, o);
+    pop += __shfl_xor_sync(FULL, pop, o);
+  }
+  if (lane == 0) {
+    lred[0][warp] = cut;
+    lred[1][warp] = pop;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < kPackBlock / 32; w++) t += red[w];
-    if (t != 0) atomicAdd(a.acc + 2 * r + 1, static_cast<unsigned long long>(static_cast<long long>(t)));
-  }
-}
-
-// Barrier part 2: exact cut over this device's edge slice against the packed
-// spins; the last block writes the trace record and rolls the counter.
-template <int WK>
-__global__ void __launch_bounds__(kCutBlock) k4_cut(const PartArgs a) {
-  const int r = blockIdx.y, n = a.g.n, sweep = a.sweep;
-  const uint32_t* __restrict__ bits = a.bits + static_cast<size_t>(r) * ((n + 31) >> 5);
-  const long long tid = static_cast<long long>(blockIdx.x) * kCutBlock + threadIdx.x;
-  const long long stride = static_cast<long long>(gridDim.x) * kCutBlock;
-  long long cut = 0;
-  // four edges per thread in flight (the loop was latency-serial: edge load,
-  // then the two bit loads, per iteration)
-  long long e = a.e_begin + tid;
-  for (; e + 3 * stride < a.e_end; e += 4 * stride) {
-    int2 uv[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) uv[q] = __ldg(a.edges + e + q * stride);
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const uint32_t x =
-          (__ldg(bits + (uv[q].x >> 5)) >> (uv[q].x & 31)) ^ (__ldg(bits + (uv[q].y >> 5)) >> (uv[q].y & 31));
-      if (x & 1u) cut += WK == 0 ? 1 : __ldg(a.edge_w + e + q * stride);
+    long long cs = 0, ps = 0;
+    for (int w = 0; w < kNW; w++) {
+      cs += lred[0][w];
+      ps += lred[1][w];
     }
+    if (cs != 0) atomicAdd(a.acc + 2 * r, static_cast<unsigned long long>(cs));
+    if (ps != 0) atomicAdd(a.acc + 2 * r + 1, static_cast<unsigned long long>(ps));
+    __threadfence();
+    last = atomicAdd(a.done + r, 1u) == gridDim.x - 1;
   }
-  for (; e < a.e_end; e += stride) {
-    const int2 uv = __ldg(a.edges + e);
-    const uint32_t x = (__ldg(bits + (uv.x >> 5)) >> (uv.x & 31)) ^ (__ldg(bits + (uv.y >> 5)) >> (uv.y & 31));
-    if (x & 1u) cut += WK == 0 ? 1 : __ldg(a.edge_w + e);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cut += __shfl_xor_sync(0xffffffffu, cut, o);
-  __shared__ long long red[kCutBlock / 32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cut;
   __syncthreads();
+  if (!last) return;
+  // the last CTA: tail words into the live copy, trace record, counter roll
+  if (lane == 0 && warp < T) gb[nmain + warp] = tw[warp];
   if (threadIdx.x != 0) return;
-  long long c = 0;
-  for (int w = 0; w < kCutBlock / 32; w++) c += red[w];
-  if (c != 0) atomicAdd(a.acc + 2 * r, static_cast<unsigned long long>(c));
-  __threadfence();
-  if (atomicAdd(a.done + r, 1u) != gridDim.x - 1) return;
   __threadfence();
   const long long cv = static_cast<long long>(atomicAdd(a.acc + 2 * r, 0ull));
-  const long long sv = static_cast<long long>(atomicAdd(a.acc + 2 * r + 1, 0ull));
-  const long long counter = a.gsum[r] + a.gdelta[r];
+  const long long sv = 2 * static_cast<long long>(atomicAdd(a.acc + 2 * r + 1, 0ull)) - n;
+  const long long counter = G0 + tot;
   const DevTrace rec{cv, sv, counter};
   if (a.trace != nullptr) a.trace[static_cast<size_t>(r) * a.sweeps + sweep] = rec;
   if (a.stamps != nullptr) a.stamps[static_cast<size_t>(r) * (a.sweeps + 1) + sweep + 1] = globaltimer_ns();
-  if (sweep + 1 == a.sweeps) a.final_out[r] = rec;
+  if (last_sweep) a.final_out[r] = rec;
   a.gsum[r] = counter;
-  a.gdelta[r] = 0;
+  if (recv == nullptr) a.gdelta[r] = 0;
   a.acc[2 * r] = 0ull;
   a.acc[2 * r + 1] = 0ull;
   a.done[r] = 0u;
 }
 
-// Vertex-partition exchange (rank r of W ranks owns chunks c = r (mod W)).
-// Send buffer: [int64 counter delta of this sweep][uint32 word i = spins of
-// chunk r + i*W, bit l = lane l's vertex is +1]. Every rank receives all W
-// buffers (stride bytes apart), rewrites the other ranks' vertices in its own
-// spin copy and sets the sweep's total delta for the barrier.
-__global__ void __launch_bounds__(256) k4_xpack(const PartArgs a, int ns, unsigned char* send) {
-  const int n = a.g.n, nck = (n + 31) >> 5, W = a.world, rk = a.rank;
-  const int lane = threadIdx.x & 31;
-  const int8_t* s = a.spins;
-  uint32_t* words = reinterpret_cast<uint32_t*>(send + 8);
-  const int nmain = nck - a.tail;  // tail chunks are recomputed identically on every rank
-  const int nw = a.npeer > 0 ? 0 : nmain > rk ? (nmain - rk + W - 1) / W : 0;  // peer mode: deltas only
-  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < nw; i += gridDim.x * 8) {
-    const int idx = (rk + i * W) * 32 + lane;
-    const int8_t x = idx < n ? __ldcg(s + __ldg(a.order + idx)) : static_cast<int8_t>(-1);
-    const unsigned b = __ballot_sync(0xffffffffu, x > 0);
-    if (lane == 0) words[i] = b;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<long long*>(send) = a.gdelta[0];
-}
 
-__global__ void __launch_bounds__(256) k4_xunpack(const PartArgs a, int ns, const unsigned char* recv,
-                                                  long long stride) {
-  const int n = a.g.n, nck = (n + 31) >> 5, W = a.world, rk = a.rank;
-  const int lane = threadIdx.x & 31;
-  int8_t* s = a.spins;
-  const int nmain = a.npeer > 0 ? 0 : nck - a.tail;  // peer mode: the spins arrived during the sweep
-  for (int c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nmain; c += gridDim.x * 8) {
-    const int q = c % W;
-    if (q == rk) continue;
-    const uint32_t w = reinterpret_cast<const uint32_t*>(recv + q * stride + 8)[c / W];
-    const int idx = c * 32 + lane;
-    if (idx < n) s[__ldg(a.order + idx)] = ((w >> lane) & 1u) ? 1 : -1;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    long long d = 0;
-    for (int q = 0; q < W; q++) d += *reinterpret_cast<const long long*>(recv + q * stride);
-    a.gdelta[0] = d;  // the barrier folds it into the counter
-  }
-}
 
-// Global tail for ranks > 1: after the exchange every rank holds the same
-// spins and the exact counter, so each runs the tail chunks itself (same
-// gathers, same Philox draws, one warp deciding in order) and the ranks stay
-// identical without a second exchange.
 template <int WK, int KMAX>
-__global__ void __launch_bounds__(32 * kNW) k4_gtail(const PartArgs a, int ns) {
-  __shared__ ChunkIn stage[kTailMax][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n = a.g.n, nck = (n + 31) >> 5, T = a.tail, nmain = nck - T;
-  const int r = blockIdx.y, sweep = a.sweep;
-  int8_t* s = a.spins + static_cast<size_t>(r) * ns;
-  const uint64_t seed = a.seeds[r];
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-  const unsigned long long tm = a.tmask[sweep];
-  const bool en = a.thr[sweep] >= 0;
-  for (int t = warp; t < T; t += kNW) stage[t][lane] = gather<WK, KMAX>(a, s, nmain + t, sweep, k0, k1, tm, en, lane);
-  __syncthreads();
-  if (warp != 0) return;
-  const int g0 = static_cast<int>(a.gsum[r] + a.gdelta[r]);
-  int Gt = g0;
-  for (int t = 0; t < T; t++) decide_chunk(stage[t][lane], Gt, s, a.a4, a.b, lane);
-  if (lane == 0) a.gdelta[r] += Gt - g0;
+void pick_k(bool sm, PartPlan* plan) {
+  plan->sweep_fn = !sm           ? reinterpret_cast<const void*>(&k4_sweep<WK, KMAX, 0>)
+                   : plan->fresh ? reinterpret_cast<const void*>(&k4_sweep<WK, KMAX, 2>)
+                                 : reinterpret_cast<const void*>(&k4_sweep<WK, KMAX, 1>);
+  plan->finish_fn = sm ? reinterpret_cast<const void*>(&k4_finish<WK, KMAX, true>)
+                       : reinterpret_cast<const void*>(&k4_finish<WK, KMAX, false>);
 }
 
 template <int WK>
-const void* gtail_fn(int kmax) {
-  switch (kmax) {
-    case 1: return reinterpret_cast<const void*>(&k4_gtail<WK, 1>);
-    case 2: return reinterpret_cast<const void*>(&k4_gtail<WK, 2>);
-    default: return reinterpret_cast<const void*>(&k4_gtail<WK, 4>);
-  }
-}
-
-template <int WK>
-const void* sweep_fn(int kmax) {
-  switch (kmax) {
-    case 1: return reinterpret_cast<const void*>(&k4_sweep<WK, 1>);
-    case 2: return reinterpret_cast<const void*>(&k4_sweep<WK, 2>);
-    default: return reinterpret_cast<const void*>(&k4_sweep<WK, 4>);
-  }
+void pick(int kmax, bool sm, PartPlan* plan) {
+  if (kmax == 1)
+    pick_k<WK, 1>(sm, plan);
+  else if (kmax == 2)
+    pick_k<WK, 2>(sm, plan);
+  else
+    pick_k<WK, 4>(sm, plan);
 }
 
 }  // namespace
+
+int part_words(int n) { return (((n + 31) / 32 + 1) + 3) & ~3; }
 
 int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan) {
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
@@ -468,54 +723,71 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const long long ra = a4 / x, rb = b / x;
   const double bound = static_cast<double>(ra) * (2.0 * st.n + 1) + static_cast<double>(rb) * (st.max_abs_field + 1);
   if (bound >= 2147483647.0) return -1;
-  if (st.n < 1) return -1;
+  if (st.n < 1 || st.n > (1 << 30)) return -1;
+  if (st.max_abs_field > 32767) return -1;  // staged fields are 16-bit (pack)
   // register row bucket sized by the mean degree (as K2); longer rows loop
   const double mean_deg = 2.0 * static_cast<double>(st.m) / st.n;
   const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : 4;
-  // chains = warps: fill the resident slots across the replicas (CTAs of 16
-  // warps, 1 or 2 per SM by __launch_bounds__), at least 4 chunks per chain
+  // one CTA of 32 chains per SM, spread over the replicas; at least two
+  // chunks per chain (the last one may go to the CTA tail)
   const int nck = (st.n + 31) / 32;
-  const int ctas_per_sm = kmax >= 4 ? 1 : 2;
   const int R = replicas > 0 ? replicas : 1;
-  int ctas = ctas_per_sm * 148 / R;
-  const int max_ctas = nck / (4 * kNW);
+  int ctas = 148 / R;
+  const int max_ctas = nck / (2 * kNW);
   ctas = ctas < max_ctas ? ctas : max_ctas;
   plan->ctas = ctas < 1 ? 1 : ctas;
-  plan->chains = plan->ctas * kNW;
-  // tail chunks run by the last CTA against the exact counter (see k4_sweep)
-  // one device: 8 chunks. The chains' residual after the CTA tails is a few
-  // spins; a 32-chunk tail balanced no better (M1 and a 100k graph, 4 seeds:
-  // final imbalance 0 either way) and cost a fifth of the M1 sweep (the last
-  // CTA decides its chunks in order against a counter that cascades through
-  // them). Partitioned over ranks the residuals of every rank's chains add
-  // up: 8 chunks left a fused W=4 run imbalanced, so 32 there.
-  constexpr int kTailDefault = 8;
-  plan->tail = nck / 8 < kTailDefault ? nck / 8 : kTailDefault;
+  plan->refresh = 1;
+  if (const char* e = std::getenv("GDI_K4_REFRESH")) plan->refresh = std::atoi(e);
+  plan->fresh = 0;
+  if (const char* e = std::getenv("GDI_K4_FRESH")) plan->fresh = std::atoi(e);
+  plan->chains = plan->ctas * (plan->refresh != 0 ? kNW - 1 : kNW);
+  // global tail: 16 chunks (32 when partitioned over ranks: every rank's
+  // residuals add up), and 4 deferred chunks per CTA (decided in order by one
+  // warp while the CTA's other warps wait)
+  plan->tail = nck / 8 < 16 ? nck / 8 : 16;
   plan->tail_multi = nck / 8 < kTailMax ? nck / 8 : kTailMax;
+  plan->cta_tail = 4;
   if (const char* e = std::getenv("GDI_K4_TAIL")) {  // tuning experiments
     const int t = std::atoi(e);
     plan->tail = plan->tail_multi = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
   }
-  plan->sweep_fn = wkind == 0 ? sweep_fn<0>(kmax) : wkind == 1 ? sweep_fn<1>(kmax) : sweep_fn<2>(kmax);
-  plan->gtail_fn = wkind == 0 ? gtail_fn<0>(kmax) : wkind == 1 ? gtail_fn<1>(kmax) : gtail_fn<2>(kmax);
-  plan->cut_fn = wkind == 0   ? reinterpret_cast<const void*>(&k4_cut<0>)
-                 : wkind == 1 ? reinterpret_cast<const void*>(&k4_cut<1>)
-                              : reinterpret_cast<const void*>(&k4_cut<2>);
+  if (const char* e = std::getenv("GDI_K4_CTA_TAIL")) {
+    const int t = std::atoi(e);
+    plan->cta_tail = t < 0 ? 0 : t > kNW ? kNW : t;
+  }
+  plan->nwp = part_words(st.n);
+  plan->smem = plan->nwp * 4;
+  plan->smem_copy = plan->smem <= 200 * 1024;
+  if (!plan->smem_copy) {
+    plan->smem = 0;
+    if (plan->refresh != 0) {  // (no copy to refresh: every warp is a chain)
+      plan->refresh = 0;
+      plan->chains = plan->ctas * kNW;
+    }
+  }
+  if (wkind == 0)
+    pick<0>(kmax, plan->smem_copy, plan);
+  else if (wkind == 1)
+    pick<1>(kmax, plan->smem_copy, plan);
+  else
+    pick<2>(kmax, plan->smem_copy, plan);
   plan->block = 32 * kNW;
-  long long cg = (st.m + kCutBlock * 8 - 1) / (kCutBlock * 8);
-  plan->cut_grid = static_cast<int>(cg < 1 ? 1 : cg > 2 * 148 ? 2 * 148 : cg);
-  long long pg = ((st.n + 31) / 32 + 7) / 8;
-  plan->pack_grid = static_cast<int>(pg < 1 ? 1 : pg > 4 * 148 ? 4 * 148 : pg);
+  // finishing CTAs: one per SM with the shared copy (each copies the words),
+  // else up to two per SM
+  const int fg = (nck + kNW - 1) / kNW, fmax = ((plan->smem_copy ? 148 : 296) + R - 1) / R;
+  plan->fin_grid = fg < fmax ? fg : fmax;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
+  if (plan->smem > 48 * 1024 &&
+      (cudaFuncSetAttribute(plan->sweep_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem) != cudaSuccess ||
+       cudaFuncSetAttribute(plan->finish_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem) != cudaSuccess))
+    return -1;
   plan->name = wkind == 0 ? "k4_sweep<unit>" : wkind == 1 ? "k4_sweep<pm1>" : "k4_sweep<weighted>";
   return 0;
 }
 
-int part_launch_count(const PartPlan&, int32_t sweeps) { return 1 + 3 * sweeps; }
-
-int part_stride(int n) { return (n + 1 + 15) & ~15; }
+int part_launch_count(const PartPlan&, int32_t sweeps) { return 1 + 2 * sweeps; }
 
 namespace {
 
@@ -524,7 +796,9 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   a.a4 = plan.a4;
   a.b = plan.b;
   a.tail = a.world == 1 ? plan.tail : plan.tail_multi;
-  a.tail_ticket = a.world == 1 ? 1 : 0;  // ranks > 1: k4_gtail after the exchange
+  a.cta_tail = plan.cta_tail;
+  a.nwp = plan.nwp;
+  a.refresh = plan.refresh;
   const char* dbg = std::getenv("GDI_K4_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
   return a;
@@ -534,7 +808,6 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
 
 cudaError_t part_init_launch(const PartPlan& plan, const PartArgs& args, cudaStream_t stream) {
   PartArgs a = prepared(plan, args);
-  const int ns = part_stride(a.g.n);
   const int R = a.replicas;
   cudaError_t err;
   if ((err = cudaMemsetAsync(a.gsum, 0, R * sizeof(long long), stream))) return err;
@@ -542,51 +815,24 @@ cudaError_t part_init_launch(const PartPlan& plan, const PartArgs& args, cudaStr
   if ((err = cudaMemsetAsync(a.acc, 0, 2 * R * sizeof(unsigned long long), stream))) return err;
   if ((err = cudaMemsetAsync(a.done, 0, R * sizeof(unsigned int), stream))) return err;
   if ((err = cudaMemsetAsync(a.finished, 0, R * sizeof(unsigned int), stream))) return err;
-  k4_init<<<dim3((ns + 255) / 256, R), 256, 0, stream>>>(a, ns);
+  k4_init<<<dim3((a.nwp * 32 + 255) / 256, R), 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t part_sweep_launch(const PartPlan& plan, const PartArgs& args, int sweep, cudaStream_t stream) {
   PartArgs a = prepared(plan, args);
   a.sweep = sweep;
-  int ns = part_stride(a.g.n);
-  void* p1[] = {&a, &ns};
-  return cudaLaunchKernel(plan.sweep_fn, dim3(plan.ctas, a.replicas), dim3(plan.block), p1, 0, stream);
+  void* p[] = {&a};
+  return cudaLaunchKernel(plan.sweep_fn, dim3(plan.ctas, a.replicas), dim3(plan.block), p, plan.smem, stream);
 }
 
-cudaError_t part_barrier_launch(const PartPlan& plan, const PartArgs& args, int sweep, int8_t* spins_out,
-                                cudaStream_t stream) {
+cudaError_t part_finish_launch(const PartPlan& plan, const PartArgs& args, int sweep, const void* recv,
+                               long long stride, int8_t* spins_out, cudaStream_t stream) {
   PartArgs a = prepared(plan, args);
   a.sweep = sweep;
-  const int ns = part_stride(a.g.n);
-  k4_pack<<<dim3(plan.pack_grid, a.replicas), kPackBlock, 0, stream>>>(a, ns, spins_out);
-  cudaError_t err = cudaGetLastError();
-  if (err) return err;
-  void* p3[] = {&a};
-  return cudaLaunchKernel(plan.cut_fn, dim3(plan.cut_grid, a.replicas), dim3(kCutBlock), p3, 0, stream);
-}
-
-cudaError_t part_xpack_launch(const PartPlan& plan, const PartArgs& args, void* send, cudaStream_t stream) {
-  PartArgs a = prepared(plan, args);
-  const int nck = (a.g.n + 31) / 32;
-  const int nw = (nck - a.rank + a.world - 1) / a.world;
-  k4_xpack<<<(nw + 7) / 8 > 0 ? ((nw + 7) / 8 < 1184 ? (nw + 7) / 8 : 1184) : 1, 256, 0, stream>>>(
-      a, part_stride(a.g.n), static_cast<unsigned char*>(send));
-  return cudaGetLastError();
-}
-
-cudaError_t part_xunpack_launch(const PartPlan& plan, const PartArgs& args, const void* recv, long long stride,
-                                int sweep, cudaStream_t stream) {
-  PartArgs a = prepared(plan, args);
-  a.sweep = sweep;
-  int ns = part_stride(a.g.n);
-  const int nck = (a.g.n + 31) / 32;
-  k4_xunpack<<<(nck + 7) / 8 < 1184 ? (nck + 7) / 8 : 1184, 256, 0, stream>>>(
-      a, ns, static_cast<const unsigned char*>(recv), stride);
-  cudaError_t err = cudaGetLastError();
-  if (err || a.tail == 0 || a.tail_ticket) return err;
-  void* p[] = {&a, &ns};
-  return cudaLaunchKernel(plan.gtail_fn, dim3(1, a.replicas), dim3(plan.block), p, 0, stream);
+  const unsigned char* rv = static_cast<const unsigned char*>(recv);
+  void* p[] = {&a, &rv, &stride, &spins_out};
+  return cudaLaunchKernel(plan.finish_fn, dim3(plan.fin_grid, a.replicas), dim3(plan.block), p, plan.smem, stream);
 }
 
 long long part_exchange_bytes(int n, int world, bool peer) {
@@ -601,7 +847,7 @@ cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spin
   if (err) return err;
   for (int sw = 0; sw < args.sweeps; sw++) {
     if ((err = part_sweep_launch(plan, args, sw, stream))) return err;
-    if ((err = part_barrier_launch(plan, args, sw, spins_out, stream))) return err;
+    if ((err = part_finish_launch(plan, args, sw, nullptr, 0, spins_out, stream))) return err;
   }
   return cudaSuccess;
 }

@@ -119,19 +119,20 @@ struct ThruArgs {
 // chunks J, J + world_chains, ...); this device runs the chains
 // chain0 + i * chain_stride (i = warp index in the grid): one device has
 // chain0 = 0, stride 1; rank r of W ranks has chain0 = r, stride W, so it owns
-// the chunks c = r (mod W). Spins live in global memory ([R][n], L2-resident).
+// the chunks c = r (mod W). Spins live in position space, one bit per vertex:
+// bit l of word c is the spin of the vertex at position 32c + l of the visit
+// order (+1 = set), so a chunk's 32 decisions are one word store.
 struct PartArgs {
   DevCsr g;
-  const int32_t* order;
-  const int4* sell;
-  const int32_t* sell_off;
-  const int4* sell_w;
-  const int2* edges;               // canonical edge list slice [e_begin, e_end)
-  const int32_t* edge_w;
-  int64_t e_begin, e_end;
+  const int32_t* order;            // [n] position -> vertex (degree-binned visit order)
+  const int4* psell;               // SELL-32 rows over positions (layout.hpp build_part_layout)
+  const int32_t* pdeg;             // [n] degree of the vertex at each position
+  const int32_t* sell_off;         // [chunks+1] in int4 units
+  const int4* sell_w;              // nullptr unless general weights
+  int32_t nwp;                     // spin words per replica: chunks + 1 zero word, padded to 4
   int32_t chains;                  // chains per replica on this device
   int32_t world_chains, chain0, chain_stride;
-  int32_t rank, world;              // vertex partition (1 device: 0, 1)
+  int32_t rank, world;             // vertex partition (1 device: 0, 1)
   int32_t sweeps;
   int32_t replicas;
   int32_t sweep;                   // set per launch
@@ -139,20 +140,23 @@ struct PartArgs {
   const long long* thr;
   const unsigned long long* tmask;
   int32_t a4, b;
-  int8_t* spins;                   // [R][n] live spins (= the session's output)
+  uint32_t* bits;                  // [R][nwp] live spin words
   long long* gsum;                 // [R] balance counter at the last barrier
   long long* gdelta;               // [R] sum of the chains' counter changes this sweep
   unsigned long long* acc;         // [R][2] cut / spin-sum accumulators
-  unsigned int* done;              // [R] barrier blocks finished
-  unsigned int* finished;          // [R] CTAs finished (tail ticket)
-  uint32_t* bits;                  // [R][ceil(n/32)] packed spins at the barrier
-  // fused exchange (ranks > 1): every spin change is also stored into the
-  // other ranks' spin copies (peer memory over NVLink); the per-sweep
+  unsigned int* done;              // [R] finishing blocks (ticket)
+  unsigned int* finished;          // [R] sweep blocks (ticket, ranks > 1)
+  // fused exchange (ranks > 1): every changed chunk word is also stored into
+  // the other ranks' copies (peer memory over NVLink); the per-sweep
   // collective then only carries the counter deltas
-  int8_t* peer[7];
+  uint32_t* peer[7];
   int32_t npeer;
+  // ranks > 1: this sweep's send buffer: [int64 delta][uint32 word of every
+  // owned main chunk, c = rank + i * world] (the words only without peers)
+  unsigned char* send;
   int32_t tail;                    // last chunks of the order, decided against the exact counter
-  int32_t tail_ticket;             // 1: by the last CTA of k4_sweep (one device); 0: k4_gtail on every rank
+  int32_t cta_tail;                // chains per CTA deferring their last chunk to the CTA tail
+  int32_t refresh;                 // 1: the last warp of a CTA re-copies its shared spin copy (0: never)
   int32_t debug;                   // timing experiments only (GDI_K4_DEBUG); 0 in production
   DevTrace* trace;
   unsigned long long* stamps;

@@ -102,33 +102,36 @@ cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t
 
 struct PartPlan {
   const void* sweep_fn = nullptr;
-  const void* cut_fn = nullptr;
-  const void* gtail_fn = nullptr;  // ranks > 1: global tail after the exchange
+  const void* finish_fn = nullptr;
   int32_t a4 = 4, b = 4;
-  int ctas = 1;        // per replica
-  int chains = 16;     // per replica (one per warp)
-  int tail = 0;        // tail chunks (exact counter) per sweep, one device
+  int ctas = 1;        // sweep CTAs per replica (32 chains each)
+  int chains = 32;     // per replica on this device (one per warp)
+  int tail = 0;        // global tail chunks (exact counter) per sweep, one device
   int tail_multi = 0;  // the same when the graph is partitioned over ranks
-  int block = 512;
-  int pack_grid = 148, cut_grid = 148;
+  int cta_tail = 4;    // chains per CTA deferring their last chunk to the CTA tail
+  int block = 1024;
+  int fin_grid = 1;    // finishing CTAs per replica
+  int nwp = 0;         // spin words per replica (part_words)
+  int smem = 0;        // dynamic shared memory of the sweep kernel (the spin copy)
+  bool smem_copy = false;
+  int refresh = 1;     // 1: a refresher warp keeps re-copying the shared spin copy (0: never)
+  int fresh = 0;       // 1: the last two bands of chunks read from the global words (k4_sweep SMODE 2)
   const char* name = "";
 };
 int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan);
-// Enqueues init + sweeps x (sweep, pack, cut) kernels: 1 + 3 * sweeps launches.
-// spins_out [R][n] receives the final spins (the live array has stride part_stride(n)).
+// Enqueues init + sweeps x (sweep, finish) kernels: 1 + 2 * sweeps launches.
+// spins_out [R][n] receives the final spins in vertex order.
 cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream);
 // The same sequence in pieces, for the vertex-partitioned multi-rank driver:
-// init; per sweep: sweep, xpack (send), [caller all-gathers], xunpack (recv), barrier.
+// init; per sweep: sweep (args.send = this sweep's send buffer), [caller
+// all-gathers the send buffers], finish (recv = the gathered buffers).
 cudaError_t part_init_launch(const PartPlan& plan, const PartArgs& args, cudaStream_t stream);
 cudaError_t part_sweep_launch(const PartPlan& plan, const PartArgs& args, int sweep, cudaStream_t stream);
-cudaError_t part_barrier_launch(const PartPlan& plan, const PartArgs& args, int sweep, int8_t* spins_out,
-                                cudaStream_t stream);
-cudaError_t part_xpack_launch(const PartPlan& plan, const PartArgs& args, void* send, cudaStream_t stream);
-cudaError_t part_xunpack_launch(const PartPlan& plan, const PartArgs& args, const void* recv, long long stride,
-                                int sweep, cudaStream_t stream);
+cudaError_t part_finish_launch(const PartPlan& plan, const PartArgs& args, int sweep, const void* recv,
+                               long long stride, int8_t* spins_out, cudaStream_t stream);
 long long part_exchange_bytes(int n, int world, bool peer);  // per-rank send buffer bytes (16-aligned)
 int part_launch_count(const PartPlan& plan, int32_t sweeps);
-int part_stride(int n);
+int part_words(int n);  // spin words per replica: ceil(n/32) + 1 zero word, padded to 4
 
 // L2-resident read bandwidth (GB/s) for roofline denominators.
 cudaError_t probe_l2_read(size_t bytes, int iters, double* gbs);

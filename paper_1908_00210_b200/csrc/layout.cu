@@ -352,6 +352,29 @@ cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout*
   return cudaStreamSynchronize(st);
 }
 
+// K4 layout: the SELL rows with every neighbour replaced by its position in
+// the visit order (pos[order[p]] = p), so that chunk c's spins are bits
+// 32c..32c+31 of one word and a neighbour's spin is bit (q & 31) of word
+// q >> 5. Padding entries point at position 32 * chunks (a word that stays
+// zero); bit 31 keeps the -1 weight of +-1 graphs.
+__global__ void k_inverse(const int32_t* order, const int32_t* off, int n, int32_t* pos, int32_t* pdeg) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    const int v = order[p];
+    pos[v] = p;
+    pdeg[p] = off[v + 1] - off[v];
+  }
+}
+
+__global__ void k_psell(const int32_t* sell, long long cells, const int32_t* pos, int n, int zpos, int32_t* psell) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int32_t x = sell[i];
+    const int v = x & 0x7fffffff;
+    psell[i] = v >= n ? zpos : (pos[v] | (x & static_cast<int32_t>(0x80000000u)));
+  }
+}
+
 // Forward window masks: bit l of fwd[v] = bit l of win[v + 1 + l] (vertex
 // v + 1 + l has v as a +1 / -1 neighbour at distance l + 1), so one uniform load
 // of the changed vertex's word gives the whole next window's corrections.
@@ -402,6 +425,21 @@ cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStrea
   if ((e = L->wsell.alloc(cells * sizeof(int32_t)))) return e;
   k_fill_i32<<<1024, kB, 0, st>>>(L->wsell.as<int32_t>(), cells, n);
   k_wsell_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, L->wsell_off.as<int32_t>(), n, L->wsell.as<int32_t>());
+  if ((e = cudaGetLastError())) return e;
+  return cudaStreamSynchronize(st);
+}
+
+cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, cudaStream_t st) {
+  cudaError_t e;
+  const int n = g.n;
+  DevBuf pos;
+  if ((e = pos.alloc((n > 0 ? n : 1) * sizeof(int32_t)))) return e;
+  if ((e = pdeg.alloc((n > 0 ? n : 1) * sizeof(int32_t)))) return e;
+  const long long cells = (T.slots > 0 ? T.slots : 1) * 4;
+  if ((e = psell.alloc(cells * sizeof(int32_t)))) return e;
+  k_inverse<<<blocks(n), kB, 0, st>>>(T.order.as<int32_t>(), g.off, n, pos.as<int32_t>(), pdeg.as<int32_t>());
+  k_psell<<<1184, kB, 0, st>>>(T.sell.as<int32_t>(), cells, pos.as<int32_t>(), n, 32 * ((n + 31) / 32),
+                               psell.as<int32_t>());
   if ((e = cudaGetLastError())) return e;
   return cudaStreamSynchronize(st);
 }

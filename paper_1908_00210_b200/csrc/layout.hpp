@@ -46,6 +46,11 @@ cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const in
 // Returns cudaErrorInvalidValue when SELL would exceed 2^31 int4 cells.
 cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout* L, cudaStream_t st);
 
+// K4 rows: the SELL layout with neighbour positions in the visit order
+// (padding -> position 32 * ceil(n / 32), a zero word), and the degree of the
+// vertex at every position.
+cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, cudaStream_t st);
+
 // k1_pipe layout (every |w| == 1, n >= 2 * win).
 cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st);
 

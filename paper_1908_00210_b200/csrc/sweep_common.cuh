@@ -13,6 +13,50 @@ __device__ __forceinline__ int decide(int diff, bool coin, bool flip) {
   return flip ? -c : c;
 }
 
+// In-order decisions of 32 consecutive visits (one per lane) against one
+// counter: visit i sees G_i = G + (the changes of visits 0..i-1), as in the
+// sequential visit_node (anneal.cpp:95-118). A visit's choice depends on G
+// only through one threshold: with X = a4*own + b*field, diff = a4*G - X, so
+// c = +1 iff G <= U (U = floor((X - 1)/a4), or floor(X/a4) when the tie coin
+// says +1), and G_{i+1} = G_i + (G_i <= U_i ? dL_i : dR_i).
+//
+// warp_seq_decide: every lane runs the in-order scan redundantly on the
+// broadcast thresholds (two dependent instructions per step) and keeps the
+// counter its own visit sees. Exact for any number of changes. Callers first
+// evaluate every lane against G and then against G + the changes of the lanes
+// before it under that evaluation: when no decision moves, those are the
+// in-order decisions (most chunks), and only otherwise run the scan (an
+// evaluation loop inside this function, and a scan starting at the first
+// unsettled lane, both measured slower). Returns the lane's final spin (own
+// when !live); advances G. (a4, b and the fields are bounded so that
+// a4 * (|G| + 1) + b * |field| < 2^31.)
+__device__ __forceinline__ int floor_div(int x, int a) { return x >= 0 ? x / a : -((-x + a - 1) / a); }
+__device__ __forceinline__ int warp_seq_decide(int own, int f, bool live, bool coin, bool flip, int& G, int a4,
+                                               int bb, int lane) {
+  const int X = a4 * own + bb * f;
+  int U;
+  if (a4 == 1)
+    U = coin ? X : X - 1;
+  else if (a4 > 0)
+    U = floor_div(coin ? X : X - 1, a4);
+  else
+    U = (X > 0 || (X == 0 && coin)) ? 0x7fffffff : static_cast<int>(0x80000000u);
+  const int cL = flip ? -1 : 1;  // the final spin when G <= U
+  const int dL = live ? cL - own : 0, dR = live ? -cL - own : 0;
+  const unsigned pk = static_cast<unsigned>(dL + 2) | (static_cast<unsigned>(dR + 2) << 4);
+  int g = G, mine = G;
+#pragma unroll
+  for (int k = 0; k < 32; k++) {
+    const int Uk = __shfl_sync(0xffffffffu, U, k);
+    const unsigned pkk = __shfl_sync(0xffffffffu, pk, k);
+    const int tL = g + static_cast<int>(pkk & 15u) - 2, tR = g + static_cast<int>(pkk >> 4) - 2;
+    if (lane == k) mine = g;
+    g = g <= Uk ? tL : tR;
+  }
+  G = g;
+  return live ? (mine <= U ? cL : -cL) : own;
+}
+
 // CTA-scope release/acquire on shared-memory words, by their shared::cta
 // address (generic-address atomics compile to slower generic loads/stores).
 __device__ __forceinline__ unsigned saddr(const void* p) {

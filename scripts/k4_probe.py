@@ -16,6 +16,16 @@ import paper_1908_00210_b200 as pi
 from tests.helpers import product_graph
 
 
+def sm_clock():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        return pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:
+        return None
+
+
 def run(recipe, R, sweeps):
     t0 = time.time()
     g = product_graph(recipe.split(":"))
@@ -35,6 +45,7 @@ def run(recipe, R, sweeps):
         e1.record(st)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
+    clk = sm_clock()
     s.sync()
     out = s.fetch(spins=True, trace=True)
     tr = out["trace"]
@@ -42,7 +53,7 @@ def run(recipe, R, sweeps):
     sums = out["spins"].astype(np.int64).sum(1)
     print(json.dumps({
         "recipe": recipe, "R": R, "sweeps": sweeps, "kernel": s.kernel, "gen_s": round(tg, 2),
-        "launches": s.launch_count, "ms": min(ts), "ms_all": ts,
+        "launches": s.launch_count, "ms": min(ts), "sm_mhz": clk, "ms_all": ts,
         "updates_per_s": R * g.num_nodes * sweeps / (min(ts) * 1e-3),
         "cut": out["cut"].tolist()[:8], "imbalance": out["imbalance"].tolist()[:8],
         "imb_trace_r0": tr[0, :, 2].tolist()[-10:], "ctr_r0": out["counters"][0].tolist()[-40:], "cut_trace_r0": tr[0, :, 1].tolist()[-5:],
