@@ -172,17 +172,24 @@ int gdi_session_destroy(gdi_session* s);
 
 /* Vertex-partitioned anneal of ONE replica across W ranks (one device each;
  * SURVEY.md §8(e), the 1M-vertex config). Throughput mode only. Rank r owns
- * the chunks c = r (mod W) of the degree-binned order and keeps a full spin
- * copy; remote spins are refreshed once per sweep (racy reads, reference
- * SPEC.md concurrency contract). Per sweep the caller runs, on `stream`:
- *   gdi_part_sweep(s, k, send)              sweep kernel + pack owned spins
+ * the chunks c = r (mod W) of the degree-binned order and keeps a full copy
+ * of the spins (one bit per vertex); remote spins are refreshed once per
+ * sweep (racy reads, reference SPEC.md concurrency contract). Per sweep the
+ * caller runs, on `stream`:
+ *   gdi_part_sweep(s, k, send)              sweep kernel: writes this rank's
+ *                                           counter delta and its owned chunk
+ *                                           spin words into `send`
  *   all-gather of the W send buffers        (e.g. ncclAllGather, same stream)
- *   gdi_part_finish(s, k, recv)             unpack, counter, barrier
+ *   gdi_part_finish(s, k, recv)             finishing kernel: global tail,
+ *                                           this rank's cut share, counter,
+ *                                           trace record
  * with send = gdi_part_exchange_bytes() bytes and recv = W times that
- * (rank-major). Trace cuts and the final cut from gdi_part_fetch are this
- * rank's share (edges [r*m/W, (r+1)*m/W) of the canonical list); the sum over
- * ranks is the cut. Imbalance, counters and spins are global on every rank.
- * W == 1 gives the single-device K4 path. */
+ * (rank-major): two kernel launches per sweep, no host work between them (the
+ * sequence can be captured as one CUDA graph with the collectives). Trace cuts
+ * and the final cut from gdi_part_fetch are this rank's share (the edges whose
+ * lower endpoint in the visit order lies in a chunk this rank owns; rank 0
+ * also counts the tail's); the sum over ranks is the cut. Imbalance, counters
+ * and spins are global on every rank. W == 1 gives the single-device K4 path. */
 typedef struct gdi_part gdi_part;
 int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int32_t rank, uint64_t seed,
                     void* stream, gdi_part** out);
@@ -194,9 +201,11 @@ int gdi_part_fetch(gdi_part* s, gdi_outputs* out);
 int gdi_part_destroy(gdi_part* s);
 
 /* Fused exchange (optional, before gdi_part_init): each rank's sweep kernel
- * stores every spin change straight into the other ranks' spin copies (peer
- * memory, NVLink), so remote spins are fresh during the sweep and the
- * per-sweep collective shrinks to the counter deltas (exchange bytes = 16).
+ * stores every changed chunk spin word (32 vertices, 4 bytes) straight into
+ * the other ranks' spin copies (peer memory, NVLink), so remote spins are
+ * fresh during the sweep and the per-sweep collective shrinks to the counter
+ * deltas (exchange bytes = 16). The ranks must not start sweep k+1 before
+ * every rank has finished gdi_part_finish(k) (a barrier collective).
  * gdi_part_ipc_handle exports this rank's spin copy (GDI_IPC_HANDLE_BYTES
  * bytes); gdi_part_attach_peers takes every rank's handle, rank-major (the
  * caller all-gathers them); gdi_part_attach_local wires W partitions of one

@@ -12,9 +12,9 @@
   change is stored by the sweep kernel itself into the other ranks' copies
   through peer memory (NVLink; CUDA IPC handles exchanged once), and the
   per-sweep collective only sums the counter deltas. Unfused: once per sweep,
-  all-gather one packed bit per owned vertex plus the delta (include/gdi.h
-  gdi_part_*). The edge list is split for the barrier cut; partial cuts are
-  summed at the end with one all-reduce.
+  all-gather the spin word of every owned chunk plus the delta (include/gdi.h
+  gdi_part_*). Each rank counts the cut over the rows of its own chunks;
+  partial cuts are summed at the end with one all-reduce.
 
 `emulate_partitioned` runs the W ranks as W sessions in one process on one
 device, the exchange being a device-side concatenation: the ranks' kernels
@@ -127,61 +127,139 @@ def combine(results: Sequence[dict], all_reduce_sum: Callable | None = None) -> 
             "balance_counter": int(r0["balance_counter"]), "seconds": max(r["seconds"] for r in results)}
 
 
-def anneal_partitioned(problem, params, seed: int, dist, device: int, stream=None, fused: bool = True) -> dict:
+class PartitionedAnneal:
+    """One rank's reusable vertex-partitioned anneal (call collectively on every
+    rank; process group initialised, one GPU per rank). The session, the peer
+    mappings (fused: CUDA IPC handles exchanged once) and the exchange buffers
+    are set up here, outside any timed region; run() is one whole anneal
+    (init + all sweeps). Under NCCL the anneal's launch sequence - per sweep the
+    sweep kernel, the all-gather of the send buffers, the finishing kernel and
+    (fused) the barrier all-reduce - is captured once as a CUDA graph and each
+    run() replays it: 2 of our launches + 1-2 collectives per sweep, no host
+    work between them. close() tears the peer mappings down in the order
+    gdi.h gdi_part_detach asks for."""
+
+    def __init__(self, problem, params, seed: int, dist, device: int, stream=None, fused: bool = True,
+                 graph: bool = True):
+        import torch
+
+        import paper_1908_00210_b200 as pi
+
+        self.dist, self.sweeps = dist, params.sweeps
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.dev = torch.device("cuda", device)
+        self.stream = stream or torch.cuda.Stream(self.dev)
+        self.ps = pi.PartSession(problem, params, self.world, self.rank, int(seed), stream=self.stream.cuda_stream,
+                                 device=device)
+        self.fused = fused and self.world > 1
+        if self.fused:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.ps.ipc_handle())
+            self.ps.attach_peers(b"".join(handles))
+        nb = self.ps.exchange_bytes
+        self.nccl = dist.get_backend() == "nccl"
+        self.cdev = self.dev if self.nccl else torch.device("cpu")
+        self.send = torch.zeros(nb, dtype=torch.uint8, device=self.dev)
+        self.recv = torch.zeros(self.world * nb, dtype=torch.uint8, device=self.dev)
+        self.token = torch.zeros(1, dtype=torch.int32, device=self.cdev)
+        self.graph = None
+        self.use_graph = graph and self.nccl
+        self.graph_error = None
+
+    def _exchange(self):
+        import torch
+
+        if self.nccl:
+            self.dist.all_gather_into_tensor(self.recv, self.send)
+        else:  # gloo (multi-rank rehearsal on fewer GPUs): host-staged
+            self.stream.synchronize()
+            out = torch.empty(self.recv.numel(), dtype=torch.uint8)
+            self.dist.all_gather_into_tensor(out, self.send.cpu())
+            self.recv.copy_(out)
+
+    def _barrier(self):  # stream-ordered under NCCL: a device-side barrier, no host round trip
+        if not self.nccl:
+            self.stream.synchronize()
+        self.dist.all_reduce(self.token)
+
+    def _enqueue(self):
+        """The anneal's launch sequence (run_partitioned's order)."""
+        ps = self.ps
+        ps.init()  # writes the whole local copy: peers must not store into it before this
+        if self.fused:
+            self._barrier()
+        sp, rp = self.send.data_ptr(), self.recv.data_ptr()
+        for k in range(self.sweeps):
+            ps.sweep(k, sp)
+            self._exchange()
+            ps.finish(k, rp)
+            if self.fused and k + 1 < self.sweeps:
+                self._barrier()
+
+    def launch(self):
+        """Enqueue one anneal on the stream (graph replay under NCCL)."""
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            if self.use_graph and self.graph is None:
+                try:
+                    self._enqueue()  # warm-up run: NCCL communicators and kernels initialised before capture
+                    self.stream.synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=self.stream):
+                        self._enqueue()
+                    self.graph = g
+                except RuntimeError as e:  # capture unsupported here: stay eager
+                    self.use_graph, self.graph_error = False, str(e)
+                    self.stream.synchronize()
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._enqueue()
+
+    @property
+    def launches_per_anneal(self) -> int:
+        return 1 + 2 * self.sweeps  # init + (sweep, finish) per sweep; collectives not counted
+
+    def result(self) -> dict:
+        import torch
+
+        res = [self.ps.fetch()]
+
+        def all_reduce_sum(a):
+            t = torch.as_tensor(a, device=self.cdev)
+            self.dist.all_reduce(t)
+            return t.cpu().numpy()
+
+        return combine(res, all_reduce_sum)
+
+    def run(self) -> dict:
+        self.launch()
+        return self.result()
+
+    def close(self):
+        if self.fused:
+            # teardown order (gdi.h gdi_part_detach): close the peers' mappings on
+            # every rank, barrier, and only then free the exported copies
+            self.ps.detach()
+            self.dist.barrier()
+        self.graph = None
+        self.ps = None
+
+
+def anneal_partitioned(problem, params, seed: int, dist, device: int, stream=None, fused: bool = True,
+                       graph: bool = True) -> dict:
     """One rank of a W-rank vertex-partitioned anneal (call on every rank;
     process group already initialised, one GPU per rank). fused: spin changes
     go straight into the other ranks' copies over peer memory (CUDA IPC
     handles exchanged once), and the per-sweep collective carries only the
-    counter deltas; otherwise one packed spin all-gather per sweep."""
-    import torch
-
-    import paper_1908_00210_b200 as pi
-
-    world, rank = dist.get_world_size(), dist.get_rank()
-    dev = torch.device("cuda", device)
-    stream = stream or torch.cuda.current_stream(dev)
-    ps = pi.PartSession(problem, params, world, rank, int(seed), stream=stream.cuda_stream, device=device)
-    if fused and world > 1:
-        handles = [None] * world
-        dist.all_gather_object(handles, ps.ipc_handle())
-        ps.attach_peers(b"".join(handles))
-    nb = ps.exchange_bytes
-    cdev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
-    send = torch.zeros(nb, dtype=torch.uint8, device=dev)
-    recv = torch.zeros(world * nb, dtype=torch.uint8, device=dev)
-    def exchange():
-        if cdev.type == "cuda":
-            dist.all_gather_into_tensor(recv, send)
-        else:  # gloo (multi-rank rehearsal on fewer GPUs): host-staged
-            torch.cuda.current_stream(dev).synchronize()
-            out = torch.empty(world * nb, dtype=torch.uint8)
-            dist.all_gather_into_tensor(out, send.cpu())
-            recv.copy_(out)
-
-    token = torch.zeros(1, dtype=torch.int32, device=cdev)
-
-    def barrier():  # stream-ordered under NCCL: a device-side barrier, no host round trip
-        if cdev.type != "cuda":
-            torch.cuda.current_stream(dev).synchronize()
-        dist.all_reduce(token)
-
-    with torch.cuda.stream(stream):
-        res = run_partitioned([ps], params.sweeps, exchange, lambda i: (send.data_ptr(), recv.data_ptr()),
-                              barrier if fused and world > 1 else None)
-
-    def all_reduce_sum(a):
-        t = torch.as_tensor(a, device=cdev)
-        dist.all_reduce(t)
-        return t.cpu().numpy()
-
-    out = combine(res, all_reduce_sum)
-    if fused and world > 1:
-        # teardown order (gdi.h gdi_part_detach): close the peers' mappings on
-        # every rank, barrier, and only then free the exported copies
-        ps.detach()
-        dist.barrier()
-    del ps
-    return out
+    counter deltas; otherwise the owned chunks' spin words are all-gathered
+    every sweep. graph: under NCCL, the anneal is one CUDA graph replay."""
+    pa = PartitionedAnneal(problem, params, seed, dist, device, stream, fused, graph)
+    try:
+        return pa.run()
+    finally:
+        pa.close()
 
 
 def emulate_partitioned(problem, params, seed: int, world: int, device: int = 0, fused: bool = False) -> dict:
