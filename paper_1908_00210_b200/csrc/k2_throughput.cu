@@ -35,6 +35,7 @@
 // spin sum for the trace and the counter-integrity value.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -346,6 +347,266 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
   for (int i = lane; i < n; i += 32) a.spins_out[rs * n + i] = s[i];
 }
 
+// K2 chains: several warps per replica (the racy pooled mode's concurrency
+// inside one replica, anneal.cpp:203-225). A CTA holds RPC replicas x P
+// chains (one warp each); a replica's spins (int8) and exact fields (biased,
+// packed in 32-bit words so a change scatters with word atomics: no carry
+// crosses into a neighbour's lane since |field| <= max degree < bias) live in
+// shared memory with the visit order and (when it fits) the CSR with 16-bit
+// columns. Chain j of a replica visits the j-th of P contiguous blocks of
+// chunks of the degree-binned order against its own counter, started from its share of the
+// replica's exact imbalance (decoupled balance, as K4); after a per-replica
+// barrier, chain 0 decides the last T chunks (lowest degrees) in order
+// against the exact counter, so sweeps end balanced. A visit reads own spin
+// and field (racy against the other chains' concurrent scatters, as the
+// contract allows); the 32 decisions of a chunk see the counter in lane order
+// (two evaluations, else the exact threshold scan). The exact cut at the
+// barrier comes from the exact fields: sum_u s_u f_u = 2 sum_e w_e s_u s_v, so
+// cut = (W - sum_u s_u f_u / 2) / 2 (evaluate.cpp:10-18), an O(n) reduction.
+template <int FB>
+__device__ __forceinline__ int fget(const unsigned char* fld, int v) {
+  if (FB == 1) return static_cast<int>(fld[v]) - 128;
+  if (FB == 2) return static_cast<int>(reinterpret_cast<const uint16_t*>(fld)[v]) - 32768;
+  return reinterpret_cast<const int*>(fld)[v];
+}
+template <int FB>
+__device__ __forceinline__ void fset(unsigned char* fld, int v, int f) {
+  if (FB == 1)
+    fld[v] = static_cast<unsigned char>(f + 128);
+  else if (FB == 2)
+    reinterpret_cast<uint16_t*>(fld)[v] = static_cast<uint16_t>(f + 32768);
+  else
+    reinterpret_cast<int*>(fld)[v] = f;
+}
+template <int FB>
+__device__ __forceinline__ void fadd(unsigned char* fld, int v, int d) {
+  unsigned* w = reinterpret_cast<unsigned*>(fld);
+  if (FB == 1)
+    atomicAdd(w + (v >> 2), static_cast<unsigned>(d) << ((v & 3) * 8));
+  else if (FB == 2)
+    atomicAdd(w + (v >> 1), static_cast<unsigned>(d) << ((v & 1) * 16));
+  else
+    atomicAdd(reinterpret_cast<int*>(fld) + v, d);
+}
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int WK, int FB, bool CS>
+__global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const ChainCfg cf) {
+  extern __shared__ __align__(16) unsigned char csm[];
+  __shared__ int red_d[32], rep_G[16];
+  __shared__ long long red_sf[32], red_s[32];
+  __shared__ long long Wtot;
+  const int n = a.g.n, P = cf.chains, T = cf.tail;
+  const int nck = (n + 31) >> 5, nmain = nck - T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = warp / P, j = warp - slot * P;
+  const int r = blockIdx.x * cf.rpc + slot;
+  const unsigned FULL = 0xffffffffu;
+  int32_t* order = reinterpret_cast<int32_t*>(csm + cf.off_order);
+  int32_t* offs = reinterpret_cast<int32_t*>(csm + cf.off_offs);
+  uint16_t* cols = reinterpret_cast<uint16_t*>(csm + cf.off_cols);
+
+  // ---- prologue (whole CTA): visit order, CSR, total edge weight W
+  long long wpart = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = __ldg(a.order + i);
+  if (CS) {
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) offs[i] = __ldg(a.g.off + i);
+    const int nnz = __ldg(a.g.off + n);
+    for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+      const int c = __ldg(a.g.col + e);
+      const bool neg = WK == 1 && __ldg(a.g.w + e) < 0;
+      cols[e] = static_cast<uint16_t>(neg ? (c | 0x8000) : c);
+      wpart += neg ? -1 : 1;
+    }
+  } else {
+    const int nnz = __ldg(a.g.off + n);
+    for (int e = threadIdx.x; e < nnz; e += blockDim.x) wpart += WK == 0 ? 1 : __ldg(a.g.w + e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wpart += __shfl_xor_sync(FULL, wpart, o);
+  if (threadIdx.x == 0) Wtot = 0;
+  __syncthreads();
+  if (lane == 0 && wpart != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&Wtot), static_cast<unsigned long long>(wpart));
+  __syncthreads();
+  if (slot >= cf.rpc || r >= a.replicas) return;  // only per-replica barriers below
+  const long long W2 = Wtot;  // = 2 * total weight (every edge twice in the CSR)
+
+  auto row = [&](int v, int& e0, int& e1) {
+    if (CS) {
+      e0 = offs[v];
+      e1 = offs[v + 1];
+    } else {
+      e0 = __ldg(a.g.off + v);
+      e1 = __ldg(a.g.off + v + 1);
+    }
+  };
+  // neighbour u and weight of CSR entry e
+  auto entry = [&](int e, int& u, int& w) {
+    if (CS) {
+      const int c = cols[e];
+      u = WK == 1 ? (c & 0x7fff) : c;
+      w = WK == 1 && (c & 0x8000) ? -1 : 1;
+    } else {
+      u = __ldg(a.g.col + e);
+      w = WK == 0 ? 1 : __ldg(a.g.w + e);
+    }
+  };
+
+  unsigned char* rep = csm + cf.off_rep + slot * cf.rep_bytes;
+  int8_t* s = reinterpret_cast<int8_t*>(rep);
+  unsigned char* fld = rep + cf.n_pad4;
+  const int bid = 1 + slot, bthreads = 32 * P;
+  const size_t rs = static_cast<size_t>(r);
+  const uint64_t seed = a.seeds[r];
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  const int a4 = a.a4, bb = a.b;
+
+  // ---- init (anneal.cpp:148-155): the serial stream-0 coins (chain 0), fields
+  if (j == 0) {
+    Xoshiro r0 = Xoshiro::stream(seed, 0);
+    int G = 0;
+    for (int i = 0; i < n; i++) {
+      const int v = (r0.next() >> 63) ? 1 : -1;
+      G += v;
+      if ((i & 31) == lane) s[i] = static_cast<int8_t>(v);
+    }
+    if (lane == 0) rep_G[slot] = G;
+  }
+  bar_sync(bid, bthreads);
+  for (int v = j * 32 + lane; v < n; v += bthreads) {
+    int e0, e1, f = 0;
+    row(v, e0, e1);
+    for (int e = e0; e < e1; e++) {
+      int u, w;
+      entry(e, u, w);
+      f += w * s[u];
+    }
+    fset<FB>(fld, v, f);
+  }
+  bar_sync(bid, bthreads);
+  if (a.snaps != nullptr)
+    for (int i = j * 32 + lane; i < n; i += bthreads) a.snaps[rs * (a.sweeps + 1) * n + i] = s[i];
+  if (j == 0 && lane == 0 && a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1)] = globaltimer_ns();
+
+  // one chunk: visits against counter G (lane order), spin stores and the
+  // scatter of every change into its neighbours' fields
+  auto chunk = [&](int c, int& G, int sweep, unsigned long long tm, bool en) {
+    const int p = c * 32 + lane;
+    const bool live = p < n;
+    const int v = live ? order[p] : 0;
+    const int own = live ? s[v] : -1, f = live ? fget<FB>(fld, v) : 0;
+    const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(v), 0u, 0u, k0, k1);
+    const bool coin = (x.z >> 31) != 0, flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
+    const int base = -a4 * own - bb * f;
+    int fin = live ? decide(a4 * G + base, coin, flip) : own;
+    unsigned up = __ballot_sync(FULL, fin > own), dn = __ballot_sync(FULL, fin < own);
+    if ((up | dn) == 0u) return;
+    const unsigned below = (1u << lane) - 1u;
+    const int fin2 = live ? decide(a4 * (G + 2 * (__popc(up & below) - __popc(dn & below))) + base, coin, flip) : own;
+    if (__all_sync(FULL, fin2 == fin)) {
+      G += 2 * (__popc(up) - __popc(dn));
+    } else {
+      fin = warp_seq_decide(own, f, live, coin, flip, G, a4, bb, lane);
+      up = __ballot_sync(FULL, fin > own);
+      dn = __ballot_sync(FULL, fin < own);
+    }
+    if (fin != own) s[v] = static_cast<int8_t>(fin);
+    for (unsigned chg = up | dn; chg != 0u; chg &= chg - 1u) {
+      const int l = __ffs(chg) - 1;
+      const int vl = __shfl_sync(FULL, v, l), dl = ((up >> l) & 1u) ? 2 : -2;
+      int e0, e1;
+      row(vl, e0, e1);
+      for (int e = e0 + lane; e < e1; e += 32) {
+        int u, w;
+        entry(e, u, w);
+        fadd<FB>(fld, u, w * dl);
+      }
+    }
+  };
+
+  for (int sweep = 0; sweep < a.sweeps; sweep++) {
+    const unsigned long long tm = a.tmask[sweep];
+    const bool en = a.thr[sweep] >= 0;
+    // this chain's share of the replica's imbalance (units of 2, remainder
+    // rotated over the chains; see k4_partition.cu). (Every chain reading the
+    // replica's live counter instead, the other chains' changes published per
+    // chunk, oscillated: G22 cut 9745 vs 6726, never balanced, even with two
+    // chains: each chain corrects the whole imbalance at once.)
+    const int Gs = rep_G[slot];
+    const int par = Gs & 1, Gh = (Gs - par) / 2;
+    int q = Gh / P, rem = Gh - q * P;
+    if (rem < 0) {
+      rem += P;
+      q -= 1;
+    }
+    const int rot = (j + P - sweep % P) % P;
+    const int share = 2 * (q + (rot < rem ? 1 : 0)) + (rot == P - 1 ? par : 0);
+    int G = share;
+    // chain j visits a contiguous block of chunks in order, so chains decide
+    // far-apart vertices at the same time (round-robin chunks made adjacent
+    // lattice sites concurrent: torus(100,20) best cut 84 vs 44 sequential)
+    const int B = (nmain + P - 1) / P, c1 = min(nmain, (j + 1) * B);
+#pragma unroll 1
+    for (int c = j * B; c < c1; c++) chunk(c, G, sweep, tm, en);
+    if (lane == 0) red_d[warp] = G - share;
+    bar_sync(bid, bthreads);
+    // the tail, in order against the replica's exact counter
+    if (j == 0) {
+      int dsum = lane < P ? red_d[slot * P + lane] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(FULL, dsum, o);
+      int Gt = Gs + dsum;
+#pragma unroll 1
+      for (int c = nmain; c < nck; c++) chunk(c, Gt, sweep, tm, en);
+      if (lane == 0) rep_G[slot] = Gt;
+    }
+    bar_sync(bid, bthreads);
+    // record_barrier: spin sum and the exact cut from the exact fields
+    long long sf = 0, ss = 0;
+    for (int v = j * 32 + lane; v < n; v += bthreads) {
+      const int sv = s[v];
+      sf += sv * fget<FB>(fld, v);
+      ss += sv;
+      if (a.snaps != nullptr) a.snaps[(rs * (a.sweeps + 1) + sweep + 1) * n + v] = static_cast<int8_t>(sv);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sf += __shfl_xor_sync(FULL, sf, o);
+      ss += __shfl_xor_sync(FULL, ss, o);
+    }
+    if (lane == 0) {
+      red_sf[warp] = sf;
+      red_s[warp] = ss;
+    }
+    bar_sync(bid, bthreads);
+    if (j == 0 && lane == 0) {
+      long long SF = 0, S = 0;
+      for (int k = 0; k < P; k++) {
+        SF += red_sf[slot * P + k];
+        S += red_s[slot * P + k];
+      }
+      const long long cut = (W2 / 2 - SF / 2) / 2;
+      const DevTrace rec{cut, S, rep_G[slot]};
+      if (a.trace != nullptr) a.trace[rs * a.sweeps + sweep] = rec;
+      if (a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1) + sweep + 1] = globaltimer_ns();
+      if (sweep + 1 == a.sweeps) a.final_out[rs] = rec;
+    }
+  }
+  for (int i = j * 32 + lane; i < n; i += bthreads) a.spins_out[rs * n + i] = s[i];
+}
+
+template <int WK, int FB>
+const void* chains_fn(bool cs) {
+  return cs ? reinterpret_cast<const void*>(&k2_chains<WK, FB, true>)
+            : reinterpret_cast<const void*>(&k2_chains<WK, FB, false>);
+}
+template <int WK>
+const void* chains_fn(int fb, bool cs) {
+  return fb == 1 ? chains_fn<WK, 1>(cs) : fb == 2 ? chains_fn<WK, 2>(cs) : chains_fn<WK, 4>(cs);
+}
+
 template <typename FT>
 const void* incf_fn(int wkind) {
   return wkind == 0   ? reinterpret_cast<const void*>(&k2_incf<0, FT>)
@@ -362,6 +623,53 @@ const void* k2_fn(int kmax) {
     case 8: return reinterpret_cast<const void*>(&k2_sweep<WK, 8, STD>);
     default: return reinterpret_cast<const void*>(&k2_sweep<WK, 16, STD>);
   }
+}
+
+}  // namespace
+
+namespace {
+
+// k2_chains shared-memory layout and shape; false when it does not fit.
+bool chains_layout(const GraphStats& st, int wkind, int32_t replicas, int fb, ChainCfg* c, bool* cs) {
+  const int n = st.n;
+  const long long nnz = 2 * st.m;
+  const int nck = (n + 31) / 32;
+  int rpc = (replicas + 147) / 148;
+  rpc = rpc < 1 ? 1 : rpc > 15 ? 15 : rpc;  // (named barriers 1..15, one per replica)
+  // chains per replica: up to 4, fewer on small graphs, where concurrent
+  // chains' last-moment flips (each balanced against its own share) leave a
+  // residual imbalance that the few tail vertices cannot absorb (G1, n = 800:
+  // 77% of runs balanced with 4 chains, 94% in the exact mode)
+  int P = 32 / rpc;
+  P = P > 4 ? 4 : P < 1 ? 1 : P;
+  P = std::min(P, std::max(1, n / 500));
+  if (const char* e = std::getenv("GDI_K2_CHAINS")) P = std::max(1, std::min(std::atoi(e), 32 / rpc));
+  int T = nck / 16;
+  T = T < 1 ? 1 : T > 4 ? 4 : T;
+  if (const char* e = std::getenv("GDI_K2_TAIL")) T = std::max(0, std::min(std::atoi(e), nck - 1));
+  if (nck - T < P) P = std::max(1, nck - T);
+  auto r16 = [](long long x) { return (x + 15) & ~15LL; };
+  const long long n_pad4 = r16(n + 4);
+  const long long rep = r16(n_pad4 + static_cast<long long>(fb) * n_pad4);
+  const long long order = r16(4LL * n);
+  const long long offs = r16(4LL * (n + 1)), cols = r16(2 * nnz);
+  const long long cap = 227 * 1024 - 2048;  // (static shared memory)
+  const bool cs_ok = wkind != 2 && n <= (wkind == 1 ? 32767 : 65535);
+  long long total = order + offs + cols + rpc * rep;
+  *cs = cs_ok && total <= cap;
+  if (!*cs) total = order + rpc * rep;
+  if (total > cap) return false;
+  c->rpc = rpc;
+  c->chains = P;
+  c->tail = T;
+  c->off_order = 0;
+  c->off_offs = static_cast<int32_t>(order);
+  c->off_cols = static_cast<int32_t>(order + offs);
+  c->off_rep = static_cast<int32_t>(*cs ? order + offs + cols : order);
+  c->rep_bytes = static_cast<int32_t>(rep);
+  c->n_pad4 = static_cast<int32_t>(n_pad4);
+  c->smem = static_cast<int32_t>(total);
+  return true;
 }
 
 }  // namespace
@@ -393,6 +701,25 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const int fb = st.max_abs_field <= 127 ? 1 : st.max_abs_field <= 32767 ? 2 : 4;
   const bool incf =
       !standard && (1LL + fb) * n_pad * kWarps <= 200 * 1024 && !(force && std::string(force) == "k2_gather");
+  ChainCfg cc{};
+  bool cs = false;
+  plan->chains = false;
+  const bool chains = !standard && !(force && (std::string(force) == "k2_gather" || std::string(force) == "k2_incf")) &&
+                      chains_layout(st, wkind, replicas, fb, &cc, &cs);
+  if (chains) {
+    plan->fn = wkind == 0 ? chains_fn<0>(fb, cs) : wkind == 1 ? chains_fn<1>(fb, cs) : chains_fn<2>(fb, cs);
+    plan->chains = true;
+    plan->cfg = cc;
+    plan->block = 32 * cc.rpc * cc.chains;
+    plan->grid = (replicas + cc.rpc - 1) / cc.rpc;
+    plan->n_pad = n_pad;
+    plan->a4 = static_cast<int32_t>(ra);
+    plan->b = static_cast<int32_t>(rb);
+    static const char* cn[3] = {"k2_chains<unit>", "k2_chains<pm1>", "k2_chains<weighted>"};
+    plan->name = cn[wkind];
+    plan->smem = cc.smem;
+    return 0;
+  }
   if (standard)
     plan->fn = wkind == 0 ? k2_fn<0, true>(kmax) : wkind == 1 ? k2_fn<1, true>(kmax) : k2_fn<2, true>(kmax);
   else if (incf)
@@ -419,6 +746,11 @@ cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t
   a.a4 = plan.a4;
   a.b = plan.b;
   a.n_pad = plan.n_pad;
+  if (plan.chains) {
+    ChainCfg c = plan.cfg;
+    void* pc[] = {&a, &c};
+    return cudaLaunchKernel(plan.fn, dim3(plan.grid), dim3(plan.block), pc, plan.smem, stream);
+  }
   void* params[] = {&a};
   return cudaLaunchKernel(plan.fn, dim3(plan.grid), dim3(plan.block), params, plan.smem, stream);
 }

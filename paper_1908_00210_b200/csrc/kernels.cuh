@@ -114,6 +114,12 @@ struct ThruArgs {
   DevTrace* final_out;
 };
 
+// k2_chains shape and shared-memory layout (byte offsets).
+struct ChainCfg {
+  int32_t rpc, chains, tail;  // replicas per CTA, chains (warps) per replica, tail chunks
+  int32_t off_order, off_offs, off_cols, off_rep, rep_bytes, n_pad4, smem;
+};
+
 // k4 (vertex-partitioned throughput sweep for large graphs): the chunks of
 // the SELL order are dealt round-robin to `world_chains` chains (chain J owns
 // chunks J, J + world_chains, ...); this device runs the chains

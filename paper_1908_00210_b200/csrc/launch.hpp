@@ -93,6 +93,8 @@ struct ThruPlan {
   const void* fn = nullptr;
   int32_t a4 = 4, b = 4;
   int block = 128, grid = 1, smem = 0, n_pad = 0;
+  bool chains = false;  // k2_chains (cfg) rather than k2_sweep / k2_incf
+  ChainCfg cfg{};
   const char* name = "";
 };
 // standard: the literal O(n)-per-visit `standard` strategy (anneal.cpp:97-101)
