@@ -136,7 +136,7 @@ def roofline(bpu: float, updates: float, ms: float, l2: float, hbm: float, peaks
            "traffic": None, "bytes_per_update": bpu, "working_set_bytes": working_set,
            "l2_bytes": l2_size,
            "peak_source": ("live L2 read probe (probe.cu: 16-byte __ldcg loads of a 48 MB L2-resident "
-                           "buffer, 4 CTAs/SM x 512 threads, 50 passes; profiles/l2_peak.json)") if in_l2
+                           "buffer, 4 CTAs/SM x 512 threads, 50 passes; profiles/r02_l2_peak.json)") if in_l2
                           else peaks_src,
            "hbm_peak_gbs": hbm, "frac_of_hbm": achieved / hbm, "l2_peak_gbs": l2, "note": note}
     if traffic:
