@@ -18,6 +18,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -119,6 +120,11 @@ namespace detail {
 struct DeviceGraphCache; // per-(graph, device) HBM copy, see src anneal.cpp
 }
 
+class Graph;
+namespace detail {
+Graph parse_gset_text(std::string_view text);  // the G-set parser (graph.cpp)
+}
+
 // Immutable weighted undirected graph, CSR form: int64 offsets[n+1] and
 // {node, weight} adjacency[2m] in edge-insertion order (reference
 // graph.hpp:25-68). Copies share one lazily built device-resident copy.
@@ -152,6 +158,11 @@ public:
   detail::DeviceGraphCache& device_cache() const;
 
 private:
+  friend Graph detail::parse_gset_text(std::string_view text);
+  // CSR from an edge list; check: endpoint range, self-loop and duplicate
+  // checks (from_edges); the parser has done them already
+  static Graph build(std::int32_t num_nodes, std::span<const Edge> edges, bool check);
+
   std::int32_t n_ = 0;
   std::int64_t m_ = 0;
   std::int32_t max_deg_ = 0;

@@ -1,7 +1,9 @@
 // Graph construction, G-set text I/O and canonical serialisation.
 // Behaviour (accepted syntax, error classes, line numbers, canonical order)
-// follows reference proj/src/graph.cpp:46-174; the implementation scans the
-// whole input buffer once instead of getline + std::unordered_set.
+// follows reference proj/src/graph.cpp:46-174; the implementation parses the
+// input buffer in parallel (one piece of whole lines per host thread) and
+// checks duplicates by hash-partitioned buckets, instead of getline +
+// std::unordered_set.
 #include <algorithm>
 #include <charconv>
 #include <fstream>
@@ -9,9 +11,11 @@
 #include <iterator>
 #include <limits>
 #include <sstream>
+#include <thread>
 
 #include "ising/ising.hpp"
 #include "pairset.hpp"
+#include "parallel.hpp"
 
 namespace ising {
 
@@ -66,7 +70,65 @@ private:
   long number_ = 0;
 };
 
-Graph parse_text(std::string_view text) {
+// One piece of the body (whole lines): its edges, its line count and its
+// first malformed line (local line number, message).
+struct Piece {
+  std::vector<Edge> edges;
+  long lines = 0;
+  long err_line = 0;  // 0: none
+  std::string err;
+};
+
+void parse_piece(std::string_view text, long long n, Piece& out) {
+  LineReader rd(text);
+  std::string_view line;
+  while (rd.next(line)) {
+    if (skippable(line)) continue;
+    long long t[3];
+    const char* msg = nullptr;
+    std::string range_msg;
+    if (!read_ints(line, t, 3)) {
+      msg = "edge line must be \"u v w\"";
+    } else if (t[0] < 1 || t[0] > n || t[1] < 1 || t[1] > n) {
+      range_msg = "endpoint out of range [1, " + std::to_string(n) + "]";
+    } else if (t[0] == t[1]) {
+      msg = "self-loop";
+    } else if (t[2] < std::numeric_limits<std::int32_t>::min() || t[2] > std::numeric_limits<std::int32_t>::max()) {
+      msg = "weight out of range";
+    }
+    if (msg != nullptr || !range_msg.empty()) {
+      out.err_line = rd.number();
+      out.err = msg != nullptr ? std::string(msg) : range_msg;
+      out.lines = rd.number();
+      return;
+    }
+    out.edges.push_back({static_cast<std::int32_t>(t[0] - 1), static_cast<std::int32_t>(t[1] - 1),
+                         static_cast<std::int32_t>(t[2])});
+  }
+  out.lines = rd.number();
+}
+
+// Local line number of the k-th edge line of a piece (error path only).
+long edge_line(std::string_view text, std::size_t k) {
+  LineReader rd(text);
+  std::string_view line;
+  std::size_t seen = 0;
+  while (rd.next(line)) {
+    if (skippable(line)) continue;
+    if (seen++ == k) return rd.number();
+  }
+  return rd.number();
+}
+
+} // namespace
+
+namespace detail {
+
+// The body is cut at newlines into one piece per host thread and parsed in
+// parallel; the duplicate check partitions the edges by key hash (one bucket
+// per thread, each bucket scanned in file order). The error reported is the
+// reference's: the first offending line in file order, with its line number.
+Graph parse_gset_text(std::string_view text) {
   LineReader rd(text);
   std::string_view line;
   long long head[2];
@@ -81,43 +143,131 @@ Graph parse_text(std::string_view text) {
   if (n <= 0) throw parse_error("node count must be positive", head_line);
   if (m < 0) throw parse_error("edge count must be non-negative", head_line);
   if (n > std::numeric_limits<std::int32_t>::max()) throw parse_error("node count too large", head_line);
+  const std::size_t body0 = static_cast<std::size_t>(line.data() + line.size() - text.data()) + 1;
+  const std::string_view body = body0 < text.size() ? text.substr(body0) : std::string_view{};
 
-  std::vector<Edge> edges;
-  edges.reserve(static_cast<std::size_t>(std::min<long long>(m, 1LL << 26)));
-  detail::PairSet seen(static_cast<std::size_t>(std::min<long long>(m, 1LL << 26)));
-  while (rd.next(line)) {
-    if (skippable(line)) continue;
-    long long t[3];
-    if (!read_ints(line, t, 3)) throw parse_error("edge line must be \"u v w\"", rd.number());
-    if (t[0] < 1 || t[0] > n || t[1] < 1 || t[1] > n)
-      throw parse_error("endpoint out of range [1, " + std::to_string(n) + "]", rd.number());
-    if (t[0] == t[1]) throw parse_error("self-loop", rd.number());
-    if (t[2] < std::numeric_limits<std::int32_t>::min() || t[2] > std::numeric_limits<std::int32_t>::max())
-      throw parse_error("weight out of range", rd.number());
-    const auto u = static_cast<std::int32_t>(t[0] - 1), v = static_cast<std::int32_t>(t[1] - 1);
-    if (!seen.insert(detail::PairSet::key(u, v))) throw parse_error("duplicate edge", rd.number());
-    edges.push_back({u, v, static_cast<std::int32_t>(t[2])});
+  // pieces: [cut[t], cut[t+1]), each starting at a line start
+  unsigned T = std::thread::hardware_concurrency();
+  T = T < 1 ? 1 : T > 16 ? 16 : T;
+  if (body.size() < (1u << 20)) T = 1;
+  std::vector<std::size_t> cut(T + 1, body.size());
+  cut[0] = 0;
+  for (unsigned t = 1; t < T; t++) {
+    std::size_t p = std::max(cut[t - 1], body.size() * t / T);
+    while (p < body.size() && p > 0 && body[p - 1] != '\n') p++;
+    cut[t] = p;
   }
-  if (static_cast<long long>(edges.size()) != m)
-    throw parse_error("header announces " + std::to_string(m) + " edges, found " +
-                      std::to_string(edges.size()));
-  return Graph::from_edges(static_cast<std::int32_t>(n), edges);
+  std::vector<Piece> pieces(T);
+  gdi::parallel_rows(T, 2, [&](std::size_t t0, std::size_t t1) {
+    for (std::size_t t = t0; t < t1; t++) parse_piece(body.substr(cut[t], cut[t + 1] - cut[t]), n, pieces[t]);
+  });
+  // the first malformed line in file order (pieces after it are not used)
+  long base = head_line;
+  unsigned used = T;
+  long syntax_line = 0;
+  std::string syntax_msg;
+  std::vector<long> first_line(T);
+  for (unsigned t = 0; t < T; t++) {
+    first_line[t] = base;
+    if (pieces[t].err_line != 0) {
+      syntax_line = base + pieces[t].err_line;
+      syntax_msg = pieces[t].err;
+      used = t + 1;
+      break;
+    }
+    base += pieces[t].lines;
+  }
+  std::vector<std::size_t> eoff(used + 1, 0);
+  for (unsigned t = 0; t < used; t++) eoff[t + 1] = eoff[t] + pieces[t].edges.size();
+  const std::size_t ne = eoff[used];
+  std::vector<Edge> edges(ne);
+  gdi::parallel_rows(used, 2, [&](std::size_t t0, std::size_t t1) {
+    for (std::size_t t = t0; t < t1; t++) std::copy(pieces[t].edges.begin(), pieces[t].edges.end(), edges.begin() + eoff[t]);
+  });
+
+  // duplicates: (key, index) scattered into per-bucket runs, in file order
+  // within a bucket; bucket b is then checked by one thread
+  const unsigned B = T;
+  auto bucket = [B](std::uint64_t k) {
+    const std::uint64_t h = k * 0x9e3779b97f4a7c15ULL;
+    return static_cast<unsigned>((h >> 32) % B);
+  };
+  std::size_t dup = ne;  // index of the first edge repeating an earlier one
+  if (ne > 1) {
+    std::vector<std::size_t> cnt(static_cast<std::size_t>(T) * B, 0);
+    gdi::parallel_rows(T, 2, [&](std::size_t t0, std::size_t t1) {
+      for (std::size_t t = t0; t < t1; t++)
+        for (std::size_t i = ne * t / T; i < ne * (t + 1) / T; i++)
+          cnt[t * B + bucket(PairSet::key(edges[i].u, edges[i].v))]++;
+    });
+    std::vector<std::size_t> start(static_cast<std::size_t>(T) * B);
+    std::vector<std::size_t> bstart(B + 1, 0);
+    std::size_t acc = 0;
+    for (unsigned b = 0; b < B; b++) {
+      bstart[b] = acc;
+      for (unsigned t = 0; t < T; t++) {
+        start[t * B + b] = acc;
+        acc += cnt[t * B + b];
+      }
+    }
+    bstart[B] = acc;
+    std::vector<std::pair<std::uint64_t, std::size_t>> keyed(ne);
+    gdi::parallel_rows(T, 2, [&](std::size_t t0, std::size_t t1) {
+      for (std::size_t t = t0; t < t1; t++) {
+        std::vector<std::size_t> pos(start.begin() + t * B, start.begin() + (t + 1) * B);
+        for (std::size_t i = ne * t / T; i < ne * (t + 1) / T; i++) {
+          const std::uint64_t k = PairSet::key(edges[i].u, edges[i].v);
+          keyed[pos[bucket(k)]++] = {k, i};
+        }
+      }
+    });
+    std::vector<std::size_t> first_dup(B, ne);
+    gdi::parallel_rows(B, 2, [&](std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; b++) {
+        PairSet seen(bstart[b + 1] - bstart[b]);
+        for (std::size_t i = bstart[b]; i < bstart[b + 1]; i++)
+          if (!seen.insert(keyed[i].first)) {
+            first_dup[b] = keyed[i].second;
+            break;
+          }
+      }
+    });
+    dup = *std::min_element(first_dup.begin(), first_dup.end());
+  }
+  if (dup < ne) {
+    unsigned t = 0;
+    while (eoff[t + 1] <= dup) t++;
+    const long dup_line = first_line[t] + edge_line(body.substr(cut[t], cut[t + 1] - cut[t]), dup - eoff[t]);
+    if (syntax_line == 0 || dup_line < syntax_line) throw parse_error("duplicate edge", dup_line);
+  }
+  if (syntax_line != 0) throw parse_error(syntax_msg, syntax_line);
+  if (static_cast<long long>(ne) != m)
+    throw parse_error("header announces " + std::to_string(m) + " edges, found " + std::to_string(ne));
+  return Graph::build(static_cast<std::int32_t>(n), edges, false);
 }
 
-} // namespace
+}  // namespace detail
 
 Graph Graph::from_edges(std::int32_t num_nodes, std::span<const Edge> edges) {
+  return build(num_nodes, edges, true);
+}
+
+Graph Graph::build(std::int32_t num_nodes, std::span<const Edge> edges, bool check) {
   if (num_nodes <= 0) throw domain_error("graph needs a positive node count");
   Graph g;
   g.n_ = num_nodes;
   g.m_ = static_cast<std::int64_t>(edges.size());
   std::vector<std::int64_t> deg(static_cast<std::size_t>(num_nodes) + 1, 0);
-  detail::PairSet seen(edges.size());
+  if (check) {
+    detail::PairSet seen(edges.size());
+    for (const Edge& e : edges) {
+      if (e.u < 0 || e.u >= num_nodes || e.v < 0 || e.v >= num_nodes)
+        throw domain_error("edge endpoint out of range");
+      if (e.u == e.v) throw domain_error("self-loop");
+      if (!seen.insert(detail::PairSet::key(e.u, e.v))) throw domain_error("duplicate edge");
+    }
+  }
   for (const Edge& e : edges) {
-    if (e.u < 0 || e.u >= num_nodes || e.v < 0 || e.v >= num_nodes)
-      throw domain_error("edge endpoint out of range");
-    if (e.u == e.v) throw domain_error("self-loop");
-    if (!seen.insert(detail::PairSet::key(e.u, e.v))) throw domain_error("duplicate edge");
     deg[e.u + 1]++;
     deg[e.v + 1]++;
     g.unit_ = g.unit_ && e.weight == 1;
@@ -139,10 +289,10 @@ Graph Graph::from_edges(std::int32_t num_nodes, std::span<const Edge> edges) {
 
 Graph Graph::parse_gset(std::istream& in) {
   std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
-  return parse_text(text);
+  return detail::parse_gset_text(text);
 }
 
-Graph Graph::parse_gset(const std::string& text) { return parse_text(text); }
+Graph Graph::parse_gset(const std::string& text) { return detail::parse_gset_text(text); }
 
 Graph Graph::parse_gset_file(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
