@@ -2,6 +2,7 @@
 // fused evaluation. Everything here is host code around the sm_100a kernels
 // in k1_exact.cu / k2_throughput.cu / k3_eval.cu.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -22,6 +23,17 @@
 #include "kernels.cuh"
 #include "launch.hpp"
 #include "layout.hpp"
+
+namespace {
+// NVTX range over a host-side phase (upload, launch, fetch show
+// up by name in nsys / ncu --nvtx timelines); header-only NVTX 3, no library.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace gdi;
 
@@ -298,6 +310,7 @@ int validate_host(int32_t n, const int64_t* offsets, const int32_t* nbr, int str
 // nbr/weights (separate arrays) or pairs (interleaved {node, weight}).
 int create_graph(int device, int32_t n, const int64_t* offsets, const int32_t* nbr, const int32_t* weights,
                  const int32_t* pairs, gdi_graph** out) {
+  NvtxRange nvtx_range("gdi_graph_create");
   if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
   *out = nullptr;
   if (n <= 0) return fail(GDI_ERR_DOMAIN, "graph needs a positive node count");
@@ -427,6 +440,7 @@ namespace {
 
 int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, void* stream, gdi_session** out,
                    bool host_trace) {
+  NvtxRange nvtx_range("gdi_session_create");
   if (!out) return fail(GDI_ERR_CONFIG, "out is NULL");
   *out = nullptr;
   if (!g) return fail(GDI_ERR_CONFIG, "graph is NULL");
@@ -559,6 +573,7 @@ namespace {
 
 // gdi_session_fetch, with the trace optionally in column form (cols)
 int fetch_impl(gdi_session* s, gdi_outputs* out, const gdi_trace_columns* cols) {
+  NvtxRange nvtx_range("gdi_session_fetch");
   if (!s || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
   if (!s->launched) return fail(GDI_ERR_CONFIG, "session has not been launched");
   GDI_CUDA(cudaSetDevice(s->g->device));
@@ -655,6 +670,7 @@ int gdi_session_set_seeds(gdi_session* s, const uint64_t* seeds) {
 }
 
 int gdi_session_launch(gdi_session* s) {
+  NvtxRange nvtx_range("gdi_session_launch");
   if (!s) return fail(GDI_ERR_CONFIG, "session is NULL");
   GDI_CUDA(cudaSetDevice(s->g->device));
   if (s->use_part) {
@@ -889,6 +905,7 @@ int gdi_anneal_batch_columns(const gdi_graph* g, const gdi_params* p, const uint
 
 int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,
                        int64_t b_num, int64_t denom, gdi_score* scores) {
+  NvtxRange nvtx_range("gdi_evaluate_batch");
   if (!g || !spins || !scores) return fail(GDI_ERR_CONFIG, "NULL argument");
   if (replicas < 1) return fail(GDI_ERR_CONFIG, "replicas must be >= 1");
   if (denom <= 0) return fail(GDI_ERR_CONFIG, "denom must be positive");
@@ -1077,6 +1094,7 @@ int gdi_part_attach_local(gdi_part* s, gdi_part* const* parts) {
 }
 
 int gdi_part_init(gdi_part* s) {
+  NvtxRange nvtx_range("gdi_part_init");
   if (!s) return fail(GDI_ERR_CONFIG, "NULL argument");
   GDI_CUDA(cudaSetDevice(s->g->device));
   GDI_CUDA(part_init_launch(s->plan, s->args, s->stream));
@@ -1085,6 +1103,7 @@ int gdi_part_init(gdi_part* s) {
 }
 
 int gdi_part_sweep(gdi_part* s, int32_t sweep, void* send) {
+  NvtxRange nvtx_range("gdi_part_sweep");
   if (!s || !send) return fail(GDI_ERR_CONFIG, "NULL argument");
   if (!s->inited) return fail(GDI_ERR_CONFIG, "gdi_part_init not called");
   if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
@@ -1096,6 +1115,7 @@ int gdi_part_sweep(gdi_part* s, int32_t sweep, void* send) {
 }
 
 int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv) {
+  NvtxRange nvtx_range("gdi_part_finish");
   if (!s || !recv) return fail(GDI_ERR_CONFIG, "NULL argument");
   if (sweep < 0 || sweep >= s->p.sweeps) return fail(GDI_ERR_CONFIG, "sweep out of range");
   GDI_CUDA(cudaSetDevice(s->g->device));
@@ -1105,6 +1125,7 @@ int gdi_part_finish(gdi_part* s, int32_t sweep, const void* recv) {
 }
 
 int gdi_part_fetch(gdi_part* s, gdi_outputs* out) {
+  NvtxRange nvtx_range("gdi_part_fetch");
   if (!s || !out) return fail(GDI_ERR_CONFIG, "NULL argument");
   GDI_CUDA(cudaSetDevice(s->g->device));
   GDI_CUDA(cudaStreamSynchronize(s->stream));
