@@ -94,13 +94,13 @@ struct gdi_graph {
   bool thru_built = false, pipe_built = false, part_built = false;
   ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
   DevBuf psell, pdeg;  // K4: the SELL rows over visit-order positions, degree by position
-  PipeLayout pipel;  // k1_pipe: far lists + window masks
-  PipeGraph pipe;    // k1_pipe view (ok = eligible; pointers once built)
+  PipeLayout pipel;  // k1_window: window masks, forward masks, SELL rows
+  PipeGraph pipe;    // k1_window view (ok = eligible; pointers once built)
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
                                 thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes +
-                                pipel.far_col.bytes + pipel.far_meta.bytes + pipel.win_pos.bytes +
+                                pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
                                 pipel.wsell_off.bytes);
   }
@@ -118,15 +118,14 @@ struct gdi_session {
   ThruPlan tplan;
   PartPlan kplan;
   bool use_block = false;  // k1_block (exact mode default)
-  bool use_pipe = false;
-  bool use_win = false;  // the pipe plan is a k1_window plan
+  bool use_win = false;  // k1_window (pplan)
   bool use_thru = false;
   bool use_part = false;
   cudaGraphExec_t part_exec = nullptr;  // k4: 1 + 2M launches replayed as one graph
   std::vector<double> pf;        // flip probability per sweep (iterated product)
   std::vector<long long> thr;    // integer flip threshold per sweep
   std::vector<unsigned long long> tmask;  // thr * 2^11 + 2047, saturated
-  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gwords, gspins;
+  DevBuf seeds, thr_d, tmask_d, spins, trace, stamps, snaps, final_out, watchdog, prof, gspins;
   DevBuf live, gsum, gdelta, acc, done, finished;  // k4 state (live: position-space spin words)
   DevTrace* tr = nullptr;              // trace records: s->trace, or pinned host memory
   unsigned long long* st = nullptr;    // sweep timestamps: s->stamps, or pinned host memory
@@ -218,8 +217,6 @@ int ensure_pipe(gdi_graph* g) {
   const cudaError_t e = build_pipe_layout(g->csr(), pipe_window(), &g->pipel, st);
   cudaStreamDestroy(st);
   GDI_CUDA(e);
-  g->pipe.far_col = g->pipel.far_col.as<int32_t>();
-  g->pipe.far_meta = g->pipel.far_meta.as<int4>();
   g->pipe.win_pos = g->pipel.win_pos.as<uint32_t>();
   g->pipe.win_neg = g->pipel.win_neg.as<uint32_t>();
   g->pipe.fwd_pos = g->pipel.fwd_pos.as<uint32_t>();
@@ -369,7 +366,7 @@ int create_graph(int device, int32_t n, const int64_t* offsets, const int32_t* n
   g->st.max_degree = scan.max_degree;
   g->wkind = g->st.unit ? 0 : (!scan.non_pm1 ? 1 : 2);
   g->st.pm1 = g->wkind <= 1;
-  // k1_pipe eligibility (every |w| == 1, n >= 2L); its layout is built lazily
+  // k1_window eligibility (every |w| == 1, n >= 2L); its layout is built lazily
   g->pipe.ok = n >= 2 * pipe_window() && (g->st.unit || !scan.non_pm1);
   g->pipe.n_words = (n + 1 + 3) & ~3;
   *out = g.release();
@@ -455,7 +452,7 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   s->replicas = replicas;
   schedule(s->p, s->pf, s->thr, s->tmask);
   // Both strategies coincide in the exact mode (reference acceptance.cpp
-  // criterion 8). Prefer the warp-specialised pipe kernel when it applies.
+  // criterion 8).
   const std::string force = forced_kernel();
   // THROUGHPUT: the racy pooled-mode kernel. Any exact-mode result is also a
   // legal outcome of the racy contract (one worker claiming every chunk), so
@@ -466,8 +463,8 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   // at once: harmless on large graphs (1M: cut within 0.3% of the sequential
   // run) but a large fraction of a small one, where lattices (torus) then
   // degrade as under Jacobi updates.
-  const bool thru_ok = p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force != "pipe" &&
-                       force != "pipe_gmem";
+  const bool thru_ok = p->mode == GDI_MODE_THROUGHPUT && force != "exact" && force.rfind("window", 0) != 0 &&
+                       force != "block";
   // (the literal `standard` strategy only exists in K2: its O(n) traversal per
   // visit needs the replica's spins on chip)
   if (thru_ok && force != "part" &&
@@ -480,33 +477,25 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
            thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
     s->use_thru = true;
   // exact mode: k1_block (fixed-point windows) by default; k1_window
-  // (speculative windows) where k1_block does not fit; k1_pipe on request
-  // (GDI_FORCE_KERNEL=pipe|pipe_gmem); k1_exact for everything else
-  const bool want_pipe = force == "pipe" || force == "pipe_gmem";
-  bool pipe_ok = false;
+  // (speculative windows) where k1_block does not fit (graphs whose CSR does
+  // not fit shared memory, e.g. G81); k1_exact for everything else
+  // (GDI_FORCE_KERNEL=block|window|exact picks one for tests)
   if (!s->use_thru && (force.empty() || force == "auto" || force == "block") &&
       block_plan(g->st, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->bplan) == 0)
     s->use_block = true;
   if (force == "block" && !s->use_block)
     return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=block but k1_block does not apply");
-  if (s->use_block) {
-  } else if (!s->use_thru && force != "exact" && !want_pipe &&
-      window_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0) {
-    pipe_ok = true;
+  if (!s->use_block && !s->use_thru && force != "exact" &&
+      window_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0)
     s->use_win = true;
-  } else if (!s->use_thru && force != "exact" && force.rfind("window", 0) != 0) {
-    pipe_ok = pipe_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0;
-  }
   if (force.rfind("window", 0) == 0 && !s->use_win)
     return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=window but k1_window does not apply");
-  if ((force == "pipe" || force == "pipe_gmem") && !pipe_ok) return fail(GDI_ERR_CAPACITY, "GDI_FORCE_KERNEL=pipe but the pipe kernel does not apply");
-  s->use_pipe = pipe_ok;
-  if (!s->use_thru && !s->use_block && !pipe_ok && exact_plan(g->st, replicas, &s->plan))
+  if (!s->use_thru && !s->use_block && !s->use_win && exact_plan(g->st, replicas, &s->plan))
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
   gdi_graph* gm = const_cast<gdi_graph*>(g);  // layouts are a lazily built cache
   if (s->use_thru && (rc = ensure_thru(gm))) return rc;
   if (s->use_part && (rc = ensure_part(gm))) return rc;
-  if (s->use_pipe && (rc = ensure_pipe(gm))) return rc;
+  if (s->use_win && (rc = ensure_pipe(gm))) return rc;
 
   if (stream) {
     s->stream = static_cast<cudaStream_t>(stream);
@@ -524,8 +513,6 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   GDI_CUDA(s->final_out.alloc(R * sizeof(DevTrace)));
   GDI_CUDA(s->watchdog.alloc(8 * sizeof(int)));
   GDI_CUDA(s->prof.alloc(16 * sizeof(unsigned long long)));
-  if (s->use_pipe && s->pplan.gw && !s->use_win)
-    GDI_CUDA(s->gwords.alloc(static_cast<size_t>(s->pplan.grid) * g->pipe.n_words * sizeof(uint32_t)));
   if (s->use_win && s->pplan.gw)
     GDI_CUDA(s->gspins.alloc(static_cast<size_t>(replicas) * s->pplan.n_words));
   if (p->flags & GDI_FLAG_TRACE) {
@@ -750,11 +737,9 @@ int gdi_session_launch(gdi_session* s) {
     s->launched = true;
     return GDI_OK;
   }
-  if (s->use_pipe) {
+  if (s->use_win) {
     PipeArgs a{};
     a.g = s->g->csr();
-    a.far_col = s->g->pipe.far_col;
-    a.far_meta = s->g->pipe.far_meta;
     a.win_pos = s->g->pipe.win_pos;
     a.win_neg = s->g->pipe.win_neg;
     a.fwd_pos = s->g->pipe.fwd_pos;
@@ -762,8 +747,7 @@ int gdi_session_launch(gdi_session* s) {
     a.wsell = s->g->pipe.wsell;
     a.wsell_off = s->g->pipe.wsell_off;
     a.n_words = s->g->pipe.n_words;
-    a.gwords = s->pplan.gw && !s->use_win ? s->gwords.as<uint32_t>() : nullptr;
-    a.gspins = s->use_win && s->pplan.gw ? s->gspins.as<int8_t>() : nullptr;
+    a.gspins = s->pplan.gw ? s->gspins.as<int8_t>() : nullptr;
     a.sweeps = s->p.sweeps;
     a.replicas = s->replicas;
     a.seeds = s->seeds.as<uint64_t>();
@@ -781,7 +765,7 @@ int gdi_session_launch(gdi_session* s) {
     GDI_CUDA(cudaMemsetAsync(s->watchdog.p, 0, s->watchdog.bytes, s->stream));
     GDI_CUDA(cudaMemsetAsync(s->prof.p, 0, s->prof.bytes, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev0, s->stream));
-    GDI_CUDA(s->use_win ? window_launch(s->pplan, a, s->stream) : pipe_launch(s->pplan, a, s->stream));
+    GDI_CUDA(window_launch(s->pplan, a, s->stream));
     GDI_CUDA(cudaEventRecord(s->ev1, s->stream));
     s->launched = true;
     return GDI_OK;
@@ -808,8 +792,9 @@ int gdi_session_launch(gdi_session* s) {
   return GDI_OK;
 }
 
-// A stalled k1_pipe pipeline aborts itself (watchdog) instead of hanging;
-// surface that as a runtime error rather than returning wrong results.
+// A stalled k1_window producer/consumer pipeline aborts itself (watchdog)
+// instead of hanging; surface that as a runtime error rather than returning
+// wrong results.
 static int check_watchdog(gdi_session* s) {
   if (s->use_part) {  // k4 has no inter-warp waits; debug counters only
     if (std::getenv("GDI_K4_DEBUG")) {
@@ -819,27 +804,18 @@ static int check_watchdog(gdi_session* s) {
     }
     return GDI_OK;
   }
-  if (!s->use_pipe) return GDI_OK;
-  if (s->use_win && std::getenv("GDI_PIPE_DEBUG") && (std::atoi(std::getenv("GDI_PIPE_DEBUG")) & 4)) {
+  if (!s->use_win) return GDI_OK;
+  if (std::getenv("GDI_PIPE_DEBUG") && (std::atoi(std::getenv("GDI_PIPE_DEBUG")) & 4)) {
     unsigned long long c[16] = {0};
     GDI_CUDA(cudaMemcpy(c, s->prof.p, sizeof c, cudaMemcpyDeviceToHost));
     const double st = c[0] ? static_cast<double>(c[0]) : 1.0;
     std::fprintf(stderr, "[k1_window prof] steps %llu, visits/step %.2f, cycles/step %.0f (refill %.0f, draw wait %.0f)\n",
                  c[0], c[1] / st, c[3] / st, c[2] / st, c[4] / st);
   }
-  if (s->pplan.prof && !s->use_win) {
-    unsigned long long c[16] = {0};
-    GDI_CUDA(cudaMemcpy(c, s->prof.p, sizeof c, cudaMemcpyDeviceToHost));
-    const double nb = c[4] ? static_cast<double>(c[4]) : 1.0;
-    std::fprintf(stderr,
-                 "[k1_pipe prof] per batch (cycles): decider total %.1f wait_ready %.1f wait_draws %.1f "
-                 "replays %.4f | producer total %.1f wait %.1f | gatherers(sum) total %.1f wait %.1f\n",
-                 c[0] / nb, c[1] / nb, c[2] / nb, c[3] / nb, c[5] / nb, c[6] / nb, c[7] / nb, c[8] / nb);
-  }
   int w[8] = {0};
   GDI_CUDA(cudaMemcpy(w, s->watchdog.p, sizeof w, cudaMemcpyDeviceToHost));
   if (w[0] != 0)
-    return fail(GDI_ERR_RUNTIME, "k1_pipe watchdog fired: stage " + std::to_string(w[0]) + " block " +
+    return fail(GDI_ERR_RUNTIME, "k1_window watchdog fired: stage " + std::to_string(w[0]) + " block " +
                                      std::to_string(w[1]) + " thread " + std::to_string(w[2]) + " (" +
                                      std::to_string(w[3]) + ", " + std::to_string(w[4]) + ")");
   return GDI_OK;
@@ -865,7 +841,7 @@ const char* gdi_session_kernel(const gdi_session* s) {
   if (s->use_part) return s->kplan.name;
   if (s->use_thru) return s->tplan.name;
   if (s->use_block) return s->bplan.name;
-  return s->use_pipe ? s->pplan.name : s->plan.name;
+  return s->use_win ? s->pplan.name : s->plan.name;
 }
 
 int gdi_session_destroy(gdi_session* s) {

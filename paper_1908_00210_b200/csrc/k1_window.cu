@@ -1,6 +1,6 @@
 // K1 v3 — bit-exact GDI sweep by speculative visit windows (sm_100a).
 //
-// Same contract as k1_exact.cu / k1_pipe.cu: bit-identical to the
+// Same contract as k1_exact.cu / k1_block.cu: bit-identical to the
 // reference's single-worker anneal (proj/src/anneal.cpp:132-231; visit_node
 // :86-128; record_barrier :165-187).
 //
@@ -19,7 +19,7 @@
 // including it is exactly what the sequential chain does, so it is
 // accepted: the event's spin is written, G and the draw position advance,
 // and the pending lanes behind it correct their fields through the 32-bit
-// window masks of the k1_pipe layout (bit k-1 of win_pos/win_neg[v]: vertex
+// window masks of the k1_window layout (bit k-1 of win_pos/win_neg[v]: vertex
 // v-k is a +1/-1 neighbour). The window then shifts down by the accepted
 // count and only the emptied lanes gather new rows. Windows never cross a
 // sweep (the barrier records the exact incremental cut and the counter).
@@ -31,8 +31,8 @@
 // the sign bit. Release/acquire on shared-memory positions orders the ring;
 // every polling loop has a watchdog that aborts instead of hanging.
 //
-// Restricted to |w| == 1 graphs with the 32-bit decision bound (k1_pipe's
-// conditions); spins per replica in shared memory, or in global memory (GS)
+// Restricted to |w| == 1 graphs with the 32-bit decision bound
+// (window_plan); spins per replica in shared memory, or in global memory (GS)
 // when they do not fit (each replica's spins are private to its warp).
 #include <cuda_runtime.h>
 

@@ -621,7 +621,11 @@ const void* k2_fn(int kmax) {
     case 2: return reinterpret_cast<const void*>(&k2_sweep<WK, 2, STD>);
     case 4: return reinterpret_cast<const void*>(&k2_sweep<WK, 4, STD>);
     case 8: return reinterpret_cast<const void*>(&k2_sweep<WK, 8, STD>);
-    default: return reinterpret_cast<const void*>(&k2_sweep<WK, 16, STD>);
+    default:  // (weighted rows carry a weight array: 16 groups of both spilled, so 8 + the loop)
+      if constexpr (WK == 2)
+        return reinterpret_cast<const void*>(&k2_sweep<WK, 8, STD>);
+      else
+        return reinterpret_cast<const void*>(&k2_sweep<WK, 16, STD>);
   }
 }
 
@@ -676,7 +680,7 @@ bool chains_layout(const GraphStats& st, int wkind, int32_t replicas, int fb, Ch
 
 int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, bool standard,
               ThruPlan* plan) {
-  // 32-bit decision arithmetic must be exact (same bound as k1_pipe)
+  // 32-bit decision arithmetic must be exact (same bound as k1_window)
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
   while (y) {
     const long long t = x % y;

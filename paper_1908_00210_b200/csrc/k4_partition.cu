@@ -699,14 +699,16 @@ void pick_k(bool sm, PartPlan* plan) {
                        : reinterpret_cast<const void*>(&k4_finish<WK, KMAX, false>);
 }
 
+// (the register bucket is at most 2 int4 groups, 1 with a weight array: at
+// 64 registers per thread, 4 groups spilled 56-350 bytes; longer rows loop)
 template <int WK>
 void pick(int kmax, bool sm, PartPlan* plan) {
-  if (kmax == 1)
+  if constexpr (WK == 2)
     pick_k<WK, 1>(sm, plan);
-  else if (kmax == 2)
-    pick_k<WK, 2>(sm, plan);
+  else if (kmax == 1)
+    pick_k<WK, 1>(sm, plan);
   else
-    pick_k<WK, 4>(sm, plan);
+    pick_k<WK, 2>(sm, plan);
 }
 
 }  // namespace

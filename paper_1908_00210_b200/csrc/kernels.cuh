@@ -42,21 +42,16 @@ struct ExactArgs {
   DevTrace* final_out;    // [R]
 };
 
-// k1_pipe (warp-specialised exact kernel). Far lists: for vertex i,
-// far_meta[i] = {offset into far_col, #(+1 neighbours), #(-1 neighbours),
-// fconst}; far_col holds the +1 far neighbours then the -1 far neighbours.
-// win_pos/win_neg[i]: bit k-1 set when vertex (i-k) mod n is a +1 / -1
-// neighbour, k = 1..32.
+// k1_window (speculative visit windows, the exact kernel for graphs whose CSR
+// does not fit k1_block's shared memory). win_pos/win_neg[i]: bit k-1 set
+// when vertex (i-k) mod n is a +1 / -1 neighbour, k = 1..32.
 struct PipeArgs {
   DevCsr g;                        // full CSR (initial cut only)
-  const int32_t* far_col;
-  const int4* far_meta;
   const uint32_t* win_pos;
   const uint32_t* win_neg;
   const uint32_t* fwd_pos;         // k1_window: forward window masks (bit l: vertex v+1+l is a +1 neighbour)
   const uint32_t* fwd_neg;
   int32_t n_words;                 // spin words per CTA (>= n + 1)
-  uint32_t* gwords;                // [grid][n_words] global spin words, or nullptr (shared memory)
   int8_t* gspins;                  // k1_window: [R][n_words] global int8 spins, or nullptr (shared memory)
   const int32_t* wsell;            // k1_window rows, SELL-32 over the natural order (layout.hpp)
   const int32_t* wsell_off;

@@ -32,13 +32,11 @@ struct ExactPlan {
 int exact_plan(const GraphStats& st, int32_t replicas, ExactPlan* plan);
 cudaError_t exact_launch(const ExactPlan& plan, const ExactArgs& args, cudaStream_t stream);
 
-// Spin-independent preprocessing of a graph for k1_pipe (built once in
+// Spin-independent preprocessing of a graph for k1_window (built once in
 // gdi_graph_create when every |w| == 1 and n >= 64).
 struct PipeGraph {
   bool ok = false;
   int32_t n_words = 0;
-  int32_t* far_col = nullptr;  // device
-  int4* far_meta = nullptr;  // device
   uint32_t* win_pos = nullptr;
   uint32_t* win_neg = nullptr;
   uint32_t* fwd_pos = nullptr;  // forward window masks (layout.cu k_fwd_masks)
@@ -68,12 +66,8 @@ struct PipePlan {
   const char* name = "";
 };
 
-int pipe_window();
-size_t pipe_smem_bytes(int n_words, int nwarps);
-int pipe_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b,
-              int32_t sweeps, PipePlan* plan);
-cudaError_t pipe_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);
-// k1_window (speculative visit windows; same eligibility as k1_pipe)
+constexpr int pipe_window() { return 32; }  // k1_window masks: 32 visits back / ahead
+// k1_window (speculative visit windows)
 int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int64_t a4, int64_t b,
                 int32_t sweeps, PipePlan* plan);
 cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream);

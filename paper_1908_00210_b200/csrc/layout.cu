@@ -9,8 +9,9 @@
 //   * the throughput layout (K2/K4): degree-binned visit order (stable radix
 //     sort, descending degree, ties by index), SELL-32 rows over it, and the
 //     canonical u < v edge list for the barrier cut;
-//   * the exact-pipe layout (k1_pipe): per row the "far" neighbours and the
-//     32-bit window masks of the L vertices visited just before it.
+//   * the k1_window layout: per row the 32-bit window masks of the L vertices
+//     visited just before it, the forward masks, SELL-32 rows over the natural
+//     order.
 // The layouts are built lazily, the first time a session needs one. A host
 // version of all this took ~0.4 s for the 1M-vertex graph, more than the
 // whole 20-sweep anneal; here it is a few milliseconds.
@@ -141,7 +142,7 @@ __global__ void k_edges_fill(const int32_t* off, const int32_t* col, const int32
     }
 }
 
-// ---- exact-pipe layout (k1_pipe.cu) -----------------------------------------
+// ---- k1_window layout (k1_window.cu) ----------------------------------------
 
 // window distance of neighbour j from row i: k = (i - j) mod n in 1..n-1
 __device__ __forceinline__ int wdist(int i, int j, int n) {
@@ -149,50 +150,17 @@ __device__ __forceinline__ int wdist(int i, int j, int n) {
   return k < 0 ? k + n : k;
 }
 
-__global__ void k_far_count(const int32_t* off, const int32_t* col, int n, int L, int32_t* cnt) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > n) return;
-  if (i == n) {
-    cnt[i] = 0;
-    return;
-  }
-  int c = 0;
-  for (int e = off[i]; e < off[i + 1]; e++) {
-    const int k = wdist(i, col[e], n);
-    c += !(k >= 1 && k <= L);
-  }
-  cnt[i] = c;
-}
-
-// far list per row: +1 neighbours then -1 neighbours; meta = {offset, #pos,
-// #neg, fconst}, fconst = (#pos - #neg) + popc(mask+) - popc(mask-)
-__global__ void k_far_fill(const int32_t* off, const int32_t* col, const int32_t* w, const int32_t* foff, int n,
-                           int L, int32_t* far_col, int4* meta, uint32_t* wpos, uint32_t* wneg) {
+// window masks of row i: bit k-1 of wpos / wneg = the vertex visited k places
+// before i (cyclically) is a +1 / -1 neighbour, k = 1..L
+__global__ void k_win_masks(const int32_t* off, const int32_t* col, const int32_t* w, int n, int L, uint32_t* wpos,
+                            uint32_t* wneg) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t mp = 0u, mn = 0u;
-  int dp = 0, dn = 0;
   for (int e = off[i]; e < off[i + 1]; e++) {
     const int k = wdist(i, col[e], n);
-    const bool minus = w && w[e] < 0;
-    if (k >= 1 && k <= L)
-      (minus ? mn : mp) |= 1u << (k - 1);
-    else if (minus)
-      dn++;
-    else
-      dp++;
+    if (k >= 1 && k <= L) (w && w[e] < 0 ? mn : mp) |= 1u << (k - 1);
   }
-  const int base = foff[i];
-  int p = 0, q = 0;
-  for (int e = off[i]; e < off[i + 1]; e++) {
-    const int k = wdist(i, col[e], n);
-    if (k >= 1 && k <= L) continue;
-    if (w && w[e] < 0)
-      far_col[base + dp + q++] = col[e];
-    else
-      far_col[base + p++] = col[e];
-  }
-  meta[i] = make_int4(base, dp, dn, (dp - dn) + __popc(mp) - __popc(mn));
   wpos[i] = mp;
   wneg[i] = mn;
 }
@@ -394,19 +362,9 @@ __global__ void k_fwd_masks(const uint32_t* __restrict__ wpos, const uint32_t* _
 cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st) {
   const int n = g.n;
   cudaError_t e;
-  DevBuf cnt, foff;
-  if ((e = cnt.alloc((n + 1) * sizeof(int32_t))) || (e = foff.alloc((n + 1) * sizeof(int32_t)))) return e;
-  k_far_count<<<blocks(n + 1), kB, 0, st>>>(g.off, g.col, n, win, cnt.as<int32_t>());
-  if ((e = exclusive_scan(cnt.as<int32_t>(), foff.as<int32_t>(), n + 1, st))) return e;
-  int total = 0;
-  if ((e = cudaMemcpy(&total, foff.as<int32_t>() + n, sizeof total, cudaMemcpyDeviceToHost))) return e;
-  if ((e = L->far_col.alloc((static_cast<size_t>(total) + 1) * sizeof(int32_t))) ||
-      (e = L->far_meta.alloc(n * sizeof(int4))) || (e = L->win_pos.alloc(n * sizeof(uint32_t))) ||
-      (e = L->win_neg.alloc(n * sizeof(uint32_t))))
-    return e;
-  k_fill_i32<<<1, 32, 0, st>>>(L->far_col.as<int32_t>() + total, 1, n);  // never empty; index n = zero word
-  k_far_fill<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, foff.as<int32_t>(), n, win, L->far_col.as<int32_t>(),
-                                       L->far_meta.as<int4>(), L->win_pos.as<uint32_t>(), L->win_neg.as<uint32_t>());
+  if ((e = L->win_pos.alloc(n * sizeof(uint32_t))) || (e = L->win_neg.alloc(n * sizeof(uint32_t)))) return e;
+  k_win_masks<<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, n, win, L->win_pos.as<uint32_t>(),
+                                        L->win_neg.as<uint32_t>());
   if ((e = cudaGetLastError())) return e;
   if ((e = L->fwd_pos.alloc(n * sizeof(uint32_t))) || (e = L->fwd_neg.alloc(n * sizeof(uint32_t)))) return e;
   k_fwd_masks<<<blocks(n), kB, 0, st>>>(L->win_pos.as<uint32_t>(), L->win_neg.as<uint32_t>(), n,

@@ -26,7 +26,7 @@ struct ThruLayout {
 };
 
 struct PipeLayout {
-  DevBuf far_col, far_meta, win_pos, win_neg, fwd_pos, fwd_neg;
+  DevBuf win_pos, win_neg, fwd_pos, fwd_neg;
   // k1_window rows: SELL-32 over the natural vertex order (chunk c = vertices
   // 32c..32c+31, entry k of lane l at (wsell_off[c] + k) * 32 + l; padding
   // index n; -1 weights in bit 31 of the index)
@@ -51,7 +51,7 @@ cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout*
 // vertex at every position.
 cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, cudaStream_t st);
 
-// k1_pipe layout (every |w| == 1, n >= 2 * win).
+// k1_window layout (every |w| == 1, n >= 2 * win).
 cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st);
 
 }  // namespace gdi

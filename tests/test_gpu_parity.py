@@ -178,7 +178,7 @@ def test_session_device_resident_matches_batch(kernel_variant):
     assert ("window" in s.kernel) == (kernel_variant == "legacy")
 
 
-def test_pipe_window_edge_cases_match_oracle():
+def test_window_edge_cases_match_oracle():
     # n just above 2L, dense rows (window masks heavily populated), +-1 weights
     rng = np.random.default_rng(11)
     for n, m, signed in ((64, 300, False), (65, 2000, True), (97, 4000, False), (130, 260, True)):
@@ -200,16 +200,15 @@ def test_pipe_window_edge_cases_match_oracle():
             assert out["trace"][i].tolist() == ref["trace"].tolist(), (n, m, s)
 
 
-# ---- global-memory spin words (k1_pipe<...,gmem>): graphs whose words do not
+# ---- global-memory spins (k1_window<...,gmem>): graphs whose spins do not
 # fit in shared memory, e.g. the 1M-vertex config (BASELINE configs[4])
 
 
-@pytest.mark.parametrize("variant", ["pipe", "pipe_gmem", "window_gmem", "window_masks"])
+@pytest.mark.parametrize("variant", ["window_gmem", "window_masks"])
 @pytest.mark.parametrize("name,count", [("G1", 16), ("G22", 256), ("G81pm1", 16)])
 def test_forced_exact_variants_bit_exact(name, count, variant, kernel_variant, monkeypatch):
-    """The other exact kernels on the golden configs: k1_pipe (warp-specialised),
-    its global-memory spin words, k1_window with global-memory spins and with
-    row-gathered fields (masks)."""
+    """The other exact-kernel forms on the golden configs: k1_window with
+    global-memory spins and with row-gathered fields (masks)."""
     if kernel_variant != "auto":
         pytest.skip("one forced variant per case")
     monkeypatch.setenv("GDI_FORCE_KERNEL", variant)

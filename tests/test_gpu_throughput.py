@@ -161,7 +161,7 @@ def test_k4_forced_matches_exact_quality(name, monkeypatch):
     doc = golden_configs()[name]
     g = product_graph(doc["recipe"])
     prob = pi.MinCutProblem.with_default_coefficients(g)
-    seeds = np.arange(1, 17, dtype=np.uint64)
+    seeds = np.arange(1, 65, dtype=np.uint64)  # (16 seeds: the mean drifted past 0.5% once in ~10 runs)
     _, ex = run_mode(prob, True, seeds)
     monkeypatch.setenv("GDI_FORCE_KERNEL", "part")
     k_th, th = run_mode(prob, False, seeds, trace=True)
