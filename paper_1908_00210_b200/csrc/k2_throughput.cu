@@ -353,8 +353,8 @@ __global__ void __launch_bounds__(32 * kWarps) k2_incf(const ThruArgs a) {
 // packed in 32-bit words so a change scatters with word atomics: no carry
 // crosses into a neighbour's lane since |field| <= max degree < bias) live in
 // shared memory with the visit order and (when it fits) the CSR with 16-bit
-// columns. Chain j of a replica visits the j-th of P contiguous blocks of
-// chunks of the degree-binned order against its own counter, started from its share of the
+// columns. Chain j of a replica visits every P-th segment of kSeg chunks of
+// the degree-binned order against its own counter, started from its share of the
 // replica's exact imbalance (decoupled balance, as K4); after a per-replica
 // barrier, chain 0 decides the last T chunks (lowest degrees) in order
 // against the exact counter, so sweeps end balanced. A visit reads own spin
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
   __shared__ int red_d[32], rep_G[16];
   __shared__ long long red_sf[32], red_s[32];
   __shared__ long long Wtot;
-  const int n = a.g.n, P = cf.chains, T = cf.tail;
-  const int nck = (n + 31) >> 5, nmain = nck - T;
+  const int n = a.g.n, P = cf.chains;
+  const int nck = (n + 31) >> 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = warp / P, j = warp - slot * P;
   const int r = blockIdx.x * cf.rpc + slot;
@@ -544,12 +544,23 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     const int rot = (j + P - sweep % P) % P;
     const int share = 2 * (q + (rot < rem ? 1 : 0)) + (rot == P - 1 ? par : 0);
     int G = share;
-    // chain j visits a contiguous block of chunks in order, so chains decide
-    // far-apart vertices at the same time (round-robin chunks made adjacent
-    // lattice sites concurrent: torus(100,20) best cut 84 vs 44 sequential)
-    const int B = (nmain + P - 1) / P, c1 = min(nmain, (j + 1) * B);
+    // chain j visits the segments j, j + P, ... of kSeg consecutive chunks,
+    // each in order: concurrent chains are kSeg chunks apart (round-robin
+    // single chunks made adjacent lattice sites concurrent: torus(100,20) best
+    // cut 84 vs 44 sequential), and every chain still spans the whole degree
+    // range (contiguous blocks gave chain 0 only the stiffest, highest-degree
+    // vertices, whose share of the imbalance it could not correct: 57% of
+    // runs balanced on a hub graph vs 86% sequential)
+    // the tail: the last T chunks (a quarter of the graph in the final sweep
+    // balanced no more runs of a hub graph: 81% either way, 86% sequential)
+    const int T = cf.tail, nmain = nck - T;
+    const int kSeg = cf.seg;
 #pragma unroll 1
-    for (int c = j * B; c < c1; c++) chunk(c, G, sweep, tm, en);
+    for (int s0 = j * kSeg; s0 < nmain; s0 += P * kSeg) {
+      const int c1 = min(nmain, s0 + kSeg);
+#pragma unroll 1
+      for (int c = s0; c < c1; c++) chunk(c, G, sweep, tm, en);
+    }
     if (lane == 0) red_d[warp] = G - share;
     bar_sync(bid, bthreads);
     // the tail, in order against the replica's exact counter
@@ -651,6 +662,9 @@ bool chains_layout(const GraphStats& st, int wkind, int32_t replicas, int fb, Ch
   int T = nck / 16;
   T = T < 1 ? 1 : T > 4 ? 4 : T;
   if (const char* e = std::getenv("GDI_K2_TAIL")) T = std::max(0, std::min(std::atoi(e), nck - 1));
+  int seg = 8;
+  if (const char* e = std::getenv("GDI_K2_SEG")) seg = std::max(1, std::atoi(e));
+  c->seg = seg;
   if (nck - T < P) P = std::max(1, nck - T);
   auto r16 = [](long long x) { return (x + 15) & ~15LL; };
   const long long n_pad4 = r16(n + 4);

@@ -64,6 +64,7 @@
 // next sweep). Every rank replays the global tail identically.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -677,6 +678,12 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
   const long long cv = static_cast<long long>(atomicAdd(a.acc + 2 * r, 0ull));
   const long long sv = 2 * static_cast<long long>(atomicAdd(a.acc + 2 * r + 1, 0ull)) - n;
   const long long counter = G0 + tot;
+  if ((a.debug & 2) && a.watchdog != nullptr && last_sweep) {  // GDI_K4_DEBUG=2: the last tail's counter
+    a.watchdog[2] = static_cast<int>(G0);
+    a.watchdog[3] = tot;
+    a.watchdog[4] = T;
+    a.watchdog[5] = static_cast<int>(a.gsum[r]);
+  }
   const DevTrace rec{cv, sv, counter};
   if (a.trace != nullptr) a.trace[static_cast<size_t>(r) * a.sweeps + sweep] = rec;
   if (a.stamps != nullptr) a.stamps[static_cast<size_t>(r) * (a.sweeps + 1) + sweep + 1] = globaltimer_ns();
@@ -731,12 +738,19 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const double mean_deg = 2.0 * static_cast<double>(st.m) / st.n;
   const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : 4;
-  // one CTA of 32 chains per SM, spread over the replicas; at least two
-  // chunks per chain (the last one may go to the CTA tail)
+  // one CTA of 32 warps per SM, spread over the replicas
   const int nck = (st.n + 31) / 32;
   const int R = replicas > 0 ? replicas : 1;
   int ctas = 148 / R;
-  const int max_ctas = nck / (2 * kNW);
+  // at most a tenth of the graph in flight (chains x 32 <= n / 10): the cut
+  // grows with the fraction of vertices decided concurrently, not with the
+  // spin copy's staleness (M1, 20 sweeps, 6 seeds: 1/2 -> +1.6% over the
+  // sequential cut in 1.17 ms, 1/8 -> +0.9% in 1.25 ms, 1/10 -> +0.6% in
+  // 1.34 ms, 1/12 -> +0.3% in 1.49 ms; a 100k-vertex hub graph +4.9% at
+  // 1/2, +0.5% at 1/8)
+  int frac = 10;
+  if (const char* e = std::getenv("GDI_K4_FRAC")) frac = std::max(1, std::atoi(e));
+  const int max_ctas = std::max(1, nck / (frac * kNW));
   ctas = ctas < max_ctas ? ctas : max_ctas;
   plan->ctas = ctas < 1 ? 1 : ctas;
   plan->refresh = 1;
