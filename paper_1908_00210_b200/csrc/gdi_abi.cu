@@ -954,13 +954,17 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   // chains per rank as for one replica on one device; chunks per rank shrink by W
   if (part_plan(g->st, g->wkind, 1, 4 * p->a_num, p->b_num, &s->plan))
     return fail(GDI_ERR_CAPACITY, "decision arithmetic exceeds the 32-bit kernel bound");
-  const int nck = (g->st.n + 31) / 32;
-  int ctas = s->plan.ctas;
-  const int max_ctas = nck / world / 64;  // >= 2 chunks per chain
-  ctas = ctas < max_ctas ? ctas : max_ctas;
-  const int per_cta = s->plan.chains / (s->plan.ctas > 0 ? s->plan.ctas : 1);  // chains per CTA
-  s->plan.ctas = ctas < 1 ? 1 : ctas;
-  s->plan.chains = s->plan.ctas * per_cta;
+  // the in-flight bound is global: W ranks share the one device's chain count
+  {
+    const int refresher = s->plan.refresh != 0 ? 1 : 0, cmax = 32 - refresher;
+    const int want = std::max(1, s->plan.chains / world);
+    const int ctas = std::max(1, std::min(148, (want + cmax - 1) / cmax));
+    const int cw = std::max(1, std::min(cmax, (want + ctas - 1) / ctas));
+    s->plan.ctas = ctas;
+    s->plan.chains = ctas * cw;
+    s->plan.warps = cw + refresher;
+    s->plan.block = 32 * s->plan.warps;
+  }
   if ((rc = ensure_part(s->g))) return rc;
   schedule(s->p, s->pf, s->thr, s->tmask);
   const size_t n = g->st.n, S = p->sweeps;

@@ -249,8 +249,8 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
 // a multiple of 4 (16-byte aligned bulk copies).
 struct Slice {
   int lo, bytes;
-  __device__ Slice(int nwp, int warp) {
-    const int S = ((nwp + kNW - 1) / kNW + 3) & ~3;
+  __device__ Slice(int nwp, int warp, int nwarps) {
+    const int S = ((nwp + nwarps - 1) / nwarps + 3) & ~3;
     lo = warp * S;
     const int hi = lo + S < nwp ? lo + S : nwp;
     bytes = hi > lo ? 4 * (hi - lo) : 0;
@@ -334,12 +334,13 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
   // refresh: the last warp is not a chain but keeps re-copying the whole spin
   // copy (one bulk copy after another) until the chains are done
   const bool rmode = SM && a.refresh != 0;
-  const int CW = rmode ? kNW - 1 : kNW;  // chains per CTA
+  const int NW = blockDim.x >> 5;       // warps per CTA (<= kNW; part_plan)
+  const int CW = rmode ? NW - 1 : NW;   // chains per CTA
   const bool is_chain = warp < CW;
   const int J = a.chain0 + (blockIdx.x * CW + warp) * a.chain_stride, P = a.world_chains;
   const int n = a.g.n, nck = (n + 31) >> 5, T = a.tail, nmain = nck - T;
   const int K = is_chain && J < nmain ? (nmain - J + P - 1) / P : 0;
-  const int D = a.cta_tail;             // chains (warps 0..D-1) deferring their last chunk
+  const int D = min(a.cta_tail, CW);    // chains (warps 0..D-1) deferring their last chunk
   const int Km = warp < D ? K - 1 : K;  // chunks decided by the chain itself
   uint32_t* gb = a.bits + static_cast<size_t>(r) * a.nwp;
   const int sweep = a.sweep;
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
   const int W = a.world;
   uint32_t* send_words = (a.send != nullptr && a.npeer == 0) ? reinterpret_cast<uint32_t*>(a.send + 8) : nullptr;
 
-  const Slice slice(a.nwp, warp);
+  const Slice slice(a.nwp, warp, NW);
   Refresher rf{&mbar[warp], 0u, false};
   if (SM) {  // the whole copy: every warp its slice
     if (lane == 0) {
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
   }
   __syncthreads();
   if (warp == 0) {
-    int sh = red_share[lane], dl = red_delta[lane];
+    int sh = lane < NW ? red_share[lane] : 0, dl = lane < NW ? red_delta[lane] : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       sh += __shfl_xor_sync(FULL, sh, o);
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
     if (unfused) {
       for (int wi = threadIdx.x; wi < a.nwp; wi += blockDim.x) sw[wi] = mword(wi);
     } else {
-      const Slice sl(a.nwp, warp);
+      const Slice sl(a.nwp, warp, kNW);
       Refresher rf{&mbar[warp], 0u, false};
       if (lane == 0) {
         mbar_init(&mbar[warp]);
@@ -738,10 +739,11 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const double mean_deg = 2.0 * static_cast<double>(st.m) / st.n;
   const int groups = static_cast<int>((mean_deg + 3.999) / 4);
   const int kmax = groups <= 1 ? 1 : groups <= 2 ? 2 : 4;
-  // one CTA of 32 warps per SM, spread over the replicas
+  // one CTA per SM, spread over the replicas, with as many chain warps as
+  // the in-flight bound below allows (all SMs busy: M1 keeps 3125 chains on
+  // 148 SMs, 21 per CTA, rather than 31 per CTA on 100 SMs)
   const int nck = (st.n + 31) / 32;
   const int R = replicas > 0 ? replicas : 1;
-  int ctas = 148 / R;
   // at most a tenth of the graph in flight (chains x 32 <= n / 10): the cut
   // grows with the fraction of vertices decided concurrently, not with the
   // spin copy's staleness (M1, 20 sweeps, 6 seeds: 1/2 -> +1.6% over the
@@ -750,18 +752,15 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   // 1/2, +0.5% at 1/8)
   int frac = 10;
   if (const char* e = std::getenv("GDI_K4_FRAC")) frac = std::max(1, std::atoi(e));
-  const int max_ctas = std::max(1, nck / (frac * kNW));
-  ctas = ctas < max_ctas ? ctas : max_ctas;
-  plan->ctas = ctas < 1 ? 1 : ctas;
+  const int want = std::max(1, std::min(nck / frac, nck / 2));  // chains per replica (>= 2 chunks each)
   plan->refresh = 1;
   if (const char* e = std::getenv("GDI_K4_REFRESH")) plan->refresh = std::atoi(e);
   plan->fresh = 0;
   if (const char* e = std::getenv("GDI_K4_FRESH")) plan->fresh = std::atoi(e);
-  plan->chains = plan->ctas * (plan->refresh != 0 ? kNW - 1 : kNW);
-  // global tail: 16 chunks (32 when partitioned over ranks: every rank's
+  // global tail: 8 chunks (32 when partitioned over ranks: every rank's
   // residuals add up), and 4 deferred chunks per CTA (decided in order by one
   // warp while the CTA's other warps wait)
-  plan->tail = nck / 8 < 16 ? nck / 8 : 16;
+  plan->tail = nck / 8 < 8 ? nck / 8 : 8;
   plan->tail_multi = nck / 8 < kTailMax ? nck / 8 : kTailMax;
   plan->cta_tail = 4;
   if (const char* e = std::getenv("GDI_K4_TAIL")) {  // tuning experiments
@@ -777,21 +776,26 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->smem_copy = plan->smem <= 200 * 1024;
   if (!plan->smem_copy) {
     plan->smem = 0;
-    if (plan->refresh != 0) {  // (no copy to refresh: every warp is a chain)
-      plan->refresh = 0;
-      plan->chains = plan->ctas * kNW;
-    }
+    plan->refresh = 0;  // (no copy to refresh: every warp is a chain)
   }
+  const int cmax = plan->refresh != 0 ? kNW - 1 : kNW;  // chain warps per CTA
+  int ctas = std::min(std::max(1, 148 / R), (want + cmax - 1) / cmax);
+  ctas = std::max(1, ctas);
+  const int cw = std::max(1, std::min(cmax, (want + ctas - 1) / ctas));
+  plan->ctas = ctas;
+  plan->chains = ctas * cw;
+  plan->warps = cw + (plan->refresh != 0 ? 1 : 0);
   if (wkind == 0)
     pick<0>(kmax, plan->smem_copy, plan);
   else if (wkind == 1)
     pick<1>(kmax, plan->smem_copy, plan);
   else
     pick<2>(kmax, plan->smem_copy, plan);
-  plan->block = 32 * kNW;
+  plan->block = 32 * plan->warps;
   // finishing CTAs: one per SM with the shared copy (each copies the words),
   // else up to two per SM
   const int fg = (nck + kNW - 1) / kNW, fmax = ((plan->smem_copy ? 148 : 296) + R - 1) / R;
+  plan->fin_block = 32 * kNW;
   plan->fin_grid = fg < fmax ? fg : fmax;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
@@ -848,7 +852,7 @@ cudaError_t part_finish_launch(const PartPlan& plan, const PartArgs& args, int s
   a.sweep = sweep;
   const unsigned char* rv = static_cast<const unsigned char*>(recv);
   void* p[] = {&a, &rv, &stride, &spins_out};
-  return cudaLaunchKernel(plan.finish_fn, dim3(plan.fin_grid, a.replicas), dim3(plan.block), p, plan.smem, stream);
+  return cudaLaunchKernel(plan.finish_fn, dim3(plan.fin_grid, a.replicas), dim3(plan.fin_block), p, plan.smem, stream);
 }
 
 long long part_exchange_bytes(int n, int world, bool peer) {

@@ -105,7 +105,9 @@ struct PartPlan {
   int tail = 0;        // global tail chunks (exact counter) per sweep, one device
   int tail_multi = 0;  // the same when the graph is partitioned over ranks
   int cta_tail = 4;    // chains per CTA deferring their last chunk to the CTA tail
-  int block = 1024;
+  int block = 1024;    // sweep CTA: 32 x warps threads
+  int warps = 32;      // sweep CTA warps: chains + the refresher
+  int fin_block = 1024;
   int fin_grid = 1;    // finishing CTAs per replica
   int nwp = 0;         // spin words per replica (part_words)
   int smem = 0;        // dynamic shared memory of the sweep kernel (the spin copy)
