@@ -108,7 +108,7 @@ __device__ __forceinline__ void load_row(const PartArgs& a, const uint32_t* gb, 
     }
   const int p = c * 32 + lane;
   r.v = p < a.g.n ? __ldg(a.order + p) : 0;
-  if (WK != 2) r.deg = p < a.g.n ? __ldg(a.pdeg + p) : 0;
+  r.deg = p < a.g.n ? __ldg(a.pdeg + p) : 0;
   r.word = __ldcg(gb + c);
 }
 
@@ -124,22 +124,39 @@ __device__ __forceinline__ int term(int x, int w, Word word) {
   return static_cast<int>((sh ^ (static_cast<unsigned>(x) >> 31)) & 1u);
 }
 
+constexpr int kLaneRows = 8;  // groups beyond the bucket walked lane per vertex; longer: warp per vertex
+
+// Row entries beyond the register bucket. A chunk's rows are padded to its
+// longest, so when one is far longer than the rest (a hub vertex, first in
+// the degree-binned order) every lane would walk the hub's length: then the
+// warp takes one lane's remaining row at a time instead (32 int4 groups per
+// step, coalesced within the row's SELL column, then a warp sum), north_star
+// (2)'s warp-per-vertex path for high-degree rows.
 template <int WK, int KMAX, typename Word>
-__device__ __forceinline__ int row_field(const PartArgs& a, const Row<WK, KMAX>& r, Word word, int lane) {
+__device__ __forceinline__ int long_rows(const PartArgs& a, const Row<WK, KMAX>& r, Word word, int lane) {
+  if (r.groups <= KMAX) return 0;
   int acc = 0;
-#pragma unroll
-  for (int k = 0; k < KMAX; k++)
-    if (k < r.groups) {
-      const int4 q = r.g[k];
-      const int4 w = WK == 2 ? r.w[k] : make_int4(1, 1, 1, 1);
+  if (r.groups - KMAX <= kLaneRows) {
+    for (int k = KMAX; k < r.groups; k++) {
+      const int4 q = __ldg(a.psell + r.c0 + k * 32 + lane);
+      const int4 w = WK == 2 ? __ldg(a.sell_w + r.c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
       acc += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
     }
-  for (int k = KMAX; k < r.groups; k++) {  // rows longer than the register bucket
-    const int4 q = __ldg(a.psell + r.c0 + k * 32 + lane);
-    const int4 w = WK == 2 ? __ldg(a.sell_w + r.c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
-    acc += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
+    return acc;
   }
-  return WK == 2 ? acc : 2 * acc - r.deg;
+  const int mine = max(0, (r.deg + 3) / 4 - KMAX);  // this lane's groups beyond the bucket
+  for (unsigned pend = __ballot_sync(FULL, mine > 0); pend != 0u; pend &= pend - 1u) {
+    const int l = __ffs(pend) - 1, gl = __shfl_sync(FULL, mine, l);
+    int sum = 0;
+    for (int k = KMAX + lane; k < KMAX + gl; k += 32) {
+      const int4 q = __ldg(a.psell + r.c0 + k * 32 + l);
+      const int4 w = WK == 2 ? __ldg(a.sell_w + r.c0 + k * 32 + l) : make_int4(1, 1, 1, 1);
+      sum += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
+    }
+    sum = __reduce_add_sync(FULL, sum);
+    if (lane == l) acc += sum;
+  }
+  return acc;
 }
 
 // The spin-word loads of the register bucket are issued first and consumed
@@ -179,11 +196,7 @@ __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMA
       acc += bit(q.x, w.x, wv[4 * k]) + bit(q.y, w.y, wv[4 * k + 1]) + bit(q.z, w.z, wv[4 * k + 2]) +
              bit(q.w, w.w, wv[4 * k + 3]);
     }
-  for (int k = KMAX; k < r.groups; k++) {  // rows longer than the register bucket
-    const int4 q = __ldg(a.psell + r.c0 + k * 32 + lane);
-    const int4 w = WK == 2 ? __ldg(a.sell_w + r.c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
-    acc += term<WK>(q.x, w.x, word) + term<WK>(q.y, w.y, word) + term<WK>(q.z, w.z, word) + term<WK>(q.w, w.w, word);
-  }
+  acc += long_rows<WK, KMAX>(a, r, word, lane);
   x.f = x.live ? (WK == 2 ? acc : 2 * acc - r.deg) : 0;
   return x;
 }
@@ -511,6 +524,40 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
   }
 }
 
+// This thread's share of the cut over a chunk's rows: the weights of the
+// entries q of lane l's row with keep(q, p_l) and spin(q) != spin(p_l). Rows
+// padded far beyond their own length (a hub's chunk) are walked warp per
+// vertex, as in long_rows (the partial sums are reduced by the caller).
+template <int WK, typename Keep, typename Word>
+__device__ __forceinline__ long long chunk_cut(const PartArgs& a, int c0, int groups, int p, unsigned sp, int lane,
+                                               Keep keep, Word word) {
+  long long cut = 0;
+  auto count = [&](int4 q4, int4 w4, int pp, unsigned ss) {
+    const int xs[4] = {q4.x, q4.y, q4.z, q4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int q = WK == 1 ? (xs[j] & 0x7fffffff) : xs[j];
+      if (keep(q, pp) && ((__funnelshift_r(word(q >> 5), 0u, q) & 1u) != ss))
+        cut += WK == 0 ? 1 : WK == 1 ? (xs[j] < 0 ? -1 : 1) : ws[j];
+    }
+  };
+  if (groups <= kLaneRows + 2) {
+    for (int k = 0; k < groups; k++)
+      count(__ldg(a.psell + c0 + k * 32 + lane),
+            WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1), p, sp);
+    return cut;
+  }
+  const int mine = p < a.g.n ? (__ldg(a.pdeg + p) + 3) / 4 : 0;
+  for (unsigned pend = __ballot_sync(FULL, mine > 0); pend != 0u; pend &= pend - 1u) {
+    const int l = __ffs(pend) - 1, gl = __shfl_sync(FULL, mine, l), pl = __shfl_sync(FULL, p, l);
+    const unsigned sl = __shfl_sync(FULL, sp, l);
+    for (int k = lane; k < gl; k += 32)
+      count(__ldg(a.psell + c0 + k * 32 + l), WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + l) : make_int4(1, 1, 1, 1),
+            pl, sl);
+  }
+  return cut;
+}
+
 // Barrier: global tail, exact cut share and spin sum, trace record, outputs.
 // recv (ranks > 1): the all-gathered send buffers, rstride bytes apart.
 // SM: the spin words are copied into shared memory first (bulk copies; in the
@@ -597,17 +644,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
       const int p = c * 32 + lane;
       const unsigned sp = (pre(c) >> lane) & 1u;
       const int c0 = __ldg(a.sell_off + c), groups = (__ldg(a.sell_off + c + 1) - c0) >> 5;
-      for (int k = 0; k < groups; k++) {
-        const int4 q4 = __ldg(a.psell + c0 + k * 32 + lane);
-        const int4 w4 = WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
-        const int xs[4] = {q4.x, q4.y, q4.z, q4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int q = WK == 1 ? (xs[j] & 0x7fffffff) : xs[j];
-          if (q > p && q < tlo && ((__funnelshift_r(pre(q >> 5), 0u, q) & 1u) != sp))
-            cut += WK == 0 ? 1 : WK == 1 ? (xs[j] < 0 ? -1 : 1) : ws[j];
-        }
-      }
+      cut += chunk_cut<WK>(a, c0, groups, p, sp, lane, [tlo](int q, int pp) { return q > pp && q < tlo; }, pre);
     }
   }
   __syncthreads();
@@ -620,17 +657,8 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
       const int c = nmain + t, p = c * 32 + lane;
       const unsigned sp = (tw[t] >> lane) & 1u;
       const int c0 = __ldg(a.sell_off + c), groups = (__ldg(a.sell_off + c + 1) - c0) >> 5;
-      for (int k = 0; k < groups; k++) {
-        const int4 q4 = __ldg(a.psell + c0 + k * 32 + lane);
-        const int4 w4 = WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1);
-        const int xs[4] = {q4.x, q4.y, q4.z, q4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int q = WK == 1 ? (xs[j] & 0x7fffffff) : xs[j];
-          if ((q < tlo || (q > p && q != zpos)) && ((__funnelshift_r(word(q >> 5), 0u, q) & 1u) != sp))
-            cut += WK == 0 ? 1 : WK == 1 ? (xs[j] < 0 ? -1 : 1) : ws[j];
-        }
-      }
+      cut += chunk_cut<WK>(
+          a, c0, groups, p, sp, lane, [tlo, zpos](int q, int pp) { return q < tlo || (q > pp && q != zpos); }, word);
     }
   // 3. the spin sum (global, on every rank), the unfused exchange's copy of the
   // other ranks' words for the next sweep, and the natural-order outputs
