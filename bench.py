@@ -343,7 +343,12 @@ def spawn_ranks(nproc: int) -> int:
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
            *sys.argv[1:]]
-    return subprocess.call(cmd)
+    # NCCL's init lines on stderr (one per rank: the ranks can be counted from
+    # the log); the JSON line stays alone on stdout
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def cpu_model() -> str:
