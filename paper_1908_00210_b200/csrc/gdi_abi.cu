@@ -958,7 +958,7 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   {
     const int refresher = s->plan.refresh != 0 ? 1 : 0, cmax = 32 - refresher;
     const int want = std::max(1, s->plan.chains / world);
-    const int ctas = std::max(1, std::min(148, (want + cmax - 1) / cmax));
+    const int ctas = std::max(1, std::min(148, want));
     const int cw = std::max(1, std::min(cmax, (want + ctas - 1) / ctas));
     s->plan.ctas = ctas;
     s->plan.chains = ctas * cw;

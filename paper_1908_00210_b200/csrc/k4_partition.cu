@@ -250,6 +250,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// The whole copy as `parts` bulk copies in flight on one barrier (one
+// expect_tx for all of them); bytes a multiple of 16 * parts.
+__device__ __forceinline__ void bulk_copy_parts(void* dst, const void* src, unsigned bytes, uint64_t* mb, int parts) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(mb)), "r"(bytes) : "memory");
+  const unsigned part = bytes / parts;
+  for (int i = 0; i < parts; i++)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     saddr(static_cast<char*>(dst) + i * part)),
+                 "l"(static_cast<const char*>(src) + i * part), "r"(part), "r"(saddr(mb))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(mb)), "r"(bytes) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     if (lane == 0) {  // (rf: this warp's barrier, its phase past the initial copy)
       int rounds = 0;
       while (*static_cast<volatile int*>(&chains_done) < CW) {
-        bulk_copy(sb, gb, a.nwp * 4, rf.mb);
+        bulk_copy_parts(sb, gb, a.nwp * 4, rf.mb, a.nwp % 32 == 0 ? a.copy_parts : 1);
         mbar_wait(rf.mb, rf.phase);
         rf.phase ^= 1u;
         rounds++;
@@ -749,7 +760,7 @@ void pick(int kmax, bool sm, PartPlan* plan) {
 
 }  // namespace
 
-int part_words(int n) { return (((n + 31) / 32 + 1) + 3) & ~3; }
+int part_words(int n) { return (((n + 31) / 32 + 1) + 31) & ~31; }  // (a multiple of 32 words: 8 equal 16-byte-aligned copy parts)
 
 int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan) {
   long long x = a4 < 0 ? -a4 : a4, y = b < 0 ? -b : b;
@@ -772,13 +783,14 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   // 148 SMs, 21 per CTA, rather than 31 per CTA on 100 SMs)
   const int nck = (st.n + 31) / 32;
   const int R = replicas > 0 ? replicas : 1;
-  // at most a tenth of the graph in flight (chains x 32 <= n / 10): the cut
-  // grows with the fraction of vertices decided concurrently, not with the
-  // spin copy's staleness (M1, 20 sweeps, 6 seeds: 1/2 -> +1.6% over the
-  // sequential cut in 1.17 ms, 1/8 -> +0.9% in 1.25 ms, 1/10 -> +0.6% in
-  // 1.34 ms, 1/12 -> +0.3% in 1.49 ms; a 100k-vertex hub graph +4.9% at
-  // 1/2, +0.5% at 1/8)
-  int frac = 10;
+  // at most 1/14 of the graph in flight (chains x 32 <= n / 14): the cut
+  // grows with the fraction of vertices decided concurrently more than with
+  // the spin copy's staleness (M1, 20 sweeps, 6 seeds, chains spread over all
+  // SMs: 1/8 -> +1.4% over the sequential cut in 1.17 ms, 1/10 -> +1.05% in
+  // 1.19 ms, 1/12 -> +0.86% in 1.20 ms, 1/14 -> +0.72% in 1.26 ms; with 31
+  // chains per CTA on fewer SMs 1/10 gave +0.7% in 1.28-1.34 ms; a 100k-vertex
+  // hub graph +4.9% at 1/2, +0.5% at 1/8)
+  int frac = 14;
   if (const char* e = std::getenv("GDI_K4_FRAC")) frac = std::max(1, std::atoi(e));
   const int want = std::max(1, std::min(nck / frac, nck / 2));  // chains per replica (>= 2 chunks each)
   plan->refresh = 1;
@@ -807,8 +819,7 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
     plan->refresh = 0;  // (no copy to refresh: every warp is a chain)
   }
   const int cmax = plan->refresh != 0 ? kNW - 1 : kNW;  // chain warps per CTA
-  int ctas = std::min(std::max(1, 148 / R), (want + cmax - 1) / cmax);
-  ctas = std::max(1, ctas);
+  const int ctas = std::max(1, std::min(148 / R, want));  // every SM, fewer chain warps each
   const int cw = std::max(1, std::min(cmax, (want + ctas - 1) / ctas));
   plan->ctas = ctas;
   plan->chains = ctas * cw;
@@ -847,6 +858,8 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   a.cta_tail = plan.cta_tail;
   a.nwp = plan.nwp;
   a.refresh = plan.refresh;
+  a.copy_parts = 1;
+  if (const char* e = std::getenv("GDI_K4_PARTS")) a.copy_parts = std::max(1, std::min(8, std::atoi(e)));
   const char* dbg = std::getenv("GDI_K4_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
   return a;

@@ -159,6 +159,7 @@ struct PartArgs {
   int32_t tail;                    // last chunks of the order, decided against the exact counter
   int32_t cta_tail;                // chains per CTA deferring their last chunk to the CTA tail
   int32_t refresh;                 // 1: the last warp of a CTA re-copies its shared spin copy (0: never)
+  int32_t copy_parts;              // bulk copies in flight per refresh
   int32_t debug;                   // timing experiments only (GDI_K4_DEBUG); 0 in production
   DevTrace* trace;
   unsigned long long* stamps;

@@ -138,8 +138,8 @@ def test_k4_m1_million_vertices_quality_and_balance():
     """BASELINE configs[4]: 1M vertices, one replica, 20 sweeps. The exact
     mode / reference deterministic run gives cut 1252631 (golden); the
     reference's own pooled mode gives 1.278M (4 workers) to 1.342M (16) on
-    this graph. K4 keeps at most a tenth of the graph in flight: measured
-    +0.4% to +0.7% over 6 seeds. Tolerance: cut within 1% of the
+    this graph. K4 keeps at most 1/14 of the graph in flight: measured
+    +0.6% to +0.9% over 6 seeds. Tolerance: cut within 1% of the
     deterministic cut, imbalance at most 2, counter == spin sum at every
     barrier."""
     _k4_m1(1.01)
