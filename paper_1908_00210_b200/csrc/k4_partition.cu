@@ -797,16 +797,9 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   if (const char* e = std::getenv("GDI_K4_REFRESH")) plan->refresh = std::atoi(e);
   plan->fresh = 0;
   if (const char* e = std::getenv("GDI_K4_FRESH")) plan->fresh = std::atoi(e);
-  // global tail: 8 chunks (32 when partitioned over ranks: every rank's
-  // residuals add up), and 4 deferred chunks per CTA (decided in order by one
-  // warp while the CTA's other warps wait)
-  plan->tail = nck / 8 < 8 ? nck / 8 : 8;
-  plan->tail_multi = nck / 8 < kTailMax ? nck / 8 : kTailMax;
+  // 4 deferred chunks per CTA (decided in order by one warp while the CTA's
+  // other warps wait); the global tail is sized below
   plan->cta_tail = 4;
-  if (const char* e = std::getenv("GDI_K4_TAIL")) {  // tuning experiments
-    const int t = std::atoi(e);
-    plan->tail = plan->tail_multi = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
-  }
   if (const char* e = std::getenv("GDI_K4_CTA_TAIL")) {
     const int t = std::atoi(e);
     plan->cta_tail = t < 0 ? 0 : t > kNW ? kNW : t;
@@ -823,6 +816,18 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   const int cw = std::max(1, std::min(cmax, (want + ctas - 1) / ctas));
   plan->ctas = ctas;
   plan->chains = ctas * cw;
+  // global tail: 8 chunks when every CTA defers 4 chunks to its own tail; 16
+  // when the CTAs hold fewer chains (shallower CTA tails leave more residual:
+  // 100k-vertex graph, 2 chains per CTA, 30 sweeps: imbalance 4-8 in 2 of 36
+  // runs with 8, 0-2 in all with 16, as the reference's own pooled mode);
+  // 32 when partitioned over ranks (every rank's residuals add up)
+  const int t1 = cw < 4 ? 16 : 8;
+  plan->tail = nck / 8 < t1 ? nck / 8 : t1;
+  plan->tail_multi = nck / 8 < kTailMax ? nck / 8 : kTailMax;
+  if (const char* e = std::getenv("GDI_K4_TAIL")) {  // tuning experiments
+    const int t = std::atoi(e);
+    plan->tail = plan->tail_multi = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
+  }
   plan->warps = cw + (plan->refresh != 0 ? 1 : 0);
   if (wkind == 0)
     pick<0>(kmax, plan->smem_copy, plan);

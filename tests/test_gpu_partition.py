@@ -168,4 +168,4 @@ def test_partitioned_anneal_nccl_cuda_graph():
     graphed, err, cuts, ev, imb, ctr_ok = q.get(timeout=600)
     p.join(timeout=120)
     assert graphed, err
-    assert cuts == ev and all(i <= 2 for i in imb) and all(ctr_ok)
+    assert cuts == ev and all(i <= 2 for i in imb) and all(ctr_ok), (cuts, ev, imb, ctr_ok)
