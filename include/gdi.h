@@ -155,6 +155,15 @@ int gdi_anneal_batch_columns(const gdi_graph* g, const gdi_params* p, const uint
 int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,
                        int64_t b_num, int64_t denom, gdi_score* scores);
 
+/* The same on device-resident spins [R][n] (int8, device pointer), enqueued
+ * on `stream` (a cudaStream_t; NULL = legacy stream) without synchronising:
+ * d_cut_sum[2r] = cut, d_cut_sum[2r+1] = spin sum (device int64 [R][2]);
+ * *d_bad (device uint32, may be NULL) becomes nonzero when a spin byte is
+ * neither +1 nor -1. H = a*sum^2 + b*cut as in evaluate.cpp:25-32. The first
+ * call on a graph builds its edge list (synchronous). */
+int gdi_evaluate_device(const gdi_graph* g, const int8_t* d_spins, int32_t replicas, int64_t* d_cut_sum,
+                        uint32_t* d_bad, void* stream);
+
 /* Session API: keeps inputs and outputs resident in HBM between launches so
  * a caller can time the kernels alone. `stream` is a cudaStream_t (NULL: the
  * session creates its own). launch() is asynchronous on that stream. */

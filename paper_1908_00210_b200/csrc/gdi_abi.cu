@@ -91,18 +91,19 @@ struct gdi_graph {
   int wkind = 0;  // 0 unit, 1 +-1 (sign bit), 2 general
   // kernel layouts, built on the device the first time a session needs one
   std::mutex mu;
-  bool thru_built = false, pipe_built = false, part_built = false;
+  bool thru_built = false, pipe_built = false, part_built = false, eval_built = false;
   ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
   DevBuf psell, pdeg;  // K4: the SELL rows over visit-order positions, degree by position
   PipeLayout pipel;  // k1_window: window masks, forward masks, SELL rows
   PipeGraph pipe;    // k1_window view (ok = eligible; pointers once built)
+  EvalLayout evl;    // K3: canonical edge list
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
                                 thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes +
                                 pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
-                                pipel.wsell_off.bytes);
+                                pipel.wsell_off.bytes + evl.edges.bytes + evl.w.bytes);
   }
 };
 
@@ -206,6 +207,19 @@ int ensure_part(gdi_graph* g) {
   cudaStreamDestroy(st);
   GDI_CUDA(e);
   g->part_built = true;
+  return GDI_OK;
+}
+
+// K3 edge list
+int ensure_eval(gdi_graph* g) {
+  std::lock_guard<std::mutex> lock(g->mu);
+  if (g->eval_built) return GDI_OK;
+  cudaStream_t st = nullptr;
+  GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const cudaError_t e = build_eval_layout(g->csr(), g->st.m, g->wkind, &g->evl, st);
+  cudaStreamDestroy(st);
+  GDI_CUDA(e);
+  g->eval_built = true;
   return GDI_OK;
 }
 
@@ -879,6 +893,53 @@ int gdi_anneal_batch_columns(const gdi_graph* g, const gdi_params* p, const uint
   return rc;
 }
 
+// K3 on device-resident spins: scratch + {cut, spin sum} + bad flag in one
+// pool allocation, results into d_out (cut, sum) per replica. Asynchronous on
+// `st` when the graph's edge list is already built.
+namespace {
+struct EvalScratch {
+  DevBuf buf;
+  size_t out_off = 0, bad_off = 0, work_off = 0;
+};
+int eval_enqueue(gdi_graph* g, const int8_t* d_spins, int32_t R, EvalScratch& sc, cudaStream_t st, int* launches) {
+  int rc = ensure_eval(g);
+  if (rc) return rc;
+  const long long ww = eval_work_words(g->st.n, R, g->wkind);
+  sc.out_off = 0;
+  sc.bad_off = static_cast<size_t>(R) * 16;
+  sc.work_off = (sc.bad_off + 4 + 15) & ~static_cast<size_t>(15);
+  const size_t bytes = sc.work_off + static_cast<size_t>(ww) * 4;
+  if (sc.buf.bytes < bytes) GDI_CUDA(sc.buf.alloc(bytes));
+  char* base = sc.buf.as<char>();
+  GDI_CUDA(cudaMemsetAsync(base, 0, sc.work_off, st));
+  EvalArgs a{};
+  a.n = g->st.n;
+  a.m = g->evl.m;
+  a.mpos = g->evl.mpos;
+  a.narrow = g->evl.narrow;
+  a.edges = g->evl.edges.p;
+  a.w = g->evl.w.as<int32_t>();
+  a.spins = d_spins;
+  a.R = R;
+  a.work = reinterpret_cast<uint32_t*>(base + sc.work_off);
+  a.out = reinterpret_cast<unsigned long long*>(base + sc.out_off);
+  a.bad = reinterpret_cast<unsigned*>(base + sc.bad_off);
+  GDI_CUDA(eval_launch(a, g->wkind, st, launches));
+  return GDI_OK;
+}
+void eval_scores(const long long* res, int32_t R, int64_t a_num, int64_t b_num, int64_t denom,
+                 gdi_score* scores) {
+  for (int32_t r = 0; r < R; r++) {
+    const long long cut = res[2 * r], sum = res[2 * r + 1];
+    scores[r].cut = cut;
+    scores[r].imbalance = sum < 0 ? -sum : sum;
+    scores[r].hamiltonian_scaled = a_num * sum * sum + b_num * cut;
+    scores[r].hamiltonian = static_cast<double>(scores[r].hamiltonian_scaled) / static_cast<double>(denom);
+    scores[r].balance_counter = sum;
+  }
+}
+}  // namespace
+
 int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas, int64_t a_num,
                        int64_t b_num, int64_t denom, gdi_score* scores) {
   NvtxRange nvtx_range("gdi_evaluate_batch");
@@ -888,25 +949,40 @@ int gdi_evaluate_batch(const gdi_graph* g, const int8_t* spins, int32_t replicas
   int rc = use_device(g->device);
   if (rc) return rc;
   const size_t R = replicas, n = g->st.n;
-  for (size_t i = 0; i < R * n; i++)
-    if (spins[i] != 1 && spins[i] != -1) return fail(GDI_ERR_DOMAIN, "spin must be -1 or +1");
-  DevBuf d_s, d_out;
+  DevBuf d_s;
+  EvalScratch sc;
   GDI_CUDA(d_s.alloc(R * n));
-  GDI_CUDA(d_out.alloc(R * 2 * sizeof(unsigned long long)));
   GDI_CUDA(cudaMemcpy(d_s.p, spins, R * n, cudaMemcpyHostToDevice));
-  GDI_CUDA(cudaMemset(d_out.p, 0, d_out.bytes));
-  EvalArgs a{g->csr(), d_s.as<int8_t>(), replicas, d_out.as<unsigned long long>()};
-  GDI_CUDA(eval_launch(a, !g->st.unit, nullptr));
-  std::vector<long long> res(R * 2);
-  GDI_CUDA(cudaMemcpy(res.data(), d_out.p, res.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-  for (size_t r = 0; r < R; r++) {
-    const long long cut = res[2 * r], sum = res[2 * r + 1];
-    scores[r].cut = cut;
-    scores[r].imbalance = sum < 0 ? -sum : sum;
-    scores[r].hamiltonian_scaled = a_num * sum * sum + b_num * cut;
-    scores[r].hamiltonian = static_cast<double>(scores[r].hamiltonian_scaled) / static_cast<double>(denom);
-    scores[r].balance_counter = sum;
+  if ((rc = eval_enqueue(const_cast<gdi_graph*>(g), d_s.as<int8_t>(), replicas, sc, nullptr, nullptr))) return rc;
+  std::vector<long long> res(R * 2 + 2);
+  GDI_CUDA(cudaMemcpy(res.data(), sc.buf.p, sc.bad_off + 4, cudaMemcpyDeviceToHost));
+  unsigned bad = 0;
+  std::memcpy(&bad, reinterpret_cast<const char*>(res.data()) + sc.bad_off, 4);
+  if (bad) return fail(GDI_ERR_DOMAIN, "spin must be -1 or +1");
+  eval_scores(res.data(), replicas, a_num, b_num, denom, scores);
+  return GDI_OK;
+}
+
+int gdi_evaluate_device(const gdi_graph* g, const int8_t* d_spins, int32_t replicas, int64_t* d_cut_sum,
+                        uint32_t* d_bad, void* stream) {
+  if (!g || !d_spins || !d_cut_sum) return fail(GDI_ERR_CONFIG, "NULL argument");
+  if (replicas < 1) return fail(GDI_ERR_CONFIG, "replicas must be >= 1");
+  int rc = use_device(g->device);
+  if (rc) return rc;
+  gdi_graph* gm = const_cast<gdi_graph*>(g);
+  if ((rc = ensure_eval(gm))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // per-thread scratch kept between calls (the bench times back-to-back calls)
+  thread_local EvalScratch sc;
+  thread_local int sc_dev = -1;
+  if (sc_dev != g->device) {
+    sc.buf.reset();
+    sc_dev = g->device;
   }
+  int launches = 0;
+  if ((rc = eval_enqueue(gm, d_spins, replicas, sc, st, &launches))) return rc;
+  GDI_CUDA(cudaMemcpyAsync(d_cut_sum, sc.buf.p, static_cast<size_t>(replicas) * 16, cudaMemcpyDeviceToDevice, st));
+  if (d_bad) GDI_CUDA(cudaMemcpyAsync(d_bad, sc.buf.as<char>() + sc.bad_off, 4, cudaMemcpyDeviceToDevice, st));
   return GDI_OK;
 }
 

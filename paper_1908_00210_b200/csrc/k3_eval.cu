@@ -1,15 +1,34 @@
-// K3 — fused exact partition evaluation (sm_100a).
+// K3 — fused exact partition evaluation (sm_100a): cut and spin sum of R spin
+// vectors, the reference's cut_value / imbalance / score (proj/src/evaluate.cpp:
+// 10-32; the same cut as record_barrier's cut_of, anneal.cpp:64-70).
+// H_scaled = a * sum^2 + b * cut is formed on the host from the two integers.
 //
-// One pass over the CSR per replica computes the exact cut (each edge once,
-// u < v, reference proj/src/evaluate.cpp:10-18 and anneal.cpp:64-70) and the
-// spin sum (evaluate.cpp:20-23) together; H_scaled = a*sum^2 + b*cut is
-// formed on the host from the two integers (evaluate.cpp:25-32).
+// Input: int8 spins [R][n] in HBM (+1 / -1; any other byte sets the `bad`
+// flag, the reference's "spin must be -1 or +1" domain error). The graph is
+// the canonical edge list (u < v, build_eval_layout): one word u | v << 16
+// per edge when n <= 65536, else int2; +1 edges first for +-1 weights.
 //
-// Layout: grid.y = replica, grid.x = vertex chunks of that replica. A thread
-// owns one vertex: it reads its own spin once, walks its adjacency row and
-// compares against the neighbour spins (L1/L2 resident for every config in
-// BASELINE.json). Partial sums are reduced warp -> block with shuffles and
-// shared memory, then one 64-bit atomic per block and quantity.
+// Two kernels, by shape:
+//
+// k3_sliced (many replicas, |w| == 1, n small enough for 4n bytes of shared
+// memory): bit-sliced over 32 replicas. A CTA takes a group of 32 replicas
+// and a slice of the edges. It first transposes the group's spins into
+// shared memory, one 32-bit word per vertex (bit r = replica 32g + r is +1):
+// lane r reads 32 consecutive spin bytes of its replica, 32 ballots turn
+// them into the 32 vertex words. Then every edge costs one coalesced load
+// and two shared-memory loads for all 32 replicas: x = T[u] ^ T[v] is the
+// mask of replicas that cut the edge, summed per bit position by a
+// carry-save (Harley-Seal) adder tree into bit-sliced counters. At the end
+// a 32 x 32 bit transpose per counter level (warp shuffles) and a popcount
+// give each lane its replica's count. ~14 instructions per edge for 32
+// replicas instead of ~6 per edge per replica.
+//
+// k3_pack + k3_bits (one or few replicas, large graphs such as the
+// 1M-vertex config, or general weights): k3_pack packs each replica's spins
+// into bit words (+ spin sum); k3_bits copies one replica's words into
+// shared memory (125 KB for 1M vertices) and streams the edges: one
+// coalesced 8-byte load and two shared-memory bit lookups per edge, so the
+// kernel is bound by the edge stream (8 B per edge from HBM / L2).
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -19,61 +38,323 @@ namespace gdi {
 
 namespace {
 
-constexpr int kEvalBlock = 256;
-constexpr int kEvalVertsPerThread = 4;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kSliceBlock = 512;
+constexpr int kBitsBlock = 512;
+constexpr int kLevels = 20;  // bit-sliced counter levels above the Harley-Seal eights: < 8 * 2^20 edges per thread
 
-template <bool WEIGHTED>
-__global__ void __launch_bounds__(kEvalBlock) k3_eval(const EvalArgs a) {
-  const int n = a.g.n;
-  const int r = blockIdx.y;
-  const int8_t* __restrict__ s = a.spins + static_cast<size_t>(r) * n;
-  long long cut = 0, sum = 0;
-  const int stride = gridDim.x * blockDim.x;
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
-    const int su = s[u];
-    sum += su;
-    const int e1 = __ldg(a.g.off + u + 1);
-    for (int e = __ldg(a.g.off + u); e < e1; e++) {
-      const int v = __ldg(a.g.col + e);
-      if (u < v && su != s[v]) cut += WEIGHTED ? __ldg(a.g.w + e) : 1;
+__device__ __forceinline__ void csa(unsigned& h, unsigned& l, unsigned a, unsigned b, unsigned c) {
+  const unsigned u = a ^ b;
+  h = (a & b) | (u & c);
+  l = u ^ c;
+}
+
+// 32 x 32 bit transpose across the warp: lane t holds row t (bit c = column
+// c) on entry, column t on exit (bit r = row r's bit t).
+__device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
+  const unsigned masks[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; s++) {
+    const int j = 16 >> s;
+    const unsigned m = masks[s];
+    const unsigned y = __shfl_xor_sync(FULL, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+// +1 mask of the four spin bytes of x (bit 7 of each byte), and whether every
+// byte is +1 (0x01) or -1 (0xff)
+__device__ __forceinline__ unsigned pos_bits(unsigned x) { return ~x & 0x80808080u; }
+__device__ __forceinline__ bool valid4(unsigned x) {
+  const unsigned s = (x >> 7) & 0x01010101u;
+  return x == ((s * 0xffu) | (s ^ 0x01010101u));
+}
+
+// Bit-sliced per-replica counter: ones/twos/fours + levels of eights.
+struct Sliced {
+  unsigned ones = 0, twos = 0, fours = 0, lv[kLevels];
+  __device__ Sliced() {
+#pragma unroll
+    for (int i = 0; i < kLevels; i++) lv[i] = 0;
+  }
+  __device__ __forceinline__ void add8(const unsigned (&x)[8]) {
+    unsigned ta, tb, fa, fb, e;
+    csa(ta, ones, ones, x[0], x[1]);
+    csa(tb, ones, ones, x[2], x[3]);
+    csa(fa, twos, twos, ta, tb);
+    csa(ta, ones, ones, x[4], x[5]);
+    csa(tb, ones, ones, x[6], x[7]);
+    csa(fb, twos, twos, ta, tb);
+    csa(e, fours, fours, fa, fb);
+#pragma unroll
+    for (int i = 0; i < kLevels; i++) {
+      const unsigned t = lv[i] & e;
+      lv[i] ^= e;
+      e = t;
     }
+  }
+  // this warp's count for replica `lane` (levels that are zero in every lane
+  // are skipped)
+  __device__ __forceinline__ long long count(int lane) const {
+    long long c = 0;
+    if (__any_sync(FULL, ones)) c += __popc(transpose32(ones, lane));
+    if (__any_sync(FULL, twos)) c += 2ll * __popc(transpose32(twos, lane));
+    if (__any_sync(FULL, fours)) c += 4ll * __popc(transpose32(fours, lane));
+#pragma unroll
+    for (int i = 0; i < kLevels; i++)
+      if (__any_sync(FULL, lv[i])) c += (8ll << i) * __popc(transpose32(lv[i], lane));
+    return c;
+  }
+};
+
+template <bool NARROW>
+__device__ __forceinline__ void edge_at(const EvalArgs& a, long long e, int& u, int& v) {
+  if (NARROW) {
+    const unsigned x = __ldg(static_cast<const unsigned*>(a.edges) + e);
+    u = static_cast<int>(x & 0xffffu);
+    v = static_cast<int>(x >> 16);
+  } else {
+    const int2 x = __ldg(static_cast<const int2*>(a.edges) + e);
+    u = x.x;
+    v = x.y;
+  }
+}
+
+// This thread's cut count over edges [lo, hi) for the 32 replicas of T.
+template <bool NARROW>
+__device__ __forceinline__ long long sliced_range(const EvalArgs& a, const unsigned* T, long long lo, long long hi,
+                                                  int lane) {
+  Sliced acc;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long e = lo + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  while (__any_sync(FULL, e < hi)) {
+    unsigned x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      x[k] = 0u;
+      const long long ek = e + k * stride;
+      if (ek < hi) {
+        int u, v;
+        edge_at<NARROW>(a, ek, u, v);
+        x[k] = T[u] ^ T[v];
+      }
+    }
+    acc.add8(x);
+    e += 8 * stride;
+  }
+  return acc.count(lane);
+}
+
+template <bool NARROW, bool SIGNED>
+__global__ void __launch_bounds__(kSliceBlock) k3_sliced(const EvalArgs a) {
+  extern __shared__ unsigned T[];
+  __shared__ long long cnt[32];
+  const int n = a.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int g = blockIdx.y, r = 32 * g + lane;
+  const bool live = r < a.R;
+  const int8_t* row = a.spins + static_cast<size_t>(live ? r : 0) * n;
+  // transpose: warp w takes the 32-vertex blocks w, w + nwarps, ...; the
+  // spin sum and the byte check are done by slice 0 only
+  long long pop = 0;
+  bool ok = true;
+  for (int v0 = 32 * warp; v0 < n; v0 += 32 * nwarps) {
+    unsigned w[8];
+    const int lim = n - v0;  // valid bytes in this block (>= 1)
+    if (a.aligned4 && lim >= 32) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) w[k] = live ? __ldg(reinterpret_cast<const unsigned*>(row + v0) + k) : 0x01010101u;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        unsigned x = 0x01010101u;  // (+1 padding: never looked up, masked from the sum)
+        for (int b = 0; b < 4; b++)
+          if (live && 4 * k + b < lim) x = (x & ~(0xffu << (8 * b))) | (static_cast<unsigned>(static_cast<uint8_t>(row[v0 + 4 * k + b])) << (8 * b));
+        w[k] = x;
+      }
+    }
+    unsigned mine = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const unsigned p = pos_bits(w[k]);
+      ok &= valid4(w[k]);
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const unsigned bal = __ballot_sync(FULL, live && ((p >> (8 * b + 7)) & 1u));
+        if (lane == 4 * k + b) mine = bal;
+      }
+      const int c = lim - 4 * k;  // bytes of word k inside the graph
+      const unsigned keep = c >= 4 ? 0x80808080u : c <= 0 ? 0u : (0x80808080u >> (8 * (4 - c)));
+      pop += __popc(p & keep);
+    }
+    if (lane < lim) T[v0 + lane] = mine;
+  }
+  if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  if (blockIdx.x == 0 && live) {
+    if (!ok) atomicOr(a.bad, 1u);
+    // the spin sum 2 * pop - n: every warp adds 2 * its blocks' pop, warp 0 also -n
+    const long long add = 2 * pop - (warp == 0 ? n : 0);
+    if (add != 0) atomicAdd(a.out + 2 * r + 1, static_cast<unsigned long long>(add));
+  }
+  // edges of this CTA's slice (grid-stride over the list), +1 then -1
+  long long c = sliced_range<NARROW>(a, T, 0, a.mpos, lane);
+  if (SIGNED) c -= sliced_range<NARROW>(a, T, a.mpos, a.m, lane);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[lane]), static_cast<unsigned long long>(c));
+  __syncthreads();
+  if (threadIdx.x < 32 && 32 * g + threadIdx.x < a.R && cnt[threadIdx.x] != 0)
+    atomicAdd(a.out + 2 * (32 * g + threadIdx.x), static_cast<unsigned long long>(cnt[threadIdx.x]));
+}
+
+// int8 spins -> bit words [R][nw] + count of +1 spins. Thread = one word of
+// one replica (32 bytes, read as 8 x 4 bytes when the rows are 4-aligned).
+__global__ void __launch_bounds__(256) k3_pack(const EvalArgs a) {
+  const int n = a.n, nw = (n + 31) >> 5, r = blockIdx.y;
+  const int8_t* row = a.spins + static_cast<size_t>(r) * n;
+  unsigned pop = 0;
+  bool ok = true;
+  for (int wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += gridDim.x * blockDim.x) {
+    const int v0 = 32 * wi, lim = n - v0;
+    unsigned bits = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      unsigned x = 0x01010101u;
+      if (a.aligned4 && lim >= 32) {
+        x = __ldcs(reinterpret_cast<const unsigned*>(row + v0) + k);
+      } else {
+        for (int b = 0; b < 4; b++)
+          if (4 * k + b < lim) x = (x & ~(0xffu << (8 * b))) | (static_cast<unsigned>(static_cast<uint8_t>(row[v0 + 4 * k + b])) << (8 * b));
+      }
+      ok &= valid4(x);
+      const unsigned p = pos_bits(x);  // bits 7, 15, 23, 31
+      const unsigned q = ((p >> 7) & 1u) | ((p >> 14) & 2u) | ((p >> 21) & 4u) | ((p >> 28) & 8u);
+      bits |= q << (4 * k);
+    }
+    if (lim < 32) bits &= (1u << lim) - 1u;
+    pop += __popc(bits);
+    a.work[static_cast<size_t>(r) * a.nwp + wi] = bits;
+  }
+  pop = __reduce_add_sync(FULL, pop);
+  ok = __all_sync(FULL, ok);
+  if ((threadIdx.x & 31) == 0) {
+    // the spin sum 2 * pop - n: every warp adds 2 * its pop, the first warp also -n
+    const long long add = 2ll * pop - (blockIdx.x == 0 && threadIdx.x == 0 ? n : 0);
+    if (add != 0) atomicAdd(a.out + 2 * r + 1, static_cast<unsigned long long>(add));
+    if (!ok) atomicOr(a.bad, 1u);
+  }
+}
+
+// One replica's cut over a slice of the edges, bit words in shared memory
+// (SM) or, for graphs whose words do not fit it, read through L1 (__ldg).
+template <bool NARROW, int WK, bool SM>
+__global__ void __launch_bounds__(kBitsBlock) k3_bits(const EvalArgs a) {
+  extern __shared__ __align__(16) unsigned S[];
+  __shared__ long long red[kBitsBlock / 32];
+  const int r = blockIdx.y, nw4 = a.nwp >> 2;
+  const unsigned* words = a.work + static_cast<size_t>(r) * a.nwp;
+  if (SM) {
+    const uint4* src = reinterpret_cast<const uint4*>(words);
+    for (int i = threadIdx.x; i < nw4; i += blockDim.x) reinterpret_cast<uint4*>(S)[i] = __ldcg(src + i);
+    __syncthreads();
+  }
+  auto bit = [&](int v) { return ((SM ? S[v >> 5] : __ldg(words + (v >> 5))) >> (v & 31)) & 1u; };
+  long long cut = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long m = a.m;
+#pragma unroll 4
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+    int u, v;
+    edge_at<NARROW>(a, e, u, v);
+    const bool c = bit(u) != bit(v);
+    if (WK == 0) cut += c;
+    if (WK == 1) cut += c ? (e < a.mpos ? 1 : -1) : 0;
+    if (WK == 2) cut += c ? __ldg(a.w + e) : 0;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    cut += __shfl_xor_sync(0xffffffffu, cut, o);
-    sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  }
-  __shared__ long long red[2][kEvalBlock / 32];
-  const int warp = threadIdx.x / 32;
-  if ((threadIdx.x & 31) == 0) {
-    red[0][warp] = cut;
-    red[1][warp] = sum;
-  }
+  for (int o = 16; o > 0; o >>= 1) cut += __shfl_xor_sync(FULL, cut, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cut;
   __syncthreads();
   if (threadIdx.x == 0) {
-    long long c = 0, t = 0;
-    for (int w = 0; w < kEvalBlock / 32; w++) {
-      c += red[0][w];
-      t += red[1][w];
-    }
-    atomicAdd(a.out + 2 * r, static_cast<unsigned long long>(c));
-    atomicAdd(a.out + 2 * r + 1, static_cast<unsigned long long>(t));
+    long long t = 0;
+    for (int w = 0; w < kBitsBlock / 32; w++) t += red[w];
+    if (t != 0) atomicAdd(a.out + 2 * r, static_cast<unsigned long long>(t));
   }
+}
+
+template <bool NARROW, bool SM>
+const void* bits_fn(int wkind) {
+  return wkind == 0   ? reinterpret_cast<const void*>(&k3_bits<NARROW, 0, SM>)
+         : wkind == 1 ? reinterpret_cast<const void*>(&k3_bits<NARROW, 1, SM>)
+                      : reinterpret_cast<const void*>(&k3_bits<NARROW, 2, SM>);
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
 }
 
 }  // namespace
 
-cudaError_t eval_launch(const EvalArgs& args, bool weighted, cudaStream_t stream) {
-  const int per_block = kEvalBlock * kEvalVertsPerThread;
-  int chunks = (args.g.n + per_block - 1) / per_block;
-  if (chunks < 1) chunks = 1;
-  if (chunks > 4096) chunks = 4096;
-  dim3 grid(chunks, args.replicas);
-  if (weighted)
-    k3_eval<true><<<grid, kEvalBlock, 0, stream>>>(args);
-  else
-    k3_eval<false><<<grid, kEvalBlock, 0, stream>>>(args);
-  return cudaGetLastError();
+bool eval_sliced(int n, int replicas, int wkind) {
+  return wkind != 2 && replicas >= 16 && static_cast<long long>(n) * 4 <= 200 * 1024;
+}
+
+long long eval_work_words(int n, int replicas, int wkind) {
+  if (eval_sliced(n, replicas, wkind)) return 0;
+  return static_cast<long long>(replicas) * (((n + 31) / 32 + 3) & ~3);
+}
+
+cudaError_t eval_launch(EvalArgs a, int wkind, cudaStream_t stream, int* launches) {
+  const int sms = sm_count();
+  const int n = a.n;
+  a.aligned4 = n % 4 == 0 && (reinterpret_cast<uintptr_t>(a.spins) & 3) == 0;
+  const bool narrow = a.narrow;
+  if (wkind == 0) a.mpos = a.m;
+  if (eval_sliced(n, a.R, wkind)) {
+    const int groups = (a.R + 31) / 32;
+    const size_t smem = static_cast<size_t>(n) * 4;
+    // slices per group: ~2 CTAs per SM in all, each with >= 64 edges per thread
+    long long S = (2LL * sms + groups - 1) / groups;
+    const long long maxs = a.m / (64LL * kSliceBlock);
+    if (S > maxs) S = maxs;
+    if (S < 1) S = 1;
+    const void* fn = narrow ? (wkind == 1 ? reinterpret_cast<const void*>(&k3_sliced<true, true>)
+                                          : reinterpret_cast<const void*>(&k3_sliced<true, false>))
+                            : (wkind == 1 ? reinterpret_cast<const void*>(&k3_sliced<false, true>)
+                                          : reinterpret_cast<const void*>(&k3_sliced<false, false>));
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e) return e;
+    void* params[] = {&a};
+    if (launches) *launches = 1;
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(S), groups), dim3(kSliceBlock), params, smem, stream);
+  }
+  a.nwp = ((n + 31) / 32 + 3) & ~3;
+  {
+    const int nw = (n + 31) / 32;
+    const int gx = (nw + 255) / 256 < 4 * sms ? (nw + 255) / 256 : 4 * sms;
+    k3_pack<<<dim3(gx < 1 ? 1 : gx, a.R), 256, 0, stream>>>(a);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  const bool sm = static_cast<long long>(a.nwp) * 4 <= 227 * 1024;
+  const size_t smem = sm ? static_cast<size_t>(a.nwp) * 4 : 0;
+  long long per = (static_cast<long long>(sms) + a.R - 1) / a.R;  // ~1 CTA per SM in all
+  const long long maxs = (a.m + 4LL * kBitsBlock - 1) / (4LL * kBitsBlock);
+  if (per > maxs) per = maxs;
+  if (per < 1) per = 1;
+  const void* fn = narrow ? (sm ? bits_fn<true, true>(wkind) : bits_fn<true, false>(wkind))
+                          : (sm ? bits_fn<false, true>(wkind) : bits_fn<false, false>(wkind));
+  if (sm && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))))
+    return e;
+  void* params[] = {&a};
+  if (launches) *launches = 2;
+  return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(per), a.R), dim3(kBitsBlock), params, smem, stream);
 }
 
 }  // namespace gdi

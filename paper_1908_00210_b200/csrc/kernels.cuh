@@ -169,10 +169,18 @@ struct PartArgs {
 };
 
 struct EvalArgs {
-  DevCsr g;
-  const int8_t* spins;    // [R][n]
-  int32_t replicas;
-  unsigned long long* out;  // [R][2] = {cut, sum} accumulated with atomics (zeroed)
+  int32_t n;
+  long long m, mpos;        // edges; +1 edges first ([0, mpos)) for +-1 weights
+  bool narrow;              // edges as u | v << 16 words (else int2)
+  bool aligned4;            // spin rows 4-byte aligned (set by eval_launch)
+  const void* edges;        // canonical u < v edge list (EvalLayout)
+  const int32_t* w;         // general weights per edge, or nullptr
+  const int8_t* spins;      // [R][n]
+  int32_t R;
+  uint32_t* work;           // k3_pack words [R][nwp] (eval_work_words)
+  int32_t nwp;
+  unsigned long long* out;  // [R][2] = {cut, spin sum}, accumulated with atomics (zeroed)
+  unsigned* bad;            // set when a spin byte is neither +1 nor -1 (zeroed)
 };
 
 } // namespace gdi

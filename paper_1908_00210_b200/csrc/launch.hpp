@@ -134,7 +134,11 @@ int part_words(int n);  // spin words per replica: ceil(n/32) + 1 zero word, pad
 // L2-resident read bandwidth (GB/s) for roofline denominators.
 cudaError_t probe_l2_read(size_t bytes, int iters, double* gbs);
 
-// K3 fused exact evaluation: {cut, sum} per replica into a zeroed buffer.
-cudaError_t eval_launch(const EvalArgs& args, bool weighted, cudaStream_t stream);
+// K3 fused exact evaluation (k3_eval.cu): {cut, spin sum} per replica
+// into a zeroed buffer. wkind: 0 unit, 1 +-1, 2 general weights. The
+// bit-packed path needs eval_work_words(...) words of scratch in args.work.
+bool eval_sliced(int n, int replicas, int wkind);
+long long eval_work_words(int n, int replicas, int wkind);
+cudaError_t eval_launch(EvalArgs args, int wkind, cudaStream_t stream, int* launches);
 
 }  // namespace gdi

@@ -142,6 +142,41 @@ __global__ void k_edges_fill(const int32_t* off, const int32_t* col, const int32
     }
 }
 
+// ---- K3 evaluation layout ----------------------------------------------------
+
+// upper-triangle entries of row u by weight class: cnt[0][u] (+1 or any
+// weight), cnt[1][u] (-1, wkind 1); row n is the scan's terminator
+__global__ void k_eval_count(const int32_t* off, const int32_t* col, const int32_t* w, int n, bool split,
+                             int32_t* cpos, int32_t* cneg) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u > n) return;
+  int p = 0, q = 0;
+  if (u < n)
+    for (int e = off[u]; e < off[u + 1]; e++)
+      if (col[e] > u) (split && w[e] < 0 ? q : p)++;
+  cpos[u] = p;
+  cneg[u] = q;
+}
+
+template <bool NARROW>
+__global__ void k_eval_fill(const int32_t* off, const int32_t* col, const int32_t* w, int n, bool split,
+                            bool weights, const int32_t* opos, const int32_t* oneg, long long mpos, void* edges,
+                            int32_t* ew) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  long long p = opos[u], q = mpos + oneg[u];
+  for (int e = off[u]; e < off[u + 1]; e++) {
+    const int v = col[e];
+    if (v <= u) continue;
+    const long long at = split && w[e] < 0 ? q++ : p++;
+    if (NARROW)
+      static_cast<uint32_t*>(edges)[at] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(v) << 16);
+    else
+      static_cast<int2*>(edges)[at] = make_int2(u, v);
+    if (weights) ew[at] = w[e];
+  }
+}
+
 // ---- k1_window layout (k1_window.cu) ----------------------------------------
 
 // window distance of neighbour j from row i: k = (i - j) mod n in 1..n-1
@@ -398,6 +433,39 @@ cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psel
   k_inverse<<<blocks(n), kB, 0, st>>>(T.order.as<int32_t>(), g.off, n, pos.as<int32_t>(), pdeg.as<int32_t>());
   k_psell<<<1184, kB, 0, st>>>(T.sell.as<int32_t>(), cells, pos.as<int32_t>(), n, 32 * ((n + 31) / 32),
                                psell.as<int32_t>());
+  if ((e = cudaGetLastError())) return e;
+  return cudaStreamSynchronize(st);
+}
+
+cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout* L, cudaStream_t st) {
+  const int n = g.n;
+  const bool split = wkind == 1, weights = wkind == 2;
+  L->m = m;
+  L->narrow = n <= 65536;
+  DevBuf cpos, cneg, opos, oneg;
+  cudaError_t e;
+  if ((e = cpos.alloc((n + 1) * sizeof(int32_t))) || (e = cneg.alloc((n + 1) * sizeof(int32_t))) ||
+      (e = opos.alloc((n + 1) * sizeof(int32_t))) || (e = oneg.alloc((n + 1) * sizeof(int32_t))))
+    return e;
+  k_eval_count<<<blocks(n + 1), kB, 0, st>>>(g.off, g.col, g.w, n, split, cpos.as<int32_t>(), cneg.as<int32_t>());
+  if ((e = exclusive_scan(cpos.as<int32_t>(), opos.as<int32_t>(), n + 1, st))) return e;
+  if ((e = exclusive_scan(cneg.as<int32_t>(), oneg.as<int32_t>(), n + 1, st))) return e;
+  int32_t mp = 0;
+  if ((e = cudaMemcpy(&mp, opos.as<int32_t>() + n, sizeof mp, cudaMemcpyDeviceToHost))) return e;
+  L->mpos = mp;
+  const size_t cells = m > 0 ? static_cast<size_t>(m) : 1;
+  if ((e = L->edges.alloc(cells * (L->narrow ? sizeof(uint32_t) : sizeof(int2))))) return e;
+  if (weights) {
+    if ((e = L->w.alloc(cells * sizeof(int32_t)))) return e;
+  } else {
+    L->w.reset();
+  }
+  if (L->narrow)
+    k_eval_fill<true><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, n, split, weights, opos.as<int32_t>(),
+                                                oneg.as<int32_t>(), L->mpos, L->edges.p, L->w.as<int32_t>());
+  else
+    k_eval_fill<false><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, n, split, weights, opos.as<int32_t>(),
+                                                 oneg.as<int32_t>(), L->mpos, L->edges.p, L->w.as<int32_t>());
   if ((e = cudaGetLastError())) return e;
   return cudaStreamSynchronize(st);
 }

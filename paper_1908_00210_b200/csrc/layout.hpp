@@ -33,6 +33,16 @@ struct PipeLayout {
   DevBuf wsell, wsell_off;
 };
 
+// K3 evaluation layout: the canonical edge list (u < v, row order), +1
+// weights first: narrow = n <= 65536, each edge one word u | v << 16, else
+// int2. wkind 1 (+-1): edges [0, mpos) have weight +1, [mpos, m) weight -1;
+// wkind 2: per-edge int32 weights in w.
+struct EvalLayout {
+  DevBuf edges, w;
+  long long m = 0, mpos = 0;
+  bool narrow = false;
+};
+
 // Uploads the reference CSR (int64 offsets, int32 neighbours, optional int32
 // weights), converts the offsets to int32 and validates on the device.
 // `w` is released when every weight is 1.
@@ -50,6 +60,9 @@ cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout*
 // (padding -> position 32 * ceil(n / 32), a zero word), and the degree of the
 // vertex at every position.
 cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, cudaStream_t st);
+
+// K3 layout (see EvalLayout).
+cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout* L, cudaStream_t st);
 
 // k1_window layout (every |w| == 1, n >= 2 * win).
 cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStream_t st);

@@ -54,6 +54,29 @@ gdi_trace_rec* trace_scratch(std::size_t count) {
 
 // Device-resident session over the C ABI: graph + buffers stay in HBM; the
 // caller times launch() on the stream it passes in.
+class Evaluator {
+public:
+  Evaluator(const MinCutProblem& problem, int dev) : n_(problem.graph().num_nodes()), c_(problem.coefficients()) {
+    const Graph& g = problem.graph();
+    check_abi(gdi_graph_create_pairs(dev, n_, g.csr_offsets().data(), adjacency_pairs(g), &graph_));
+  }
+  ~Evaluator() {
+    if (graph_) gdi_graph_destroy(graph_);
+  }
+  py::dict evaluate(py::array_t<std::int8_t, py::array::c_style | py::array::forcecast> spins);
+  void evaluate_device(std::uintptr_t spins, int replicas, std::uintptr_t cut_sum, std::uintptr_t bad,
+                       std::uintptr_t stream) {
+    check_abi(gdi_evaluate_device(graph_, reinterpret_cast<const std::int8_t*>(spins), replicas,
+                                  reinterpret_cast<std::int64_t*>(cut_sum), reinterpret_cast<std::uint32_t*>(bad),
+                                  reinterpret_cast<void*>(stream)));
+  }
+
+private:
+  std::int32_t n_;
+  Coefficients c_;
+  gdi_graph* graph_ = nullptr;
+};
+
 class Session {
 public:
   Session(const MinCutProblem& problem, const AnnealParams& params_in, int replicas, std::uintptr_t stream,
@@ -275,6 +298,17 @@ private:
   std::int32_t n_ = 0;
   int sweeps_ = 0;
 };
+
+py::dict Evaluator::evaluate(py::array_t<std::int8_t, py::array::c_style | py::array::forcecast> spins) {
+  if (spins.ndim() != 2 || spins.shape(1) != n_) throw domain_error("spins must have shape (replicas, num_nodes)");
+  const auto R = static_cast<std::int32_t>(spins.shape(0));
+  std::vector<gdi_score> sc(static_cast<std::size_t>(R));
+  {
+    py::gil_scoped_release nogil;
+    check_abi(gdi_evaluate_batch(graph_, spins.data(), R, c_.a_num, c_.b_num, c_.denom, sc.data()));
+  }
+  return Session::pack({}, sc, {}, static_cast<std::size_t>(R), 0, 0, 0.0, false, false);
+}
 
 PYBIND11_MODULE(pyising, m) {
   m.doc() = "gdi-b200: GDI Ising annealing for balanced min-cut on NVIDIA B200 (sm_100a)";
@@ -560,6 +594,15 @@ PYBIND11_MODULE(pyising, m) {
         return Session::pack({}, sc, {}, static_cast<std::size_t>(R), 0, 0, 0.0, false, false);
       },
       py::arg("problem"), py::arg("spins"), "K3 fused exact cut/imbalance/H of (R, n) spin rows on the device.");
+
+  // a device graph kept for repeated K3 evaluations (gdi_evaluate_batch on
+  // host spins, gdi_evaluate_device on device pointers)
+  py::class_<Evaluator>(m, "Evaluator")
+      .def(py::init<const MinCutProblem&, int>(), py::arg("problem"), py::arg("device") = 0)
+      .def("evaluate", &Evaluator::evaluate, py::arg("spins"))
+      .def("evaluate_device", &Evaluator::evaluate_device, py::arg("spins_ptr"), py::arg("replicas"),
+           py::arg("cut_sum_ptr"), py::arg("bad_ptr") = 0, py::arg("stream") = 0,
+           "Enqueue K3 on device int8 spins [R][n]; writes int64 {cut, sum} per replica to cut_sum_ptr.");
 
   py::class_<Session>(m, "Session")
       .def(py::init<const MinCutProblem&, const AnnealParams&, int, std::uintptr_t, bool, int>(), py::arg("problem"),
