@@ -328,6 +328,59 @@ def run_partition_bench(args, pi, torch, dist, world, rank, local, dev, recipe, 
     return 0
 
 
+def eval_leg(pi, torch, prob, g, spins, stream, flush, dev, hbm, hbm_src, reps=20):
+    """K3 (k3_eval.cu, north_star (4)): the fused exact cut + spin sum of the
+    step's final spins, device-resident, timed alone with CUDA events (L2
+    flushed before every call); plus the same spins tiled to 16x the batch,
+    where the int8 spin stream dominates. Roofline: algorithmic bytes = the
+    int8 spins (R * n) + the canonical edge list (4 B per edge up to 65536
+    vertices, else 8 B; +4 B weights if general) per call, against HBM."""
+    ev = pi.Evaluator(prob, dev.index or 0)
+    n, m = g.num_nodes, g.num_edges
+    eb = (4 if n <= 65536 else 8) + (4 if not g.all_unit_weights and not _pm1(g) else 0)
+    out = {}
+    for label, tile in (("batch", 1), ("batch_x16", 16)):
+        sp = np.ascontiguousarray(np.tile(spins, (tile, 1)))
+        R = sp.shape[0]
+        d = torch.from_numpy(sp).to(dev)
+        res = torch.zeros((R, 2), dtype=torch.int64, device=dev)
+        bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        ts = []
+        for i in range(reps + 3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ev.evaluate_device(d.data_ptr(), R, res.data_ptr(), bad.data_ptr(), stream.cuda_stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if i >= 3:
+                ts.append(e0.elapsed_time(e1))
+        ref = ev.evaluate(sp[:1])  # host path on the first row (its own upload) as a spot check
+        got = res.cpu().numpy()
+        ms = statistics.median(ts)
+        algo = R * n + m * eb
+        out[label] = {
+            "replicas": R, "ms": ms, "evals_per_s": R / (ms * 1e-3), "edge_checks_per_s": R * m / (ms * 1e-3),
+            "kernel": "k3_slice + k3_sliced" if (R >= 16 and n * 4 <= 200 * 1024 and (g.all_unit_weights or _pm1(g)))
+                      else "k3_pack + k3_bits",
+            "launches": 4, "note": "timed region = 2 memsets + 2 kernels of gdi_evaluate_device",
+            "roofline": {"bound": "hbm", "achieved": algo / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": algo / (ms * 1e-3) / 1e9 / hbm, "algorithmic_bytes": algo, "peak_source": hbm_src},
+            "check": bool(int(got[0, 0]) == int(ref["cut"][0]) and abs(int(got[0, 1])) == int(ref["imbalance"][0])
+                          and int(bad.item()) == 0)}
+    return out
+
+
+def _pm1(g) -> bool:
+    return not g.all_unit_weights and all(abs(w) == 1 for _, _, w in _edge_weights(g))
+
+
+def _edge_weights(g):
+    for u in range(g.num_nodes):
+        for v, w in g.neighbors(u):
+            yield u, v, w
+
+
 def free_port() -> int:
     import socket
 
@@ -373,6 +426,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-throughput", action="store_true")
+    ap.add_argument("--no-eval", action="store_true", help="skip the K3 evaluation leg")
     ap.add_argument("--mode", default="exact", choices=["exact", "throughput"],
                     help="headline mode: exact (bit-exact, default) or throughput (pooled racy mode)")
     ap.add_argument("--topology-only", action="store_true",
@@ -527,6 +581,9 @@ def main():
             "result": best,
         }
     sess.sync()
+    if rank == 0 and not args.no_eval:
+        fin = sess.fetch(spins=True, trace=False)
+        line["evaluation"] = eval_leg(pi, torch, prob, g, fin["spins"], stream, flush, dev, hbm, hbm_src)
     del sess
 
     # Throughput mode (K2, the reference's pooled racy mode) on the same

@@ -973,16 +973,32 @@ int gdi_evaluate_device(const gdi_graph* g, const int8_t* d_spins, int32_t repli
   if ((rc = ensure_eval(gm))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // per-thread scratch kept between calls (the bench times back-to-back calls)
-  thread_local EvalScratch sc;
-  thread_local int sc_dev = -1;
-  if (sc_dev != g->device) {
-    sc.buf.reset();
-    sc_dev = g->device;
+  thread_local DevBuf work;
+  thread_local int work_dev = -1;
+  if (work_dev != g->device) {
+    work.reset();
+    work_dev = g->device;
   }
-  int launches = 0;
-  if ((rc = eval_enqueue(gm, d_spins, replicas, sc, st, &launches))) return rc;
-  GDI_CUDA(cudaMemcpyAsync(d_cut_sum, sc.buf.p, static_cast<size_t>(replicas) * 16, cudaMemcpyDeviceToDevice, st));
-  if (d_bad) GDI_CUDA(cudaMemcpyAsync(d_bad, sc.buf.as<char>() + sc.bad_off, 4, cudaMemcpyDeviceToDevice, st));
+  const size_t ww = static_cast<size_t>(eval_work_words(g->st.n, replicas, g->wkind)) * 4 + 16;
+  if (work.bytes < ww) GDI_CUDA(work.alloc(ww));
+  // results straight into the caller's buffer (zeroed here), the bad flag
+  // into the caller's word or the scratch's last 4 bytes
+  uint32_t* bad = d_bad ? d_bad : reinterpret_cast<uint32_t*>(work.as<char>() + ww - 4);
+  GDI_CUDA(cudaMemsetAsync(d_cut_sum, 0, static_cast<size_t>(replicas) * 16, st));
+  GDI_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  EvalArgs a{};
+  a.n = g->st.n;
+  a.m = g->evl.m;
+  a.mpos = g->evl.mpos;
+  a.narrow = g->evl.narrow;
+  a.edges = g->evl.edges.p;
+  a.w = g->evl.w.as<int32_t>();
+  a.spins = d_spins;
+  a.R = replicas;
+  a.work = work.as<uint32_t>();
+  a.out = reinterpret_cast<unsigned long long*>(d_cut_sum);
+  a.bad = bad;
+  GDI_CUDA(eval_launch(a, g->wkind, st, nullptr));
   return GDI_OK;
 }
 

@@ -31,6 +31,8 @@
 // kernel is bound by the edge stream (8 B per edge from HBM / L2).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "launch.hpp"
 
@@ -39,8 +41,8 @@ namespace gdi {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kSliceBlock = 512;
-constexpr int kBitsBlock = 512;
+constexpr int kSliceBlock = 256;
+constexpr int kBitsBlock = 1024;
 constexpr int kLevels = 20;  // bit-sliced counter levels above the Harley-Seal eights: < 8 * 2^20 edges per thread
 
 __device__ __forceinline__ void csa(unsigned& h, unsigned& l, unsigned a, unsigned b, unsigned c) {
@@ -146,68 +148,90 @@ __device__ __forceinline__ long long sliced_range(const EvalArgs& a, const unsig
   return acc.count(lane);
 }
 
-template <bool NARROW, bool SIGNED>
-__global__ void __launch_bounds__(kSliceBlock) k3_sliced(const EvalArgs a) {
-  extern __shared__ unsigned T[];
-  __shared__ long long cnt[32];
-  const int n = a.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int g = blockIdx.y, r = 32 * g + lane;
-  const bool live = r < a.R;
-  const int8_t* row = a.spins + static_cast<size_t>(live ? r : 0) * n;
-  // transpose: warp w takes the 32-vertex blocks w, w + nwarps, ...; the
-  // spin sum and the byte check are done by slice 0 only
-  long long pop = 0;
-  bool ok = true;
-  for (int v0 = 32 * warp; v0 < n; v0 += 32 * nwarps) {
-    unsigned w[8];
-    const int lim = n - v0;  // valid bytes in this block (>= 1)
-    if (a.aligned4 && lim >= 32) {
+// 32 spin bytes (8 words) -> 32 bits, bit j = byte j is +1
+__device__ __forceinline__ unsigned pack32(const unsigned (&w)[8]) {
+  unsigned bits = 0u;
 #pragma unroll
-      for (int k = 0; k < 8; k++) w[k] = live ? __ldg(reinterpret_cast<const unsigned*>(row + v0) + k) : 0x01010101u;
+  for (int k = 0; k < 8; k++) {
+    const unsigned t = (~w[k] >> 7) & 0x01010101u;   // byte b -> bit 8b
+    bits |= ((t * 0x01020408u) >> 24 & 0xfu) << (4 * k);  // bits 24..27 = bytes 0..3
+  }
+  return bits;
+}
+
+// 32 spin bytes of one replica row from v0 on (lim valid bytes; +1 padding)
+__device__ __forceinline__ void load32(const int8_t* row, int v0, int lim, bool aligned4, unsigned (&w)[8]) {
+  if (aligned4 && lim >= 32) {
+    const uint4* q = reinterpret_cast<const uint4*>(row + v0);
+    if ((reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+      const uint4 x = __ldg(q), y = __ldg(q + 1);
+      w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w, w[4] = y.x, w[5] = y.y, w[6] = y.z, w[7] = y.w;
     } else {
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        unsigned x = 0x01010101u;  // (+1 padding: never looked up, masked from the sum)
-        for (int b = 0; b < 4; b++)
-          if (live && 4 * k + b < lim) x = (x & ~(0xffu << (8 * b))) | (static_cast<unsigned>(static_cast<uint8_t>(row[v0 + 4 * k + b])) << (8 * b));
-        w[k] = x;
-      }
+      for (int k = 0; k < 8; k++) w[k] = __ldg(reinterpret_cast<const unsigned*>(row + v0) + k);
     }
-    unsigned mine = 0u;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const unsigned p = pos_bits(w[k]);
-      ok &= valid4(w[k]);
-#pragma unroll
-      for (int b = 0; b < 4; b++) {
-        const unsigned bal = __ballot_sync(FULL, live && ((p >> (8 * b + 7)) & 1u));
-        if (lane == 4 * k + b) mine = bal;
-      }
-      const int c = lim - 4 * k;  // bytes of word k inside the graph
-      const unsigned keep = c >= 4 ? 0x80808080u : c <= 0 ? 0u : (0x80808080u >> (8 * (4 - c)));
-      pop += __popc(p & keep);
-    }
-    if (lane < lim) T[v0 + lane] = mine;
+    return;
   }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    unsigned x = 0x01010101u;
+    for (int b = 0; b < 4; b++)
+      if (4 * k + b < lim)
+        x = (x & ~(0xffu << (8 * b))) | (static_cast<unsigned>(static_cast<uint8_t>(row[v0 + 4 * k + b])) << (8 * b));
+    w[k] = x;
+  }
+}
+
+// Transpose of a replica group's spins into vertex words T[g][v] (bit r =
+// replica 32g + r is +1), with the spin sums and the byte check. Warp = one
+// 32-vertex block of one group: lane r packs its replica's 32 bytes into one
+// word, a 32 x 32 bit transpose hands lane j the word of vertex v0 + j.
+__global__ void __launch_bounds__(256) k3_slice(const EvalArgs a) {
+  const int n = a.n, lane = threadIdx.x & 31, g = blockIdx.y, r = 32 * g + lane;
+  const bool live = r < a.R;
+  const int8_t* row = a.spins + static_cast<size_t>(live ? r : 0) * n;
+  const int nb = (n + 31) >> 5, gw = gridDim.x * (blockDim.x >> 5);
+  long long pop = 0;
+  bool ok = true;
+  for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += gw) {
+    const int v0 = 32 * b, lim = n - v0;
+    unsigned w[8];
+    load32(row, v0, lim, a.aligned4, w);
+#pragma unroll
+    for (int k = 0; k < 8; k++) ok &= valid4(w[k]);
+    unsigned bits = live ? pack32(w) : 0u;
+    if (lim < 32) bits &= (1u << lim) - 1u;
+    pop += __popc(bits);
+    const unsigned col = transpose32(bits, lane);
+    if (lane < lim) a.work[static_cast<size_t>(g) * n + v0 + lane] = col;
+  }
+  ok = __all_sync(FULL, ok || !live);
+  const long long add = 2 * pop - (blockIdx.x == 0 && threadIdx.x < 32 ? n : 0);  // spin sum; one warp adds -n
+  if (live && add != 0) atomicAdd(a.out + 2 * r + 1, static_cast<unsigned long long>(add));
+  if (!ok && lane == 0) atomicOr(a.bad, 1u);
+}
+
+// The cut of a replica group over one slice of the edges, T[g] staged in
+// shared memory.
+template <bool NARROW, bool SIGNED>
+__global__ void __launch_bounds__(kSliceBlock) k3_sliced(const EvalArgs a) {
+  extern __shared__ __align__(16) unsigned T[];
+  __shared__ long long cnt[32];
+  const int n = a.n, lane = threadIdx.x & 31, g = blockIdx.y;
+  const unsigned* src = a.work + static_cast<size_t>(g) * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) T[i] = __ldg(src + i);
   if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
   __syncthreads();
-  if (blockIdx.x == 0 && live) {
-    if (!ok) atomicOr(a.bad, 1u);
-    // the spin sum 2 * pop - n: every warp adds 2 * its blocks' pop, warp 0 also -n
-    const long long add = 2 * pop - (warp == 0 ? n : 0);
-    if (add != 0) atomicAdd(a.out + 2 * r + 1, static_cast<unsigned long long>(add));
-  }
-  // edges of this CTA's slice (grid-stride over the list), +1 then -1
   long long c = sliced_range<NARROW>(a, T, 0, a.mpos, lane);
   if (SIGNED) c -= sliced_range<NARROW>(a, T, a.mpos, a.m, lane);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[lane]), static_cast<unsigned long long>(c));
+  if (c != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[lane]), static_cast<unsigned long long>(c));
   __syncthreads();
   if (threadIdx.x < 32 && 32 * g + threadIdx.x < a.R && cnt[threadIdx.x] != 0)
     atomicAdd(a.out + 2 * (32 * g + threadIdx.x), static_cast<unsigned long long>(cnt[threadIdx.x]));
 }
 
-// int8 spins -> bit words [R][nw] + count of +1 spins. Thread = one word of
-// one replica (32 bytes, read as 8 x 4 bytes when the rows are 4-aligned).
+// int8 spins -> bit words [R][nwp] + the spin sum. Thread = one word of one
+// replica (32 bytes: two 16-byte loads when the rows are aligned).
 __global__ void __launch_bounds__(256) k3_pack(const EvalArgs a) {
   const int n = a.n, nw = (n + 31) >> 5, r = blockIdx.y;
   const int8_t* row = a.spins + static_cast<size_t>(r) * n;
@@ -215,21 +239,11 @@ __global__ void __launch_bounds__(256) k3_pack(const EvalArgs a) {
   bool ok = true;
   for (int wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += gridDim.x * blockDim.x) {
     const int v0 = 32 * wi, lim = n - v0;
-    unsigned bits = 0u;
+    unsigned w[8];
+    load32(row, v0, lim, a.aligned4, w);
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      unsigned x = 0x01010101u;
-      if (a.aligned4 && lim >= 32) {
-        x = __ldcs(reinterpret_cast<const unsigned*>(row + v0) + k);
-      } else {
-        for (int b = 0; b < 4; b++)
-          if (4 * k + b < lim) x = (x & ~(0xffu << (8 * b))) | (static_cast<unsigned>(static_cast<uint8_t>(row[v0 + 4 * k + b])) << (8 * b));
-      }
-      ok &= valid4(x);
-      const unsigned p = pos_bits(x);  // bits 7, 15, 23, 31
-      const unsigned q = ((p >> 7) & 1u) | ((p >> 14) & 2u) | ((p >> 21) & 4u) | ((p >> 28) & 8u);
-      bits |= q << (4 * k);
-    }
+    for (int k = 0; k < 8; k++) ok &= valid4(w[k]);
+    unsigned bits = pack32(w);
     if (lim < 32) bits &= (1u << lim) - 1u;
     pop += __popc(bits);
     a.work[static_cast<size_t>(r) * a.nwp + wi] = bits;
@@ -254,21 +268,48 @@ __global__ void __launch_bounds__(kBitsBlock) k3_bits(const EvalArgs a) {
   const unsigned* words = a.work + static_cast<size_t>(r) * a.nwp;
   if (SM) {
     const uint4* src = reinterpret_cast<const uint4*>(words);
+#pragma unroll 8
     for (int i = threadIdx.x; i < nw4; i += blockDim.x) reinterpret_cast<uint4*>(S)[i] = __ldcg(src + i);
     __syncthreads();
   }
   auto bit = [&](int v) { return ((SM ? S[v >> 5] : __ldg(words + (v >> 5))) >> (v & 31)) & 1u; };
   long long cut = 0;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  const long long m = a.m;
-#pragma unroll 4
-  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
-    int u, v;
-    edge_at<NARROW>(a, e, u, v);
+  auto one = [&](int u, int v, long long e) {
     const bool c = bit(u) != bit(v);
     if (WK == 0) cut += c;
     if (WK == 1) cut += c ? (e < a.mpos ? 1 : -1) : 0;
     if (WK == 2) cut += c ? __ldg(a.w + e) : 0;
+  };
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long m = a.m;
+  // 16-byte edge loads (4 narrow / 2 wide edges), 4 issued before any is
+  // used (out-of-range slots are the edge (0, 0): never cut)
+  constexpr int PER = NARROW ? 4 : 2;
+  const long long mq = m / PER;
+  const uint4* E = static_cast<const uint4*>(a.edges);
+  for (long long q0 = tid; q0 < mq; q0 += 4 * stride) {
+    uint4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) x[k] = q0 + k * stride < mq ? __ldg(E + q0 + k * stride) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const long long e = (q0 + k * stride) * PER;
+      if (NARROW) {
+        one(x[k].x & 0xffffu, x[k].x >> 16, e);
+        one(x[k].y & 0xffffu, x[k].y >> 16, e + 1);
+        one(x[k].z & 0xffffu, x[k].z >> 16, e + 2);
+        one(x[k].w & 0xffffu, x[k].w >> 16, e + 3);
+      } else {
+        one(static_cast<int>(x[k].x), static_cast<int>(x[k].y), e);
+        one(static_cast<int>(x[k].z), static_cast<int>(x[k].w), e + 1);
+      }
+    }
+  }
+  for (long long e = mq * PER + tid; e < m; e += stride) {
+    int u, v;
+    edge_at<NARROW>(a, e, u, v);
+    one(u, v, e);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cut += __shfl_xor_sync(FULL, cut, o);
@@ -306,7 +347,7 @@ bool eval_sliced(int n, int replicas, int wkind) {
 }
 
 long long eval_work_words(int n, int replicas, int wkind) {
-  if (eval_sliced(n, replicas, wkind)) return 0;
+  if (eval_sliced(n, replicas, wkind)) return static_cast<long long>((replicas + 31) / 32) * n;
   return static_cast<long long>(replicas) * (((n + 31) / 32 + 3) & ~3);
 }
 
@@ -316,22 +357,34 @@ cudaError_t eval_launch(EvalArgs a, int wkind, cudaStream_t stream, int* launche
   a.aligned4 = n % 4 == 0 && (reinterpret_cast<uintptr_t>(a.spins) & 3) == 0;
   const bool narrow = a.narrow;
   if (wkind == 0) a.mpos = a.m;
+  cudaError_t e;
   if (eval_sliced(n, a.R, wkind)) {
     const int groups = (a.R + 31) / 32;
+    // transpose: 8 vertex blocks per CTA, ~4 CTAs per SM in all
+    {
+      const long long nb = (n + 31) / 32;
+      long long gx = (nb + 7) / 8;
+      const long long cap = (4LL * sms + groups - 1) / groups;
+      if (gx > cap) gx = cap;
+      if (gx < 1) gx = 1;
+      k3_slice<<<dim3(static_cast<unsigned>(gx), groups), 256, 0, stream>>>(a);
+      if ((e = cudaGetLastError())) return e;
+    }
+    // cut: slices per group for ~2 CTAs per SM in all, >= 16 edges per thread
     const size_t smem = static_cast<size_t>(n) * 4;
-    // slices per group: ~2 CTAs per SM in all, each with >= 64 edges per thread
     long long S = (2LL * sms + groups - 1) / groups;
-    const long long maxs = a.m / (64LL * kSliceBlock);
+    const long long maxs = a.m / (16LL * kSliceBlock);
     if (S > maxs) S = maxs;
     if (S < 1) S = 1;
     const void* fn = narrow ? (wkind == 1 ? reinterpret_cast<const void*>(&k3_sliced<true, true>)
                                           : reinterpret_cast<const void*>(&k3_sliced<true, false>))
                             : (wkind == 1 ? reinterpret_cast<const void*>(&k3_sliced<false, true>)
                                           : reinterpret_cast<const void*>(&k3_sliced<false, false>));
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e) return e;
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))))
+      return e;
     void* params[] = {&a};
-    if (launches) *launches = 1;
+    if (launches) *launches = 2;
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(S), groups), dim3(kSliceBlock), params, smem, stream);
   }
   a.nwp = ((n + 31) / 32 + 3) & ~3;
@@ -340,9 +393,9 @@ cudaError_t eval_launch(EvalArgs a, int wkind, cudaStream_t stream, int* launche
     const int gx = (nw + 255) / 256 < 4 * sms ? (nw + 255) / 256 : 4 * sms;
     k3_pack<<<dim3(gx < 1 ? 1 : gx, a.R), 256, 0, stream>>>(a);
   }
-  cudaError_t e = cudaGetLastError();
-  if (e) return e;
-  const bool sm = static_cast<long long>(a.nwp) * 4 <= 227 * 1024;
+  if ((e = cudaGetLastError())) return e;
+  bool sm = static_cast<long long>(a.nwp) * 4 <= 227 * 1024;
+  if (const char* x = std::getenv("GDI_K3_SMEM")) sm = sm && std::atoi(x) != 0;  // A/B: L1-cached lookups
   const size_t smem = sm ? static_cast<size_t>(a.nwp) * 4 : 0;
   long long per = (static_cast<long long>(sms) + a.R - 1) / a.R;  // ~1 CTA per SM in all
   const long long maxs = (a.m + 4LL * kBitsBlock - 1) / (4LL * kBitsBlock);
@@ -350,7 +403,7 @@ cudaError_t eval_launch(EvalArgs a, int wkind, cudaStream_t stream, int* launche
   if (per < 1) per = 1;
   const void* fn = narrow ? (sm ? bits_fn<true, true>(wkind) : bits_fn<true, false>(wkind))
                           : (sm ? bits_fn<false, true>(wkind) : bits_fn<false, false>(wkind));
-  if (sm && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))))
+  if (smem > 48 * 1024 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))))
     return e;
   void* params[] = {&a};
   if (launches) *launches = 2;
