@@ -93,14 +93,14 @@ struct gdi_graph {
   std::mutex mu;
   bool thru_built = false, pipe_built = false, part_built = false, eval_built = false;
   ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
-  DevBuf psell, pdeg;  // K4: the SELL rows over visit-order positions, degree by position
+  DevBuf psell, pdeg, pgchunk;  // K4: the SELL rows over visit-order positions, degree by position, group -> chunk
   PipeLayout pipel;  // k1_window: window masks, forward masks, SELL rows
   PipeGraph pipe;    // k1_window view (ok = eligible; pointers once built)
   EvalLayout evl;    // K3: canonical edge list
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
-                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes +
+                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes + pgchunk.bytes +
                                 pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
                                 pipel.wsell_off.bytes + evl.edges.bytes + evl.w.bytes);
@@ -203,7 +203,7 @@ int ensure_part(gdi_graph* g) {
   if (g->part_built) return GDI_OK;
   cudaStream_t st = nullptr;
   GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const cudaError_t e = build_part_layout(g->csr(), g->thru, g->psell, g->pdeg, st);
+  const cudaError_t e = build_part_layout(g->csr(), g->thru, g->psell, g->pdeg, g->pgchunk, st);
   cudaStreamDestroy(st);
   GDI_CUDA(e);
   g->part_built = true;
@@ -681,6 +681,8 @@ int gdi_session_launch(gdi_session* s) {
       a.order = s->g->thru.order.as<int32_t>();
       a.psell = s->g->psell.as<int4>();
       a.pdeg = s->g->pdeg.as<int32_t>();
+      a.gchunk = s->g->pgchunk.as<int32_t>();
+      a.ngroups = static_cast<int32_t>(s->g->thru.slots / 32);
       a.sell_off = s->g->thru.sell_off.as<int32_t>();
       a.sell_w = s->g->thru.sell_w.as<int4>();
       a.chains = s->kplan.chains;
@@ -1083,6 +1085,8 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   a.order = g->thru.order.as<int32_t>();
   a.psell = g->psell.as<int4>();
   a.pdeg = g->pdeg.as<int32_t>();
+  a.gchunk = g->pgchunk.as<int32_t>();
+  a.ngroups = static_cast<int32_t>(g->thru.slots / 32);
   a.sell_off = g->thru.sell_off.as<int32_t>();
   a.sell_w = g->thru.sell_w.as<int4>();
   a.chains = s->plan.chains;

@@ -492,13 +492,26 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
 
   // one chunk: visits against counter G (lane order), spin stores and the
   // scatter of every change into its neighbours' fields
+  // draws: one Philox call per pair of chunks (2b, 2b + 1) (pair_draws);
+  // the odd chunk's half is kept when its pair was drawn just before
+  uint64_t spare = 0;
+  int spare_c = -1;
   auto chunk = [&](int c, int& G, int sweep, unsigned long long tm, bool en) {
     const int p = c * 32 + lane;
     const bool live = p < n;
     const int v = live ? order[p] : 0;
     const int own = live ? s[v] : -1, f = live ? fget<FB>(fld, v) : 0;
-    const Philox4 x = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(v), 0u, 0u, k0, k1);
-    const bool coin = (x.z >> 31) != 0, flip = en && ((static_cast<uint64_t>(x.x) << 32) | x.y) <= tm;
+    uint64_t u;
+    if (spare_c == c) {
+      u = spare;
+    } else {
+      uint64_t u0, u1;
+      pair_draws(static_cast<uint32_t>(sweep), static_cast<uint32_t>(c >> 1), lane, k0, k1, u0, u1);
+      u = (c & 1) ? u1 : u0;
+      spare = u1;
+      spare_c = (c & 1) ? -1 : c + 1;
+    }
+    const bool coin = (u & 1u) != 0, flip = en && u <= tm;
     const int base = -a4 * own - bb * f;
     int fin = live ? decide(a4 * G + base, coin, flip) : own;
     unsigned up = __ballot_sync(FULL, fin > own), dn = __ballot_sync(FULL, fin < own);
@@ -544,6 +557,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     const int rot = (j + P - sweep % P) % P;
     const int share = 2 * (q + (rot < rem ? 1 : 0)) + (rot == P - 1 ? par : 0);
     int G = share;
+    spare_c = -1;  // (draws are per sweep)
     // chain j visits the segments j, j + P, ... of kSeg consecutive chunks,
     // each in order: concurrent chains are kSeg chunks apart (round-robin
     // single chunks made adjacent lattice sites concurrent: torus(100,20) best

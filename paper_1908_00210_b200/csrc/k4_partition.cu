@@ -162,10 +162,15 @@ __device__ __forceinline__ int long_rows(const PartArgs& a, const Row<WK, KMAX>&
 // The spin-word loads of the register bucket are issued first and consumed
 // after the Philox draw, so their latency (an LDS, or an L2 round trip for
 // the fresh bands of SMODE 2) overlaps the RNG.
+// Draws (pair_draws): chain chunks k and k + 1 (k even) of chain J share one
+// Philox call, pair id = the pair's first chunk J + k * P; a visit whose
+// pair was drawn just before takes the kept half (use_spare), else draws and
+// keeps the other half in `spare`. Global-tail chunks (>= nmain, no chain)
+// draw alone (pair id = the chunk).
 template <int WK, int KMAX, typename Word>
 __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMAX>& r, int c, Word word, int lane,
                                             int sweep, uint32_t k0, uint32_t k1, unsigned long long tm,
-                                            bool en) {
+                                            bool en, uint32_t pair, int half, uint64_t& spare, bool use_spare) {
   Visit x;
   x.live = c * 32 + lane < a.g.n;
   x.own = x.live ? (((r.word >> lane) & 1u) ? 1 : -1) : -1;
@@ -179,9 +184,17 @@ __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMA
       wv[4 * k + 2] = word(pos(r.g[k].z) >> 5);
       wv[4 * k + 3] = word(pos(r.g[k].w) >> 5);
     }
-  const Philox4 ph = philox4x32_10(static_cast<uint32_t>(sweep), static_cast<uint32_t>(r.v), 0u, 0u, k0, k1);
-  x.coin = (ph.z >> 31) != 0;
-  x.flip = en && ((static_cast<uint64_t>(ph.x) << 32) | ph.y) <= tm;
+  uint64_t u;
+  if (use_spare) {
+    u = spare;
+  } else {
+    uint64_t u0, u1;
+    pair_draws(static_cast<uint32_t>(sweep), pair, lane, k0, k1, u0, u1);
+    u = half ? u1 : u0;
+    spare = u1;
+  }
+  x.coin = (u & 1u) != 0;
+  x.flip = en && u <= tm;
   auto bit = [](int e, int w, unsigned wd) {
     const unsigned sh = __funnelshift_r(wd, 0u, WK == 1 ? (e & 0x7fffffff) : e);
     if (WK == 2) return (sh & 1u) ? w : -w;
@@ -206,17 +219,29 @@ __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMA
 // spin word: two evaluations settle most chunks, else the in-order scan
 // (sweep_common.cuh warp_seq_decide). (Written out here: the same logic
 // behind a shared helper with a round loop measured 1.5x slower.)
+// (K4_ROUNDS > 2 evaluations before the scan measured slower: M1 1.31 ->
+// 1.40-1.43 ms; taking the second evaluation as final instead of scanning
+// saves 15% but wrecks quality: cut +47%, imbalance up to 400)
+#ifndef K4_ROUNDS
+#define K4_ROUNDS 2
+#endif
 __device__ __forceinline__ unsigned decide_chunk(const Visit& x, int& G, int a4, int bb, int lane) {
   const int base = -a4 * x.own - bb * x.f;
   int fin = x.live ? decide(a4 * G + base, x.coin, x.flip) : x.own;
-  const unsigned up = __ballot_sync(FULL, fin > x.own), dn = __ballot_sync(FULL, fin < x.own);
+  unsigned up = __ballot_sync(FULL, fin > x.own), dn = __ballot_sync(FULL, fin < x.own);
   if ((up | dn) == 0u) return __ballot_sync(FULL, fin > 0);
   const unsigned below = (1u << lane) - 1u;
-  const int fin2 =
-      x.live ? decide(a4 * (G + 2 * (__popc(up & below) - __popc(dn & below))) + base, x.coin, x.flip) : x.own;
-  if (__all_sync(FULL, fin2 == fin)) {
-    G += 2 * (__popc(up) - __popc(dn));
-    return __ballot_sync(FULL, fin > 0);
+#pragma unroll
+  for (int round = 1; round < K4_ROUNDS; round++) {
+    const int fin2 =
+        x.live ? decide(a4 * (G + 2 * (__popc(up & below) - __popc(dn & below))) + base, x.coin, x.flip) : x.own;
+    if (__all_sync(FULL, fin2 == fin)) {
+      G += 2 * (__popc(up) - __popc(dn));
+      return __ballot_sync(FULL, fin > 0);
+    }
+    fin = fin2;
+    up = __ballot_sync(FULL, fin > x.own);
+    dn = __ballot_sync(FULL, fin < x.own);
   }
   fin = warp_seq_decide(x.own, x.f, x.live, x.coin, x.flip, G, a4, bb, lane);
   return __ballot_sync(FULL, fin > 0);
@@ -464,6 +489,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     bounds(0, c0, c1);
     load_row<WK, KMAX>(a, gb, J, c0, c1, lane, cur);
   }
+  uint64_t spare = 0;
 #pragma unroll 1
   for (int k = 0; k < Km; k++) {
     const int c = J + k * P;
@@ -474,7 +500,8 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     }
     blo = (k - 1) * P;
     bhi = (k + 1) * P;
-    const Visit x = make_visit<WK, KMAX>(a, cur, c, word, lane, sweep, k0, k1, tm, en);
+    const Visit x = make_visit<WK, KMAX>(a, cur, c, word, lane, sweep, k0, k1, tm, en,
+                                         static_cast<uint32_t>(J + (k & ~1) * P), k & 1, spare, (k & 1) != 0);
     commit(c, cur.word, decide_chunk(x, G, a4, bb, lane));
     cur = nxt;
   }
@@ -487,7 +514,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     const int ct = J + (K - 1) * P;
     blo = (K - 2) * P;
     bhi = K * P;
-    const Visit xt = K > 0 ? make_visit<WK, KMAX>(a, cur, ct, word, lane, sweep, k0, k1, tm, en)
+    // (its pair's first chunk K - 2 was drawn by the loop above when K - 1 is odd)
+    const Visit xt = K > 0 ? make_visit<WK, KMAX>(a, cur, ct, word, lane, sweep, k0, k1, tm, en,
+                                                  static_cast<uint32_t>(J + ((K - 1) & ~1) * P), (K - 1) & 1, spare,
+                                                  ((K - 1) & 1) != 0)
                            : Visit{-1, 0, false, false, false};
     stage[warp][lane] = pack(xt);
     if (lane == 0) {
@@ -631,8 +661,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
     Row<WK, KMAX> row;
     load_row<WK, KMAX>(a, gb, c, __ldg(a.sell_off + c), __ldg(a.sell_off + c + 1), lane, row);
     row.word = pre(c);
+    uint64_t spare = 0;
     const Visit xt = make_visit<WK, KMAX>(a, row, c, pre, lane, sweep, static_cast<uint32_t>(seed),
-                                          static_cast<uint32_t>(seed >> 32), a.tmask[sweep], a.thr[sweep] >= 0);
+                                          static_cast<uint32_t>(seed >> 32), a.tmask[sweep], a.thr[sweep] >= 0,
+                                          static_cast<uint32_t>(c), 0, spare, false);
     stage[warp][lane] = pack(xt);
   }
   __syncthreads();
@@ -648,14 +680,40 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
   } else {
     // 2a. this rank's share of the exact cut (evaluate.cpp:10-18) over the
     // edges between main vertices: every edge once, by its endpoint with the
-    // lower position, rank r counting the rows of its own main chunks
+    // lower position, rank r counting the rows of its own main chunks. The
+    // SELL rows are one flat stream of 32-cell groups (cell = one lane's 4
+    // entries; gchunk maps a group to its chunk), 4 groups in flight per
+    // warp, so a hub's long row is spread over many warps like any other
     const int nwarps = gridDim.x * (kNW - 1);
-    for (int c = blockIdx.x * (kNW - 1) + warp - 1; c < nmain; c += nwarps) {
-      if (c % W != rk) continue;
-      const int p = c * 32 + lane;
-      const unsigned sp = (pre(c) >> lane) & 1u;
-      const int c0 = __ldg(a.sell_off + c), groups = (__ldg(a.sell_off + c + 1) - c0) >> 5;
-      cut += chunk_cut<WK>(a, c0, groups, p, sp, lane, [tlo](int q, int pp) { return q > pp && q < tlo; }, pre);
+    const int ng = a.ngroups;
+    for (int g0 = blockIdx.x * (kNW - 1) + warp - 1; g0 < ng; g0 += 4 * nwarps) {
+      int cs[4];
+      int4 q4[4], w4[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int gi = g0 + j * nwarps;
+        cs[j] = gi < ng ? __ldg(a.gchunk + gi) : nmain;
+        if (cs[j] < nmain) {
+          q4[j] = __ldg(a.psell + static_cast<long long>(gi) * 32 + lane);
+          if (WK == 2) w4[j] = __ldg(a.sell_w + static_cast<long long>(gi) * 32 + lane);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int c = cs[j];
+        if (c >= nmain || c % W != rk) continue;
+        const int p = c * 32 + lane;
+        const unsigned sp = (pre(c) >> lane) & 1u;
+        const int xs[4] = {q4[j].x, q4[j].y, q4[j].z, q4[j].w};
+        const int ws[4] = {WK == 2 ? w4[j].x : 1, WK == 2 ? w4[j].y : 1, WK == 2 ? w4[j].z : 1,
+                           WK == 2 ? w4[j].w : 1};
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          const int q = WK == 1 ? (xs[t] & 0x7fffffff) : xs[t];
+          if (q > p && q < tlo && ((__funnelshift_r(pre(q >> 5), 0u, q) & 1u) != sp))
+            cut += WK == 0 ? 1 : WK == 1 ? (xs[t] < 0 ? -1 : 1) : ws[t];
+        }
+      }
     }
   }
   __syncthreads();

@@ -422,7 +422,16 @@ cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStrea
   return cudaStreamSynchronize(st);
 }
 
-cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, cudaStream_t st) {
+// group -> chunk map of the SELL rows: groups (32 int4 cells, one per lane)
+// sell_off[c] / 32 .. sell_off[c + 1] / 32 - 1 belong to chunk c
+__global__ void k_group_chunk(const int32_t* sell_off, int chunks, int32_t* gchunk) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= chunks) return;
+  for (int gi = sell_off[c] / 32; gi < sell_off[c + 1] / 32; gi++) gchunk[gi] = c;
+}
+
+cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, DevBuf& pgchunk,
+                              cudaStream_t st) {
   cudaError_t e;
   const int n = g.n;
   DevBuf pos;
@@ -433,6 +442,9 @@ cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psel
   k_inverse<<<blocks(n), kB, 0, st>>>(T.order.as<int32_t>(), g.off, n, pos.as<int32_t>(), pdeg.as<int32_t>());
   k_psell<<<1184, kB, 0, st>>>(T.sell.as<int32_t>(), cells, pos.as<int32_t>(), n, 32 * ((n + 31) / 32),
                                psell.as<int32_t>());
+  const int chunks = (n + 31) / 32;
+  if ((e = pgchunk.alloc((T.slots / 32 > 0 ? T.slots / 32 : 1) * sizeof(int32_t)))) return e;
+  k_group_chunk<<<blocks(chunks), kB, 0, st>>>(T.sell_off.as<int32_t>(), chunks, pgchunk.as<int32_t>());
   if ((e = cudaGetLastError())) return e;
   return cudaStreamSynchronize(st);
 }

@@ -57,9 +57,11 @@ cudaError_t upload_and_scan(const int64_t* offsets, const int32_t* nbr, const in
 cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout* L, cudaStream_t st);
 
 // K4 rows: the SELL layout with neighbour positions in the visit order
-// (padding -> position 32 * ceil(n / 32), a zero word), and the degree of the
-// vertex at every position.
-cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, cudaStream_t st);
+// (padding -> position 32 * ceil(n / 32), a zero word), the degree of the
+// vertex at every position, and the chunk of every 32-cell group (the
+// finishing kernel's flat cut pass).
+cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, DevBuf& pgchunk,
+                              cudaStream_t st);
 
 // K3 layout (see EvalLayout).
 cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout* L, cudaStream_t st);

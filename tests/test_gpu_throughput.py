@@ -5,7 +5,10 @@ is statistical against the exact mode / reference on the same seeds, with
 the tolerances written here:
   * best balanced cut over the seeds and mean cut no worse than the exact
     mode's by more than 0.5% of the exact mean cut;
-  * fraction of balanced runs (imbalance at the parity floor) >= exact - 2%;
+  * fraction of balanced runs (imbalance at the parity floor) >= exact - 2%,
+    over 4096 seeds (the two modes draw different random streams, so the
+    fractions are independent samples: at p ~ 0.94 the standard deviation of
+    their difference is 0.5% with 4096 seeds, 2.1% with 256);
   * the exact invariants hold every run: trace[-1] == final score, counter ==
     spin sum at every barrier (acceptance criterion 4), pf schedule exact.
 """
@@ -39,7 +42,7 @@ def test_throughput_quality_matches_exact(name):
     doc = golden_configs()[name]
     g = product_graph(doc["recipe"])
     prob = pi.MinCutProblem.with_default_coefficients(g)
-    seeds = np.arange(1, 257, dtype=np.uint64)
+    seeds = np.arange(1, 4097, dtype=np.uint64)
     k_ex, ex = run_mode(prob, True, seeds)
     k_th, th = run_mode(prob, False, seeds, trace=True)
     assert k_th.startswith("k2_"), k_th
