@@ -93,14 +93,14 @@ struct gdi_graph {
   std::mutex mu;
   bool thru_built = false, pipe_built = false, part_built = false, eval_built = false;
   ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
-  DevBuf psell, pdeg, pgchunk;  // K4: the SELL rows over visit-order positions, degree by position, group -> chunk
+  DevBuf psell, pdeg, pedges, pedge_w;  // K4: SELL rows over visit-order positions, degree by position, edges by position
   PipeLayout pipel;  // k1_window: window masks, forward masks, SELL rows
   PipeGraph pipe;    // k1_window view (ok = eligible; pointers once built)
   EvalLayout evl;    // K3: canonical edge list
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
-                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes + pgchunk.bytes +
+                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes + pedges.bytes + pedge_w.bytes +
                                 pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
                                 pipel.wsell_off.bytes + evl.edges.bytes + evl.w.bytes);
@@ -203,10 +203,18 @@ int ensure_part(gdi_graph* g) {
   if (g->part_built) return GDI_OK;
   cudaStream_t st = nullptr;
   GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const cudaError_t e = build_part_layout(g->csr(), g->thru, g->psell, g->pdeg, g->pgchunk, st);
+  const cudaError_t e = build_part_layout(g->csr(), g->thru, g->st.m, g->wkind, g->psell, g->pdeg, g->pedges, g->pedge_w, st);
   cudaStreamDestroy(st);
   GDI_CUDA(e);
   g->part_built = true;
+  return GDI_OK;
+}
+
+// K4 plan: the edges between main vertices for both tail lengths
+int part_splits(const gdi_graph* g, PartPlan* plan) {
+  const int nck = (g->st.n + 31) / 32;
+  GDI_CUDA(part_edges_below(g->pedges, g->st.m, 32 * (nck - plan->tail), &plan->m_main));
+  GDI_CUDA(part_edges_below(g->pedges, g->st.m, 32 * (nck - plan->tail_multi), &plan->m_main_multi));
   return GDI_OK;
 }
 
@@ -508,7 +516,7 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
     return fail(GDI_ERR_CAPACITY, "graph too large for the exact kernel's shared-memory spins");
   gdi_graph* gm = const_cast<gdi_graph*>(g);  // layouts are a lazily built cache
   if (s->use_thru && (rc = ensure_thru(gm))) return rc;
-  if (s->use_part && (rc = ensure_part(gm))) return rc;
+  if (s->use_part && ((rc = ensure_part(gm)) || (rc = part_splits(gm, &s->kplan)))) return rc;
   if (s->use_win && (rc = ensure_pipe(gm))) return rc;
 
   if (stream) {
@@ -681,8 +689,9 @@ int gdi_session_launch(gdi_session* s) {
       a.order = s->g->thru.order.as<int32_t>();
       a.psell = s->g->psell.as<int4>();
       a.pdeg = s->g->pdeg.as<int32_t>();
-      a.gchunk = s->g->pgchunk.as<int32_t>();
-      a.ngroups = static_cast<int32_t>(s->g->thru.slots / 32);
+      a.pedges = s->g->pedges.as<int2>();
+      a.pedge_w = s->g->pedge_w.as<int32_t>();
+      a.m_edges = s->g->st.m;
       a.sell_off = s->g->thru.sell_off.as<int32_t>();
       a.sell_w = s->g->thru.sell_w.as<int4>();
       a.chains = s->kplan.chains;
@@ -1059,7 +1068,7 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
     s->plan.warps = cw + refresher;
     s->plan.block = 32 * s->plan.warps;
   }
-  if ((rc = ensure_part(s->g))) return rc;
+  if ((rc = ensure_part(s->g)) || (rc = part_splits(s->g, &s->plan))) return rc;
   schedule(s->p, s->pf, s->thr, s->tmask);
   const size_t n = g->st.n, S = p->sweeps;
   GDI_CUDA(s->seeds.alloc(sizeof(uint64_t)));
@@ -1085,8 +1094,9 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
   a.order = g->thru.order.as<int32_t>();
   a.psell = g->psell.as<int4>();
   a.pdeg = g->pdeg.as<int32_t>();
-  a.gchunk = g->pgchunk.as<int32_t>();
-  a.ngroups = static_cast<int32_t>(g->thru.slots / 32);
+  a.pedges = g->pedges.as<int2>();
+  a.pedge_w = g->pedge_w.as<int32_t>();
+  a.m_edges = g->st.m;
   a.sell_off = g->thru.sell_off.as<int32_t>();
   a.sell_w = g->thru.sell_w.as<int4>();
   a.chains = s->plan.chains;

@@ -565,36 +565,50 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
   }
 }
 
-// This thread's share of the cut over a chunk's rows: the weights of the
-// entries q of lane l's row with keep(q, p_l) and spin(q) != spin(p_l). Rows
-// padded far beyond their own length (a hub's chunk) are walked warp per
-// vertex, as in long_rows (the partial sums are reduced by the caller).
-template <int WK, typename Keep, typename Word>
-__device__ __forceinline__ long long chunk_cut(const PartArgs& a, int c0, int groups, int p, unsigned sp, int lane,
-                                               Keep keep, Word word) {
+// This lane's share of the cut over edges [lo, hi) of the position-space
+// edge list (u | -1 weight in bit 31, v), warp w of nw warps taking the
+// 64-edge blocks w, w + nw, ... (lane = 2 edges of a block per load).
+template <int WK, typename Word>
+__device__ __forceinline__ long long edge_cut(const PartArgs& a, long long lo, long long hi, int w, int nw, int lane,
+                                              Word word) {
   long long cut = 0;
-  auto count = [&](int4 q4, int4 w4, int pp, unsigned ss) {
-    const int xs[4] = {q4.x, q4.y, q4.z, q4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
+  const int4* E = reinterpret_cast<const int4*>(a.pedges);
+  // [lo, hi) in edge pairs: an odd lo / hi is handled as a single edge
+  if (lo & 1) {
+    if (w == 0 && lane == 0 && lo < hi) {
+      const int2 e = __ldg(a.pedges + lo);
+      const int u = e.x & 0x7fffffff;
+      if (((word(u >> 5) >> (u & 31)) ^ (word(e.y >> 5) >> (e.y & 31))) & 1u)
+        cut += WK == 0 ? 1 : WK == 1 ? (e.x < 0 ? -1 : 1) : __ldg(a.pedge_w + lo);
+    }
+    lo++;
+  }
+  const long long q0 = lo >> 1, q1 = hi >> 1;  // int4 pairs [q0, q1); edge hi - 1 alone when hi is odd
+  const long long stride = static_cast<long long>(nw) * 32;
+  for (long long q = q0 + static_cast<long long>(w) * 32 + lane; q < q1; q += 4 * stride) {
+    int4 x[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      const int q = WK == 1 ? (xs[j] & 0x7fffffff) : xs[j];
-      if (keep(q, pp) && ((__funnelshift_r(word(q >> 5), 0u, q) & 1u) != ss))
-        cut += WK == 0 ? 1 : WK == 1 ? (xs[j] < 0 ? -1 : 1) : ws[j];
+      const long long qq = q + j * stride;
+      x[j] = qq < q1 ? __ldg(E + qq) : make_int4(0, 0, 0, 0);  // (edge (0, 0): never cut)
     }
-  };
-  if (groups <= kLaneRows + 2) {
-    for (int k = 0; k < groups; k++)
-      count(__ldg(a.psell + c0 + k * 32 + lane),
-            WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + lane) : make_int4(1, 1, 1, 1), p, sp);
-    return cut;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int us[2] = {x[j].x, x[j].z}, vs[2] = {x[j].y, x[j].w};
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const int u = us[t] & 0x7fffffff, v = vs[t];
+        if (((word(u >> 5) >> (u & 31)) ^ (word(v >> 5) >> (v & 31))) & 1u)
+          cut += WK == 0 ? 1 : WK == 1 ? (us[t] < 0 ? -1 : 1) : __ldg(a.pedge_w + 2 * (q + j * stride) + t);
+      }
+    }
   }
-  const int mine = p < a.g.n ? (__ldg(a.pdeg + p) + 3) / 4 : 0;
-  for (unsigned pend = __ballot_sync(FULL, mine > 0); pend != 0u; pend &= pend - 1u) {
-    const int l = __ffs(pend) - 1, gl = __shfl_sync(FULL, mine, l), pl = __shfl_sync(FULL, p, l);
-    const unsigned sl = __shfl_sync(FULL, sp, l);
-    for (int k = lane; k < gl; k += 32)
-      count(__ldg(a.psell + c0 + k * 32 + l), WK == 2 ? __ldg(a.sell_w + c0 + k * 32 + l) : make_int4(1, 1, 1, 1),
-            pl, sl);
+  if ((hi & 1) && hi - 1 >= lo && w == 0 && lane == 1) {
+    const long long e1 = hi - 1;
+    const int2 e = __ldg(a.pedges + e1);
+    const int u = e.x & 0x7fffffff;
+    if (((word(u >> 5) >> (u & 31)) ^ (word(e.y >> 5) >> (e.y & 31))) & 1u)
+      cut += WK == 0 ? 1 : WK == 1 ? (e.x < 0 ? -1 : 1) : __ldg(a.pedge_w + e1);
   }
   return cut;
 }
@@ -679,56 +693,18 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
     if (lane == 0) tail_delta = Gt - static_cast<int>(G0);
   } else {
     // 2a. this rank's share of the exact cut (evaluate.cpp:10-18) over the
-    // edges between main vertices: every edge once, by its endpoint with the
-    // lower position, rank r counting the rows of its own main chunks. The
-    // SELL rows are one flat stream of 32-cell groups (cell = one lane's 4
-    // entries; gchunk maps a group to its chunk), 4 groups in flight per
-    // warp, so a hub's long row is spread over many warps like any other
-    const int nwarps = gridDim.x * (kNW - 1);
-    const int ng = a.ngroups;
-    for (int g0 = blockIdx.x * (kNW - 1) + warp - 1; g0 < ng; g0 += 4 * nwarps) {
-      int cs[4];
-      int4 q4[4], w4[4];
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int gi = g0 + j * nwarps;
-        cs[j] = gi < ng ? __ldg(a.gchunk + gi) : nmain;
-        if (cs[j] < nmain) {
-          q4[j] = __ldg(a.psell + static_cast<long long>(gi) * 32 + lane);
-          if (WK == 2) w4[j] = __ldg(a.sell_w + static_cast<long long>(gi) * 32 + lane);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int c = cs[j];
-        if (c >= nmain || c % W != rk) continue;
-        const int p = c * 32 + lane;
-        const unsigned sp = (pre(c) >> lane) & 1u;
-        const int xs[4] = {q4[j].x, q4[j].y, q4[j].z, q4[j].w};
-        const int ws[4] = {WK == 2 ? w4[j].x : 1, WK == 2 ? w4[j].y : 1, WK == 2 ? w4[j].z : 1,
-                           WK == 2 ? w4[j].w : 1};
-#pragma unroll
-        for (int t = 0; t < 4; t++) {
-          const int q = WK == 1 ? (xs[t] & 0x7fffffff) : xs[t];
-          if (q > p && q < tlo && ((__funnelshift_r(pre(q >> 5), 0u, q) & 1u) != sp))
-            cut += WK == 0 ? 1 : WK == 1 ? (xs[t] < 0 ? -1 : 1) : ws[t];
-        }
-      }
-    }
+    // edges between main vertices: the prefix [0, m_main) of the
+    // position-space edge list (each edge once), rank r taking the r-th
+    // slice; two edges per 16-byte load, 4 loads in flight per lane
+    const long long lo = a.m_main * rk / W, hi = a.m_main * (rk + 1) / W;
+    cut += edge_cut<WK>(a, lo, hi, blockIdx.x * (kNW - 1) + warp - 1, gridDim.x * (kNW - 1), lane, pre);
   }
   __syncthreads();
   const int tot = tail_delta;
   auto word = [&](int wi) -> unsigned { return wi >= nmain && wi < nck ? tw[wi - nmain] : pre(wi); };
-  // 2b. the edges with a tail endpoint, from the tail rows (rank 0): to a
-  // main vertex always, to another tail vertex once (higher position)
-  if (rk == 0)
-    for (int t = blockIdx.x * kNW + warp; t < T; t += gridDim.x * kNW) {
-      const int c = nmain + t, p = c * 32 + lane;
-      const unsigned sp = (tw[t] >> lane) & 1u;
-      const int c0 = __ldg(a.sell_off + c), groups = (__ldg(a.sell_off + c + 1) - c0) >> 5;
-      cut += chunk_cut<WK>(
-          a, c0, groups, p, sp, lane, [tlo, zpos](int q, int pp) { return q < tlo || (q > pp && q != zpos); }, word);
-    }
+  // 2b. the edges with a tail endpoint (the rest of the list), after the
+  // tail is decided: rank 0
+  if (rk == 0) cut += edge_cut<WK>(a, a.m_main, a.m_edges, blockIdx.x * kNW + warp, gridDim.x * kNW, lane, word);
   // 3. the spin sum (global, on every rank), the unfused exchange's copy of the
   // other ranks' words for the next sweep, and the natural-order outputs
   const bool last_sweep = sweep + 1 == a.sweeps;
@@ -800,8 +776,8 @@ void pick_k(bool sm, PartPlan* plan) {
   plan->sweep_fn = !sm           ? reinterpret_cast<const void*>(&k4_sweep<WK, KMAX, 0>)
                    : plan->fresh ? reinterpret_cast<const void*>(&k4_sweep<WK, KMAX, 2>)
                                  : reinterpret_cast<const void*>(&k4_sweep<WK, KMAX, 1>);
-  plan->finish_fn = sm ? reinterpret_cast<const void*>(&k4_finish<WK, KMAX, true>)
-                       : reinterpret_cast<const void*>(&k4_finish<WK, KMAX, false>);
+  plan->finish_fn = plan->fin_smem > 0 ? reinterpret_cast<const void*>(&k4_finish<WK, KMAX, true>)
+                                       : reinterpret_cast<const void*>(&k4_finish<WK, KMAX, false>);
 }
 
 // (the register bucket is at most 2 int4 groups, 1 with a weight array: at
@@ -887,6 +863,8 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
     plan->tail = plan->tail_multi = t < 0 ? 0 : t > kTailMax ? kTailMax : t > nck / 8 ? nck / 8 : t;
   }
   plan->warps = cw + (plan->refresh != 0 ? 1 : 0);
+  plan->fin_smem = plan->smem;
+  if (const char* e = std::getenv("GDI_K4_FIN_COPY")) plan->fin_smem = std::atoi(e) ? plan->smem : 0;  // A/B
   if (wkind == 0)
     pick<0>(kmax, plan->smem_copy, plan);
   else if (wkind == 1)
@@ -896,14 +874,15 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->block = 32 * plan->warps;
   // finishing CTAs: one per SM with the shared copy (each copies the words),
   // else up to two per SM
-  const int fg = (nck + kNW - 1) / kNW, fmax = ((plan->smem_copy ? 148 : 296) + R - 1) / R;
+  const int fg = (nck + kNW - 1) / kNW, fmax = (148 + R - 1) / R;  // (64 registers x 1024 threads: 1 CTA per SM)
   plan->fin_block = 32 * kNW;
   plan->fin_grid = fg < fmax ? fg : fmax;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
   if (plan->smem > 48 * 1024 &&
       (cudaFuncSetAttribute(plan->sweep_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem) != cudaSuccess ||
-       cudaFuncSetAttribute(plan->finish_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem) != cudaSuccess))
+       (plan->fin_smem > 0 && cudaFuncSetAttribute(plan->finish_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   plan->fin_smem) != cudaSuccess)))
     return -1;
   plan->name = wkind == 0 ? "k4_sweep<unit>" : wkind == 1 ? "k4_sweep<pm1>" : "k4_sweep<weighted>";
   return 0;
@@ -918,6 +897,7 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   a.a4 = plan.a4;
   a.b = plan.b;
   a.tail = a.world == 1 ? plan.tail : plan.tail_multi;
+  a.m_main = a.world == 1 ? plan.m_main : plan.m_main_multi;
   a.cta_tail = plan.cta_tail;
   a.nwp = plan.nwp;
   a.refresh = plan.refresh;
@@ -956,7 +936,8 @@ cudaError_t part_finish_launch(const PartPlan& plan, const PartArgs& args, int s
   a.sweep = sweep;
   const unsigned char* rv = static_cast<const unsigned char*>(recv);
   void* p[] = {&a, &rv, &stride, &spins_out};
-  return cudaLaunchKernel(plan.finish_fn, dim3(plan.fin_grid, a.replicas), dim3(plan.fin_block), p, plan.smem, stream);
+  return cudaLaunchKernel(plan.finish_fn, dim3(plan.fin_grid, a.replicas), dim3(plan.fin_block), p, plan.fin_smem,
+                          stream);
 }
 
 long long part_exchange_bytes(int n, int world, bool peer) {

@@ -129,8 +129,9 @@ struct PartArgs {
   const int32_t* order;            // [n] position -> vertex (degree-binned visit order)
   const int4* psell;               // SELL-32 rows over positions (layout.hpp build_part_layout)
   const int32_t* pdeg;             // [n] degree of the vertex at each position
-  const int32_t* gchunk;           // [ngroups] chunk of each 32-cell SELL group
-  int32_t ngroups;
+  const int2* pedges;              // [m] canonical edges in position space, sorted by the larger position
+  const int32_t* pedge_w;          // [m] their weights (general graphs) or nullptr
+  long long m_edges, m_main;       // edges; those between main vertices (a prefix of pedges)
   const int32_t* sell_off;         // [chunks+1] in int4 units
   const int4* sell_w;              // nullptr unless general weights
   int32_t nwp;                     // spin words per replica: chunks + 1 zero word, padded to 4

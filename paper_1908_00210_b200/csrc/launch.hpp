@@ -111,6 +111,8 @@ struct PartPlan {
   int fin_grid = 1;    // finishing CTAs per replica
   int nwp = 0;         // spin words per replica (part_words)
   int smem = 0;        // dynamic shared memory of the sweep kernel (the spin copy)
+  int fin_smem = 0;    // dynamic shared memory of the finishing kernel (0: lookups through L1)
+  long long m_main = 0, m_main_multi = 0;  // position-space edges between main vertices (tail / tail_multi)
   bool smem_copy = false;
   int refresh = 1;     // 1: a refresher warp keeps re-copying the shared spin copy (0: never)
   int fresh = 0;       // 1: the last two bands of chunks read from the global words (k4_sweep SMODE 2)

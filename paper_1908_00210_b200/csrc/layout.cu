@@ -422,16 +422,32 @@ cudaError_t build_pipe_layout(const DevCsr& g, int win, PipeLayout* L, cudaStrea
   return cudaStreamSynchronize(st);
 }
 
-// group -> chunk map of the SELL rows: groups (32 int4 cells, one per lane)
-// sell_off[c] / 32 .. sell_off[c + 1] / 32 - 1 belong to chunk c
-__global__ void k_group_chunk(const int32_t* sell_off, int chunks, int32_t* gchunk) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= chunks) return;
-  for (int gi = sell_off[c] / 32; gi < sell_off[c + 1] / 32; gi++) gchunk[gi] = c;
+// position-space canonical edges (K4 finishing kernel's cut): edge i of the
+// u < v list as (min position | -1 weight in bit 31, max position), keyed
+// for a sort by the larger position
+__global__ void k_pedge_keys(const int2* edges, long long m, const int32_t* pos, int32_t* key, int32_t* idx) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int2 e = edges[i];
+    key[i] = max(pos[e.x], pos[e.y]);
+    idx[i] = static_cast<int32_t>(i);
+  }
+}
+__global__ void k_pedge_fill(const int2* edges, const int32_t* ew, long long m, const int32_t* pos,
+                             const int32_t* idx, int wkind, int2* pedges, int32_t* pw) {
+  for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j < m;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = idx[j];
+    const int2 e = edges[i];
+    const int a = pos[e.x], b = pos[e.y];
+    const int w = ew ? ew[i] : 1;
+    pedges[j] = make_int2(min(a, b) | (wkind == 1 && w < 0 ? static_cast<int>(0x80000000u) : 0), max(a, b));
+    if (pw) pw[j] = w;
+  }
 }
 
-cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, DevBuf& pgchunk,
-                              cudaStream_t st) {
+cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, long long m, int wkind, DevBuf& psell,
+                              DevBuf& pdeg, DevBuf& pedges, DevBuf& pedge_w, cudaStream_t st) {
   cudaError_t e;
   const int n = g.n;
   DevBuf pos;
@@ -442,11 +458,62 @@ cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psel
   k_inverse<<<blocks(n), kB, 0, st>>>(T.order.as<int32_t>(), g.off, n, pos.as<int32_t>(), pdeg.as<int32_t>());
   k_psell<<<1184, kB, 0, st>>>(T.sell.as<int32_t>(), cells, pos.as<int32_t>(), n, 32 * ((n + 31) / 32),
                                psell.as<int32_t>());
-  const int chunks = (n + 31) / 32;
-  if ((e = pgchunk.alloc((T.slots / 32 > 0 ? T.slots / 32 : 1) * sizeof(int32_t)))) return e;
-  k_group_chunk<<<blocks(chunks), kB, 0, st>>>(T.sell_off.as<int32_t>(), chunks, pgchunk.as<int32_t>());
+  // edges sorted by their larger position: those between main vertices form
+  // a prefix for any tail length
+  const long long mm = m > 0 ? m : 1;
+  DevBuf key, key_s, idx, idx_s;
+  if ((e = key.alloc(mm * 4)) || (e = key_s.alloc(mm * 4)) || (e = idx.alloc(mm * 4)) || (e = idx_s.alloc(mm * 4)) ||
+      (e = pedges.alloc(mm * sizeof(int2))))
+    return e;
+  if (wkind == 2) {
+    if ((e = pedge_w.alloc(mm * 4))) return e;
+  } else {
+    pedge_w.reset();
+  }
+  if (m > 0) {
+    k_pedge_keys<<<1184, kB, 0, st>>>(T.edges.as<int2>(), m, pos.as<int32_t>(), key.as<int32_t>(), idx.as<int32_t>());
+    size_t bytes = 0;
+    int bits = 1;
+    while (bits < 31 && (1LL << bits) <= n) bits++;
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.as<int32_t>(), key_s.as<int32_t>(), idx.as<int32_t>(),
+                                             idx_s.as<int32_t>(), static_cast<int>(m), 0, bits, st)))
+      return e;
+    DevBuf tmp;
+    if ((e = tmp.alloc(bytes))) return e;
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.as<int32_t>(), key_s.as<int32_t>(), idx.as<int32_t>(),
+                                             idx_s.as<int32_t>(), static_cast<int>(m), 0, bits, st)))
+      return e;
+    k_pedge_fill<<<1184, kB, 0, st>>>(T.edges.as<int2>(), wkind != 0 ? T.edge_w.as<int32_t>() : nullptr, m,
+                                      pos.as<int32_t>(), idx_s.as<int32_t>(), wkind, pedges.as<int2>(),
+                                      wkind == 2 ? pedge_w.as<int32_t>() : nullptr);
+    if ((e = cudaGetLastError())) return e;
+    if ((e = cudaStreamSynchronize(st))) return e;  // (tmp is released on return)
+  }
   if ((e = cudaGetLastError())) return e;
   return cudaStreamSynchronize(st);
+}
+
+// edges of a position-sorted list with larger position < lim (one thread: a
+// binary search)
+__global__ void k_count_below(const int2* pedges, long long m, int lim, long long* out) {
+  long long lo = 0, hi = m;
+  while (lo < hi) {
+    const long long mid = (lo + hi) / 2;
+    if (pedges[mid].y < lim)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  *out = lo;
+}
+
+cudaError_t part_edges_below(const DevBuf& pedges, long long m, int lim, long long* count) {
+  DevBuf d;
+  cudaError_t e;
+  if ((e = d.alloc(sizeof(long long)))) return e;
+  k_count_below<<<1, 1>>>(pedges.as<int2>(), m, lim, d.as<long long>());
+  if ((e = cudaGetLastError())) return e;
+  return cudaMemcpy(count, d.p, sizeof(long long), cudaMemcpyDeviceToHost);
 }
 
 cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout* L, cudaStream_t st) {

@@ -58,10 +58,13 @@ cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout*
 
 // K4 rows: the SELL layout with neighbour positions in the visit order
 // (padding -> position 32 * ceil(n / 32), a zero word), the degree of the
-// vertex at every position, and the chunk of every 32-cell group (the
-// finishing kernel's flat cut pass).
-cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, DevBuf& psell, DevBuf& pdeg, DevBuf& pgchunk,
-                              cudaStream_t st);
+// vertex at every position, and the canonical edges in position space (min
+// position | -1 weight in bit 31, max position) sorted by the larger
+// position (+ weights for general graphs): the finishing kernel's cut pass.
+cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, long long m, int wkind, DevBuf& psell,
+                              DevBuf& pdeg, DevBuf& pedges, DevBuf& pedge_w, cudaStream_t st);
+// number of position-space edges whose larger position is < lim
+cudaError_t part_edges_below(const DevBuf& pedges, long long m, int lim, long long* count);
 
 // K3 layout (see EvalLayout).
 cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout* L, cudaStream_t st);
