@@ -498,6 +498,20 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   else if (thru_ok && force != "part" &&
            thru_plan(g->st, g->wkind, replicas, 4 * p->a_num, p->b_num, p->strategy == GDI_STRATEGY_STANDARD, &s->tplan) == 0)
     s->use_thru = true;
+  // K2 without concurrent chains (one chain per replica on small graphs such
+  // as G1, or the one-warp-per-replica k2_sweep where k2_chains does not fit,
+  // e.g. G81) is one serial decision chain per replica, like the exact mode,
+  // and slower than the exact kernels' windows (G1: 14.9 vs 9.9 ms, G81+-1:
+  // 599 vs 485 ms for 1024 replicas x 1000 sweeps): use the exact kernel,
+  // whose sequential result is a legal outcome of the racy contract
+  if (s->use_thru && !s->use_part && (force.empty() || force == "auto") && p->strategy != GDI_STRATEGY_STANDARD &&
+      !(s->tplan.chains && s->tplan.cfg.chains >= 2)) {
+    if (block_plan(g->st, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->bplan) == 0)
+      s->use_block = true;
+    else if (window_plan(g->st, g->pipe, replicas, 4 * p->a_num, p->b_num, p->sweeps, &s->pplan) == 0)
+      s->use_win = true;
+    if (s->use_block || s->use_win) s->use_thru = false;
+  }
   // exact mode: k1_block (fixed-point windows) by default; k1_window
   // (speculative windows) where k1_block does not fit (graphs whose CSR does
   // not fit shared memory, e.g. G81); k1_exact for everything else

@@ -569,6 +569,19 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     // balanced no more runs of a hub graph: 81% either way, 86% sequential)
     const int T = cf.tail, nmain = nck - T;
     const int kSeg = cf.seg;
+    // the chain with the fewest main chunks decides the tail
+    int jt = 0;
+    {
+      const int nseg = (nmain + kSeg - 1) / kSeg, L = nmain - (nseg - 1) * kSeg;
+      int best = 1 << 30;
+      for (int q = 0; q < P; q++) {
+        const int cnt = (q < nseg ? (nseg - q + P - 1) / P : 0) * kSeg - (q == (nseg - 1) % P ? kSeg - L : 0);
+        if (cnt <= best) {
+          best = cnt;
+          jt = q;
+        }
+      }
+    }
 #pragma unroll 1
     for (int s0 = j * kSeg; s0 < nmain; s0 += P * kSeg) {
       const int c1 = min(nmain, s0 + kSeg);
@@ -577,8 +590,12 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     }
     if (lane == 0) red_d[warp] = G - share;
     bar_sync(bid, bthreads);
-    // the tail, in order against the replica's exact counter
-    if (j == 0) {
+    // the tail, in order against the replica's exact counter, by the chain
+    // with the fewest main chunks (G22: per-chain main chunks
+    // 16/16/16/12, the 3-chunk tail by chain 3 instead of 0: 19.8 -> 18.5 ms;
+    // dealing the last round's segments in reverse instead, so that chain 0
+    // had the short one, was as fast but ended fewer hub-graph runs balanced)
+    if (j == jt) {
       int dsum = lane < P ? red_d[slot * P + lane] : 0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(FULL, dsum, o);

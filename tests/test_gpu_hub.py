@@ -75,7 +75,10 @@ def test_hub_pooled_invariants_and_quality(hub, big_hub, kernel, replicas, monke
     correct (imbalance ~100 of 100k after 200 sweeps; K4)."""
     g = hub[0] if kernel == "k2" else big_hub
     prob = pi.MinCutProblem.with_default_coefficients(g)
-    seeds = np.arange(1, replicas + 1, dtype=np.uint64)
+    # k2: three sessions of 256 replicas (the shape that runs k2_chains),
+    # seeds 1..768: the balanced fraction of 256 runs varies by +-2.5% from
+    # run to run (racy chains), so the comparison pools 768
+    blocks = 3 if kernel == "k2" else 1
     res = {}
     for det in (True, False):
         p = pi.AnnealParams()
@@ -84,11 +87,14 @@ def test_hub_pooled_invariants_and_quality(hub, big_hub, kernel, replicas, monke
             p.deterministic = True
         else:
             p.workers = 8
-        s = pi.Session(prob, p, replicas, trace=True)
-        s.set_seeds(seeds)
-        s.launch()
-        s.sync()
-        res[det] = (s.kernel, s.fetch(spins=True, trace=True))
+        outs = []
+        for b in range(blocks):
+            s = pi.Session(prob, p, replicas, trace=True)
+            s.set_seeds(np.arange(1 + b * replicas, 1 + (b + 1) * replicas, dtype=np.uint64))
+            s.launch()
+            s.sync()
+            outs.append(s.fetch(spins=True, trace=True))
+        res[det] = (s.kernel, {k: np.concatenate([o[k] for o in outs]) for k in outs[0] if np.ndim(outs[0][k]) > 0})
     kern, th = res[False]
     assert kern.startswith("k4_sweep" if kernel == "k4" else "k2_chains"), kern
     sums = th["spins"].astype(np.int64).sum(1)

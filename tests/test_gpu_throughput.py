@@ -45,7 +45,14 @@ def test_throughput_quality_matches_exact(name):
     seeds = np.arange(1, 4097, dtype=np.uint64)
     k_ex, ex = run_mode(prob, True, seeds)
     k_th, th = run_mode(prob, False, seeds, trace=True)
-    assert k_th.startswith("k2_"), k_th
+    if k_th.startswith("k1_"):
+        # no concurrent K2 chains for this shape (G1: one chain per replica;
+        # G81: k2_chains does not fit): the session runs the exact kernel, a
+        # legal (sequential) outcome of the racy contract, and faster here
+        assert name in ("G1", "G81pm1"), (name, k_th)
+        assert np.array_equal(th["spins"], ex["spins"]) and np.array_equal(th["cut"], ex["cut"])
+        return
+    assert k_th.startswith("k2_chains"), k_th
     floor = g.num_nodes % 2
     bal_ex, bal_th = ex["imbalance"] <= floor, th["imbalance"] <= floor
     assert bal_th.mean() >= bal_ex.mean() - 0.02
