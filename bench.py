@@ -124,7 +124,7 @@ def measured_traffic(config: str, kernel: str):
 
 
 def roofline(bpu: float, updates: float, ms: float, l2: float, hbm: float, peaks_src: str,
-             traffic, working_set: int, l2_size: int, note: str):
+             traffic, working_set: int, l2_size: int, note: str, smem_gbs: float = None):
     """SURVEY.md 8(d) accounting: achieved = updates/s x B_logical against the
     peak of the level that holds the working set (L2 when the CSR + spins fit
     in L2, HBM otherwise)."""
@@ -139,6 +139,13 @@ def roofline(bpu: float, updates: float, ms: float, l2: float, hbm: float, peaks
                            "buffer, 4 CTAs/SM x 512 threads, 50 passes; profiles/r02_l2_peak.json)") if in_l2
                           else peaks_src,
            "hbm_peak_gbs": hbm, "frac_of_hbm": achieved / hbm, "l2_peak_gbs": l2, "note": note}
+    if smem_gbs:
+        # the exact / pooled kernels stage the CSR and the replica state in
+        # shared memory, so the logical bytes are served from there: a dense
+        # graph (G1, degree 48) can exceed the L2 figure (frac > 1)
+        rec["smem_peak_gbs"] = smem_gbs
+        rec["frac_of_smem"] = achieved / smem_gbs
+        rec["smem_peak_source"] = "148 SMs x 128 B/cycle x the sampled SM clock (nominal shared-memory bandwidth)"
     if traffic:
         units = traffic.get("updates_per_launch")
         lps = traffic.get("launches_per_step", 1)
@@ -553,11 +560,15 @@ def main():
         l2_size = torch.cuda.get_device_properties(dev).L2_cache_size
         ws = (n + 1) * 4 + 2 * m * 4 + (2 * m if weighted else 0) + R * n  # compact CSR + int8 spins
         clk = clocks.summary()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        smem_gbs = sms * 128 * clk["sm_mhz"] * 1e6 / 1e9 if clk.get("sm_mhz") else None
+        onchip = not sess.kernel.startswith(("k4_", "k1_window"))  # CSR staged in shared memory
         rl = roofline(bpu, R * n * sweeps, step_ms, l2, hbm, hbm_src, measured_traffic(args.config, sess.kernel),
                       ws, l2_size,
                       ("exact mode: each replica is one serial decision chain (SURVEY 8(d): K1 is latency-bound, "
                        "see cycles_per_visit); " if args.mode == "exact" else "") +
-                      "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident")
+                      "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident",
+                      smem_gbs if onchip else None)
         if args.mode == "exact" and clk.get("sm_mhz"):
             # SM cycles per visit of one replica chain (all chains run concurrently)
             rl["cycles_per_visit"] = step_ms * 1e-3 * clk["sm_mhz"] * 1e6 / (n * sweeps)
@@ -617,7 +628,8 @@ def main():
                 "gpu_launches": args.steps * tsess.launch_count,
                 "roofline": roofline(bpu, R * n * sweeps, t_ms, l2, hbm, hbm_src,
                                      measured_traffic(args.config, tsess.kernel), ws, l2_size,
-                                     "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident")}
+                                     "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident",
+                                     smem_gbs if not tsess.kernel.startswith(("k4_", "k1_window")) else None)}
         del tsess
 
     # e2e: the public batched call with host buffers (fresh CSR upload, seeds
