@@ -91,19 +91,20 @@ struct gdi_graph {
   int wkind = 0;  // 0 unit, 1 +-1 (sign bit), 2 general
   // kernel layouts, built on the device the first time a session needs one
   std::mutex mu;
-  bool thru_built = false, pipe_built = false, part_built = false, eval_built = false;
+  bool thru_built = false, pipe_built = false, part_built = false, eval_built = false, brow_built = false;
   ThruLayout thru;   // K2/K4: degree-binned order, SELL-32 rows, edge list
   DevBuf psell, pdeg, pedges, pedge_w;  // K4: SELL rows over visit-order positions, degree by position, edges by position
   PipeLayout pipel;  // k1_window: window masks, forward masks, SELL rows
   PipeGraph pipe;    // k1_window view (ok = eligible; pointers once built)
   EvalLayout evl;    // K3: canonical edge list
+  DevBuf brow;       // k1_block row records (rows variant)
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
                                 thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes + pedges.bytes + pedge_w.bytes +
                                 pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
-                                pipel.wsell_off.bytes + evl.edges.bytes + evl.w.bytes);
+                                pipel.wsell_off.bytes + evl.edges.bytes + evl.w.bytes + brow.bytes);
   }
 };
 
@@ -215,6 +216,19 @@ int part_splits(const gdi_graph* g, PartPlan* plan) {
   const int nck = (g->st.n + 31) / 32;
   GDI_CUDA(part_edges_below(g->pedges, g->st.m, 32 * (nck - plan->tail), &plan->m_main));
   GDI_CUDA(part_edges_below(g->pedges, g->st.m, 32 * (nck - plan->tail_multi), &plan->m_main_multi));
+  return GDI_OK;
+}
+
+// k1_block row records
+int ensure_brow(gdi_graph* g) {
+  std::lock_guard<std::mutex> lock(g->mu);
+  if (g->brow_built) return GDI_OK;
+  cudaStream_t st = nullptr;
+  GDI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const cudaError_t e = build_block_rows(g->csr(), g->brow, st);
+  cudaStreamDestroy(st);
+  GDI_CUDA(e);
+  g->brow_built = true;
   return GDI_OK;
 }
 
@@ -532,6 +546,7 @@ int session_create(const gdi_graph* g, const gdi_params* p, int32_t replicas, vo
   if (s->use_thru && (rc = ensure_thru(gm))) return rc;
   if (s->use_part && ((rc = ensure_part(gm)) || (rc = part_splits(gm, &s->kplan)))) return rc;
   if (s->use_win && (rc = ensure_pipe(gm))) return rc;
+  if (s->use_block && s->bplan.rows && (rc = ensure_brow(gm))) return rc;
 
   if (stream) {
     s->stream = static_cast<cudaStream_t>(stream);
@@ -811,6 +826,7 @@ int gdi_session_launch(gdi_session* s) {
   }
   ExactArgs a{};
   a.g = s->g->csr();
+  a.brow = s->g->brow.as<uint4>();
   a.n_pad = s->plan.n_pad;
   a.sweeps = s->p.sweeps;
   a.replicas = s->replicas;

@@ -40,6 +40,7 @@
 // producer warp, no inter-warp synchronisation after the prologue.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -65,14 +66,16 @@ __device__ __forceinline__ int ring_phys(int li) { return kTail + li + (li >> 5)
 
 struct BlkLayout {
   int jt, maskp, maskn, off, col, rep, rep_bytes, ring, words, fields, total;
-  __host__ __device__ static BlkLayout make(int n, int nnz, int rc, int fb, bool sgn) {
+  // rows > 0: the graph stays in global memory (row records, jump table), only
+  // the replicas' state is in shared memory
+  __host__ __device__ static BlkLayout make(int n, int nnz, int rc, int fb, bool sgn, int rows = 0) {
     BlkLayout L;
     L.jt = 0;                                   // 64 x 4 x 16 uint2 = 32 KB
-    L.maskp = L.jt + 64 * 4 * 16 * 8;
-    L.maskn = L.maskp + n * 4;
-    L.off = L.maskn + (sgn ? n * 4 : 0);
-    L.col = L.off + (n + 1) * 4;
-    L.rep = (L.col + nnz * 2 + 15) & ~15;
+    L.maskp = L.jt + (rows ? 0 : 64 * 4 * 16 * 8);
+    L.maskn = L.maskp + (rows ? 0 : n * 4);
+    L.off = L.maskn + (sgn && !rows ? n * 4 : 0);
+    L.col = L.off + (rows ? 0 : (n + 1) * 4);
+    L.rep = (L.col + (rows ? 0 : nnz * 2) + 15) & ~15;
     const int nw = (n + 31) / 32;
     L.ring = 0;
     L.words = kRingElems * 8;
@@ -86,6 +89,7 @@ struct BlkLayout {
 
 struct BlockArgs {
   DevCsr g;
+  const uint4* brow;  // ROWS: per vertex {maskp, maskn, cols 0-1, cols 2-3} (build_block_rows)
   int32_t nnz;
   int32_t sweeps, replicas, rc;
   const uint64_t* seeds;
@@ -150,13 +154,19 @@ __device__ __forceinline__ void field_add(unsigned char* fld, int t, int dv) {
     atomicAdd(w + (t >> 1), static_cast<unsigned>(dv) << ((t & 1) * 16));
 }
 
-template <bool SIGNED, bool UNITAB, int FB>
+// ROWS (= 4): graphs whose CSR and window masks do not fit shared memory
+// next to the replicas (G81+-1: 20000 vertices), with max degree <= 4: each
+// vertex's window masks and its (<= 4) 16-bit columns form one 16-byte row
+// record in global memory, loaded two windows ahead into registers; a
+// change scatters from the changed lane's record (shuffled to KD lanes per
+// change, 32 / KD changes per pass); the jump table is read through L1.
+template <bool SIGNED, bool UNITAB, int FB, int ROWS>
 __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.g.n, nnz = a.nnz;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const BlkLayout L = BlkLayout::make(n, nnz, a.rc, FB, SIGNED);
-  uint2* jt = reinterpret_cast<uint2*>(smem + L.jt);
+  const BlkLayout L = BlkLayout::make(n, nnz, a.rc, FB, SIGNED, ROWS);
+  uint2* jt = ROWS ? const_cast<uint2*>(a.jump) : reinterpret_cast<uint2*>(smem + L.jt);
   uint32_t* maskp = reinterpret_cast<uint32_t*>(smem + L.maskp);
   uint32_t* maskn = reinterpret_cast<uint32_t*>(smem + L.maskn);
   int32_t* offs = reinterpret_cast<int32_t*>(smem + L.off);
@@ -164,6 +174,7 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
   const unsigned FULL = 0xffffffffu;
 
   // ---- prologue (whole CTA): jump table, CSR, in-window masks ----
+  if (!ROWS) {
   for (int i = threadIdx.x; i < 64 * 4 * 16; i += blockDim.x) jt[i] = __ldg(a.jump + i);
   for (int i = threadIdx.x; i <= n; i += blockDim.x) offs[i] = __ldg(a.g.off + i);
   for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
@@ -186,6 +197,7 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
     }
     maskp[v] = mp;
     if (SIGNED) maskn[v] = mn;
+  }
   }
   __syncthreads();
 
@@ -224,13 +236,23 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
   for (int u = lane; u < n; u += 32) {
     const int su = spin(u);
     int acc = 0;
-    for (int e = offs[u]; e < offs[u + 1]; e++) {
-      const int c = cols[e];
+    auto entry = [&](int c) {
       const int v = SIGNED ? (c & 0x7fff) : c;
       const int wt = SIGNED && (c & 0x8000) ? -1 : 1;
       const int sv = spin(v);
       acc += wt * sv;
       if (v > u && sv != su) cut += wt;
+    };
+    if (ROWS) {
+      const uint4 rr = __ldg(a.brow + u);
+      const unsigned cw[2] = {rr.z, rr.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const unsigned c = (cw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        if (c != 0xffffu) entry(static_cast<int>(c));
+      }
+    } else {
+      for (int e = offs[u]; e < offs[u + 1]; e++) entry(cols[e]);
     }
     if (FB == 1)
       fld[u] = static_cast<unsigned char>(acc + 128);
@@ -256,6 +278,18 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
   const unsigned lt = (1u << lane) - 1u;
   const int nn = __shfl_sync(FULL, n, 0);
   const int nsw = __shfl_sync(FULL, sweeps, 0);
+  // ROWS: row records of the current window and the next (loaded two
+  // windows ahead; the windows repeat sweep after sweep)
+  const int nwin32 = ((nn + 31) >> 5) << 5;
+  auto ldrow = [&](int w0) -> uint4 {
+    const int vv = w0 + lane;
+    return vv < nn ? __ldg(a.brow + vv) : make_uint4(0u, 0u, 0xffffffffu, 0xffffffffu);
+  };
+  uint4 rw0 = make_uint4(0u, 0u, 0u, 0u), rw1 = rw0;
+  if (ROWS) {
+    rw0 = ldrow(0);
+    rw1 = ldrow(32 % nwin32);
+  }
 
 #pragma unroll 1
   for (int sweep = 0; sweep < nsw; sweep++) {
@@ -284,7 +318,14 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
       const int own = ((word >> lane) & 1u) ? 1 : -1;
       int f0 = 0;
       uint32_t wp = 0u, wn = 0u;
-      if (act) {
+      uint4 rcur = rw0;
+      if (ROWS) {
+        rw0 = rw1;
+        rw1 = ldrow((i0 + 64) % nwin32);
+        wp = rcur.x;
+        if (SIGNED) wn = rcur.y;
+        if (act) f0 = field_at<FB>(fld, v);
+      } else if (act) {
         f0 = field_at<FB>(fld, v);
         wp = maskp[v];
         if (SIGNED) wn = maskn[v];
@@ -335,6 +376,30 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
         if (lane == 0) words[i0 >> 5] = nwd;
         AG += (UNITAB ? 2 : 2 * a4) * (__popc(U) - __popc(D));
         if (act && fin != own) dcut += fin > own ? -f : f;
+        if (ROWS) {
+          // the changed lanes' records: KD = 4 lanes per change (lane 4s + k
+          // takes column k of the s-th changed lane), 8 changes per pass
+          unsigned C = U | D;
+          const int sl = lane >> 2, k = lane & 3;
+#pragma unroll 1
+          do {
+            const int cnt = __popc(C);
+            const int cl = sl < cnt ? static_cast<int>(__fns(C, 0u, sl + 1)) : lane;
+            const unsigned cz = __shfl_sync(FULL, rcur.z, cl), cw = __shfl_sync(FULL, rcur.w, cl);
+            const unsigned c = ((k < 2 ? cz : cw) >> (16 * (k & 1))) & 0xffffu;
+            if (sl < cnt && c != 0xffffu) {
+              const int dv = ((U >> cl) & 1u) ? 2 : -2;
+              if (SIGNED)
+                field_add<FB>(fld, static_cast<int>(c & 0x7fffu), (c & 0x8000u) ? -dv : dv);
+              else
+                field_add<FB>(fld, static_cast<int>(c), dv);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; t++) C &= C - 1u;
+          } while (C);
+          __syncwarp();
+          continue;
+        }
         // row bounds of every changed lane in one round trip, then one pass
         // per change with the lanes over its row (rows of <= 64 entries in
         // two predicated steps)
@@ -386,9 +451,12 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
 }
 
 template <bool S, bool U>
-const void* blk_fn(int fb) {
-  return fb == 1 ? reinterpret_cast<const void*>(&k1_block<S, U, 1>)
-                 : reinterpret_cast<const void*>(&k1_block<S, U, 2>);
+const void* blk_fn(int fb, int rows) {
+  if (rows)
+    return fb == 1 ? reinterpret_cast<const void*>(&k1_block<S, U, 1, 4>)
+                   : reinterpret_cast<const void*>(&k1_block<S, U, 2, 4>);
+  return fb == 1 ? reinterpret_cast<const void*>(&k1_block<S, U, 1, 0>)
+                 : reinterpret_cast<const void*>(&k1_block<S, U, 2, 0>);
 }
 
 }  // namespace
@@ -427,20 +495,31 @@ int block_plan(const GraphStats& st, int32_t replicas, int64_t a4, int64_t b, in
   int rc = (replicas + 147) / 148;
   rc = rc < 1 ? 1 : rc > 16 ? 16 : rc;
   const int cap = 227 * 1024;
-  if (BlkLayout::make(st.n, nnz, rc, fb, sgn).total > cap) return -1;
+  // the CSR and window masks in shared memory next to the replicas, else
+  // (degree <= 4) row records in global memory (ROWS)
+  int rows = 0;
+  if (BlkLayout::make(st.n, nnz, rc, fb, sgn).total > cap) {
+    if (st.max_degree > 4 || BlkLayout::make(st.n, nnz, rc, fb, sgn, 4).total > cap) return -1;
+    rows = 4;
+  }
+  if (const char* e = std::getenv("GDI_BLOCK_ROWS"))  // tests: force the row-record variant
+    if (std::atoi(e) != 0 && st.max_degree <= 4 && BlkLayout::make(st.n, nnz, rc, fb, sgn, 4).total <= cap) rows = 4;
   const bool unitab = ra == 1 && rb == 1;
-  plan->fn = sgn ? (unitab ? blk_fn<true, true>(fb) : blk_fn<true, false>(fb))
-                 : (unitab ? blk_fn<false, true>(fb) : blk_fn<false, false>(fb));
+  plan->fn = sgn ? (unitab ? blk_fn<true, true>(fb, rows) : blk_fn<true, false>(fb, rows))
+                 : (unitab ? blk_fn<false, true>(fb, rows) : blk_fn<false, false>(fb, rows));
+  plan->rows = rows;
   plan->rc = rc;
   plan->block = 32 * rc;
   plan->grid = (replicas + rc - 1) / rc;
-  plan->smem = BlkLayout::make(st.n, nnz, rc, fb, sgn).total;
+  plan->smem = BlkLayout::make(st.n, nnz, rc, fb, sgn, rows).total;
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
   plan->nnz = nnz;
-  static const char* names[2][2] = {{"k1_block<signed>", "k1_block<signed,ab=1>"},
-                                    {"k1_block<unit>", "k1_block<unit,ab=1>"}};
-  plan->name = names[sgn ? 0 : 1][unitab ? 1 : 0];
+  static const char* names[2][2][2] = {{{"k1_block<signed>", "k1_block<signed,ab=1>"},
+                                        {"k1_block<unit>", "k1_block<unit,ab=1>"}},
+                                       {{"k1_block<signed,rows>", "k1_block<signed,ab=1,rows>"},
+                                        {"k1_block<unit,rows>", "k1_block<unit,ab=1,rows>"}}};
+  plan->name = names[rows ? 1 : 0][sgn ? 0 : 1][unitab ? 1 : 0];
   return 0;
 }
 
@@ -449,6 +528,8 @@ cudaError_t block_launch(const BlockPlan& plan, const ExactArgs& ex, cudaStream_
   if (err != cudaSuccess) return err;
   BlockArgs a{};
   a.g = ex.g;
+  a.brow = ex.brow;
+  if (plan.rows && a.brow == nullptr) return cudaErrorInvalidValue;  // (ensure_brow first)
   a.nnz = plan.nnz;
   a.sweeps = ex.sweeps;
   a.replicas = ex.replicas;

@@ -27,6 +27,7 @@ struct DevTrace {
 
 struct ExactArgs {
   DevCsr g;
+  const uint4* brow;      // k1_block rows variant: per vertex {maskp, maskn, 4 x 16-bit columns}
   int32_t n_pad;          // per-replica spin stride in shared memory
   int32_t sweeps;
   int32_t replicas;

@@ -142,6 +142,25 @@ __global__ void k_edges_fill(const int32_t* off, const int32_t* col, const int32
     }
 }
 
+// ---- k1_block row records ---------------------------------------------------
+
+// vertex v: {in-window +1 mask, in-window -1 mask, columns 0-1, columns 2-3}
+// (16-bit columns, bit 15 = weight -1, 0xffff = empty; degree <= 4). Mask
+// bit k-1: vertex v-k of v's own aligned 32-window is a neighbour.
+__global__ void k_block_rows(const int32_t* off, const int32_t* col, const int32_t* w, int n, uint4* rows) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  unsigned mp = 0u, mn = 0u, c[4] = {0xffffu, 0xffffu, 0xffffu, 0xffffu};
+  const int lo = v & ~31;
+  for (int e = off[v], k = 0; e < off[v + 1] && k < 4; e++, k++) {
+    const int u = col[e];
+    const bool neg = w && w[e] < 0;
+    c[k] = static_cast<unsigned>(u) | (neg ? 0x8000u : 0u);
+    if (u < v && u >= lo) (neg ? mn : mp) |= 1u << (v - u - 1);
+  }
+  rows[v] = make_uint4(mp, mn, c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+}
+
 // ---- K3 evaluation layout ----------------------------------------------------
 
 // upper-triangle entries of row u by weight class: cnt[0][u] (+1 or any
@@ -545,6 +564,14 @@ cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout*
   else
     k_eval_fill<false><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, n, split, weights, opos.as<int32_t>(),
                                                  oneg.as<int32_t>(), L->mpos, L->edges.p, L->w.as<int32_t>());
+  if ((e = cudaGetLastError())) return e;
+  return cudaStreamSynchronize(st);
+}
+
+cudaError_t build_block_rows(const DevCsr& g, DevBuf& rows, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = rows.alloc((g.n > 0 ? g.n : 1) * sizeof(uint4)))) return e;
+  k_block_rows<<<blocks(g.n), kB, 0, st>>>(g.off, g.col, g.w, g.n, rows.as<uint4>());
   if ((e = cudaGetLastError())) return e;
   return cudaStreamSynchronize(st);
 }

@@ -66,6 +66,10 @@ cudaError_t build_part_layout(const DevCsr& g, const ThruLayout& T, long long m,
 // number of position-space edges whose larger position is < lim
 cudaError_t part_edges_below(const DevBuf& pedges, long long m, int lim, long long* count);
 
+// k1_block row records (degree <= 4, n <= 32767 / 65535): per vertex its
+// in-window +1 / -1 masks and 16-bit columns (bit 15 = weight -1).
+cudaError_t build_block_rows(const DevCsr& g, DevBuf& rows, cudaStream_t st);
+
 // K3 layout (see EvalLayout).
 cudaError_t build_eval_layout(const DevCsr& g, int64_t m, int wkind, EvalLayout* L, cudaStream_t st);
 
