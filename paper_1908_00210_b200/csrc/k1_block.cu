@@ -285,10 +285,14 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
     const int vv = w0 + lane;
     return vv < nn ? __ldg(a.brow + vv) : make_uint4(0u, 0u, 0xffffffffu, 0xffffffffu);
   };
-  uint4 rw0 = make_uint4(0u, 0u, 0u, 0u), rw1 = rw0;
+#ifndef K1_ROWS_AHEAD
+#define K1_ROWS_AHEAD 2
+#endif
+  uint4 rw0 = make_uint4(0u, 0u, 0u, 0u), rw1 = rw0, rw2 = rw0;
   if (ROWS) {
     rw0 = ldrow(0);
     rw1 = ldrow(32 % nwin32);
+    if (K1_ROWS_AHEAD > 2) rw2 = ldrow(64 % nwin32);
   }
 
 #pragma unroll 1
@@ -321,7 +325,15 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
       uint4 rcur = rw0;
       if (ROWS) {
         rw0 = rw1;
-        rw1 = ldrow((i0 + 64) % nwin32);
+        int wa = i0 + 32 * K1_ROWS_AHEAD;  // (the window K1_ROWS_AHEAD ahead, cyclically; no division)
+        if (wa >= nwin32) wa -= nwin32;
+        if (wa >= nwin32) wa -= nwin32;
+        if (K1_ROWS_AHEAD > 2) {
+          rw1 = rw2;
+          rw2 = ldrow(wa);
+        } else {
+          rw1 = ldrow(wa);
+        }
         wp = rcur.x;
         if (SIGNED) wn = rcur.y;
         if (act) f0 = field_at<FB>(fld, v);
@@ -384,7 +396,16 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
 #pragma unroll 1
           do {
             const int cnt = __popc(C);
-            const int cl = sl < cnt ? static_cast<int>(__fns(C, 0u, sl + 1)) : lane;
+            // this lane group's changed lane: the (sl + 1)-th set bit of C
+            // (a uniform peel of the first 8 bits; __fns measured slower)
+            int cl = lane;
+            unsigned Cc = C;
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+              const int pbit = __ffs(Cc) - 1;
+              if (sl == t && pbit >= 0) cl = pbit;
+              Cc &= Cc - 1u;
+            }
             const unsigned cz = __shfl_sync(FULL, rcur.z, cl), cw = __shfl_sync(FULL, rcur.w, cl);
             const unsigned c = ((k < 2 ? cz : cw) >> (16 * (k & 1))) & 0xffffu;
             if (sl < cnt && c != 0xffffu) {
@@ -394,8 +415,7 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
               else
                 field_add<FB>(fld, static_cast<int>(c), dv);
             }
-#pragma unroll
-            for (int t = 0; t < 8; t++) C &= C - 1u;
+            C = Cc;
           } while (C);
           __syncwarp();
           continue;
