@@ -562,7 +562,7 @@ def main():
         clk = clocks.summary()
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         smem_gbs = sms * 128 * clk["sm_mhz"] * 1e6 / 1e9 if clk.get("sm_mhz") else None
-        onchip = not sess.kernel.startswith(("k4_", "k1_window"))  # CSR staged in shared memory
+        onchip = not sess.kernel.startswith(("k4_", "k1_window")) and ",rows" not in sess.kernel  # CSR in smem
         rl = roofline(bpu, R * n * sweeps, step_ms, l2, hbm, hbm_src, measured_traffic(args.config, sess.kernel),
                       ws, l2_size,
                       ("exact mode: each replica is one serial decision chain (SURVEY 8(d): K1 is latency-bound, "
@@ -629,7 +629,8 @@ def main():
                 "roofline": roofline(bpu, R * n * sweeps, t_ms, l2, hbm, hbm_src,
                                      measured_traffic(args.config, tsess.kernel), ws, l2_size,
                                      "logical bytes per SURVEY 8(d); the CSR and spins are smem/L2 resident",
-                                     smem_gbs if not tsess.kernel.startswith(("k4_", "k1_window")) else None)}
+                                     smem_gbs if not tsess.kernel.startswith(("k4_", "k1_window"))
+                                     and ",rows" not in tsess.kernel else None)}
         del tsess
 
     # e2e: the public batched call with host buffers (fresh CSR upload, seeds
