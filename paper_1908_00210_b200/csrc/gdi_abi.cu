@@ -1013,15 +1013,25 @@ int gdi_evaluate_device(const gdi_graph* g, const int8_t* d_spins, int32_t repli
   gdi_graph* gm = const_cast<gdi_graph*>(g);
   if ((rc = ensure_eval(gm))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // per-thread scratch kept between calls (the bench times back-to-back calls)
+  // per-thread scratch kept between calls (the bench times back-to-back
+  // calls); a call on another stream first waits for the previous call's
+  // kernels (the scratch is reused)
   thread_local DevBuf work;
   thread_local int work_dev = -1;
+  thread_local cudaEvent_t done = nullptr;
   if (work_dev != g->device) {
+    if (done) cudaEventDestroy(done);
+    done = nullptr;
     work.reset();
     work_dev = g->device;
   }
+  if (!done) GDI_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  GDI_CUDA(cudaStreamWaitEvent(st, done, 0));
   const size_t ww = static_cast<size_t>(eval_work_words(g->st.n, replicas, g->wkind)) * 4 + 16;
-  if (work.bytes < ww) GDI_CUDA(work.alloc(ww));
+  if (work.bytes < ww) {
+    GDI_CUDA(cudaEventSynchronize(done));  // (the old buffer may still be in use)
+    GDI_CUDA(work.alloc(ww));
+  }
   // results straight into the caller's buffer (zeroed here), the bad flag
   // into the caller's word or the scratch's last 4 bytes
   uint32_t* bad = d_bad ? d_bad : reinterpret_cast<uint32_t*>(work.as<char>() + ww - 4);
@@ -1040,6 +1050,7 @@ int gdi_evaluate_device(const gdi_graph* g, const int8_t* d_spins, int32_t repli
   a.out = reinterpret_cast<unsigned long long*>(d_cut_sum);
   a.bad = bad;
   GDI_CUDA(eval_launch(a, g->wkind, st, nullptr));
+  GDI_CUDA(cudaEventRecord(done, st));
   return GDI_OK;
 }
 
