@@ -157,9 +157,9 @@ __device__ __forceinline__ void field_add(unsigned char* fld, int t, int dv) {
 // ROWS (= 4): graphs whose CSR and window masks do not fit shared memory
 // next to the replicas (G81+-1: 20000 vertices), with max degree <= 4: each
 // vertex's window masks and its (<= 4) 16-bit columns form one 16-byte row
-// record in global memory, loaded two windows ahead into registers; a
-// change scatters from the changed lane's record (shuffled to KD lanes per
-// change, 32 / KD changes per pass); the jump table is read through L1.
+// record in global memory, loaded two windows ahead into registers; every
+// changed lane scatters its own record's columns (all changes of a window at
+// once); the jump table is read through L1.
 template <bool SIGNED, bool UNITAB, int FB, int ROWS>
 __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -389,34 +389,22 @@ __global__ void __launch_bounds__(512, 1) k1_block(const BlockArgs a) {
         AG += (UNITAB ? 2 : 2 * a4) * (__popc(U) - __popc(D));
         if (act && fin != own) dcut += fin > own ? -f : f;
         if (ROWS) {
-          // the changed lanes' records: KD = 4 lanes per change (lane 4s + k
-          // takes column k of the s-th changed lane), 8 changes per pass
-          unsigned C = U | D;
-          const int sl = lane >> 2, k = lane & 3;
-#pragma unroll 1
-          do {
-            const int cnt = __popc(C);
-            // this lane group's changed lane: the (sl + 1)-th set bit of C
-            // (a uniform peel of the first 8 bits; __fns measured slower)
-            int cl = lane;
-            unsigned Cc = C;
+          // every changed lane scatters its own record's (<= 4) columns,
+          // all changed lanes at once (shared-memory atomics on the packed
+          // fields; no shuffles)
+          if (act && fin != own) {
+            const int dv = fin > own ? 2 : -2;
 #pragma unroll
-            for (int t = 0; t < 8; t++) {
-              const int pbit = __ffs(Cc) - 1;
-              if (sl == t && pbit >= 0) cl = pbit;
-              Cc &= Cc - 1u;
+            for (int k = 0; k < 4; k++) {
+              const unsigned c = ((k < 2 ? rcur.z : rcur.w) >> (16 * (k & 1))) & 0xffffu;
+              if (c != 0xffffu) {
+                if (SIGNED)
+                  field_add<FB>(fld, static_cast<int>(c & 0x7fffu), (c & 0x8000u) ? -dv : dv);
+                else
+                  field_add<FB>(fld, static_cast<int>(c), dv);
+              }
             }
-            const unsigned cz = __shfl_sync(FULL, rcur.z, cl), cw = __shfl_sync(FULL, rcur.w, cl);
-            const unsigned c = ((k < 2 ? cz : cw) >> (16 * (k & 1))) & 0xffffu;
-            if (sl < cnt && c != 0xffffu) {
-              const int dv = ((U >> cl) & 1u) ? 2 : -2;
-              if (SIGNED)
-                field_add<FB>(fld, static_cast<int>(c & 0x7fffu), (c & 0x8000u) ? -dv : dv);
-              else
-                field_add<FB>(fld, static_cast<int>(c), dv);
-            }
-            C = Cc;
-          } while (C);
+          }
           __syncwarp();
           continue;
         }

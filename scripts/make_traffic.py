@@ -2,7 +2,7 @@
 DRAM bytes, L2 bytes (lts__t_sectors x 32) and shared-memory wavefronts of the
 dominant kernel of each bench config, read by bench.py (measured_traffic).
 
-usage: python scripts/make_traffic.py KEY=REPORT:UPDATES:LAUNCHES_PER_STEP:SOURCE_TXT ...
+usage: python scripts/make_traffic.py "KEY|REPORT|UPDATES|LAUNCHES_PER_STEP|SOURCE_TXT" ...
 """
 import json
 import os
@@ -15,8 +15,7 @@ out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__
                         "roofline_traffic.json")
 doc = json.load(open(out_path)) if os.path.exists(out_path) else {}
 for arg in sys.argv[1:]:
-    key, spec = arg.split("=", 1)
-    rep, upl, lps, src = spec.split(":", 3)
+    key, rep, upl, lps, src = arg.split("|", 4)
     h, u, v, d = values(rep)
     doc[key] = {
         "dram_bytes_per_launch": d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0),
