@@ -78,6 +78,7 @@ struct BlockPlan {
   int32_t a4 = 4, b = 4;  // coefficients reduced by gcd(4A, B)
   int rc = 1;             // replica warps per CTA
   int rows = 0;           // > 0: row records in global memory (ExactArgs::brow, build_block_rows)
+  int lane_rows = 0;      // max degree <= 16
   int block = 32, grid = 1, smem = 0, nnz = 0;
   const char* name = "";
 };
