@@ -526,6 +526,21 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
       dn = __ballot_sync(FULL, fin < own);
     }
     if (fin != own) s[v] = static_cast<int8_t>(fin);
+    if (cf.lane_rows && __popc(up | dn) >= 2) {
+      // short rows, several changes: every changed lane walks its own row
+      if (live && fin != own) {
+        int e0, e1;
+        row(v, e0, e1);
+        const int dl = fin > own ? 2 : -2;
+#pragma unroll 1
+        for (int e = e0; e < e1; e++) {
+          int u, w;
+          entry(e, u, w);
+          fadd<FB>(fld, u, w * dl);
+        }
+      }
+      return;
+    }
     for (unsigned chg = up | dn; chg != 0u; chg &= chg - 1u) {
       const int l = __ffs(chg) - 1;
       const int vl = __shfl_sync(FULL, v, l), dl = ((up >> l) & 1u) ? 2 : -2;
@@ -696,6 +711,9 @@ bool chains_layout(const GraphStats& st, int wkind, int32_t replicas, int fb, Ch
   int seg = 8;
   if (const char* e = std::getenv("GDI_K2_SEG")) seg = std::max(1, std::atoi(e));
   c->seg = seg;
+  int lane_maxdeg = 16;
+  if (const char* e = std::getenv("GDI_K2_LANE_MAXDEG")) lane_maxdeg = std::atoi(e);  // A/B
+  c->lane_rows = st.max_degree <= lane_maxdeg;
   if (nck - T < P) P = std::max(1, nck - T);
   auto r16 = [](long long x) { return (x + 15) & ~15LL; };
   const long long n_pad4 = r16(n + 4);

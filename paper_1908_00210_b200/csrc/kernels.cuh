@@ -114,6 +114,7 @@ struct ThruArgs {
 struct ChainCfg {
   int32_t rpc, chains, tail;  // replicas per CTA, chains (warps) per replica, tail chunks
   int32_t seg;                // chunks per segment (chain j visits segments j, j + chains, ...)
+  int32_t lane_rows;          // max degree <= 16: changed lanes walk their own rows
   int32_t off_order, off_offs, off_cols, off_rep, rep_bytes, n_pad4, smem;
 };
 
