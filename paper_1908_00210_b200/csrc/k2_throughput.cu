@@ -396,6 +396,8 @@ template <int WK, int FB, bool CS>
 __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const ChainCfg cf) {
   extern __shared__ __align__(16) unsigned char csm[];
   __shared__ int red_d[32], rep_G[16];
+  __shared__ __align__(16) int2 scan_buf[32][32];  // in-order scan scratch per warp (warp_seq_decide)
+  __shared__ __align__(16) int scan_g[32][32];
   __shared__ long long red_sf[32], red_s[32];
   __shared__ long long Wtot;
   const int n = a.g.n, P = cf.chains;
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     if (__all_sync(FULL, fin2 == fin)) {
       G += 2 * (__popc(up) - __popc(dn));
     } else {
-      fin = warp_seq_decide(own, f, live, coin, flip, G, a4, bb, lane);
+      fin = warp_seq_decide(own, f, live, coin, flip, G, a4, bb, lane, scan_buf[warp], scan_g[warp]);
       up = __ballot_sync(FULL, fin > own);
       dn = __ballot_sync(FULL, fin < own);
     }

@@ -225,7 +225,8 @@ __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMA
 #ifndef K4_ROUNDS
 #define K4_ROUNDS 2
 #endif
-__device__ __forceinline__ unsigned decide_chunk(const Visit& x, int& G, int a4, int bb, int lane) {
+__device__ __forceinline__ unsigned decide_chunk(const Visit& x, int& G, int a4, int bb, int lane, int2* sbuf,
+                                                 int* sgout) {
   const int base = -a4 * x.own - bb * x.f;
   int fin = x.live ? decide(a4 * G + base, x.coin, x.flip) : x.own;
   unsigned up = __ballot_sync(FULL, fin > x.own), dn = __ballot_sync(FULL, fin < x.own);
@@ -243,7 +244,7 @@ __device__ __forceinline__ unsigned decide_chunk(const Visit& x, int& G, int a4,
     up = __ballot_sync(FULL, fin > x.own);
     dn = __ballot_sync(FULL, fin < x.own);
   }
-  fin = warp_seq_decide(x.own, x.f, x.live, x.coin, x.flip, G, a4, bb, lane);
+  fin = warp_seq_decide(x.own, x.f, x.live, x.coin, x.flip, G, a4, bb, lane, sbuf, sgout);
   return __ballot_sync(FULL, fin > 0);
 }
 
@@ -376,6 +377,8 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
   __shared__ int st_c[kNW];
   __shared__ unsigned st_w[kNW];
   __shared__ int red_share[kNW], red_delta[kNW];
+  __shared__ __align__(16) int2 scan_buf[kNW][32];  // in-order scan scratch (warp_seq_decide)
+  __shared__ __align__(16) int scan_g[kNW][32];
   __shared__ int last, chains_done;
   __shared__ uint64_t mbar[kNW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     bhi = (k + 1) * P;
     const Visit x = make_visit<WK, KMAX>(a, cur, c, word, lane, sweep, k0, k1, tm, en,
                                          static_cast<uint32_t>(J + (k & ~1) * P), k & 1, spare, (k & 1) != 0);
-    commit(c, cur.word, decide_chunk(x, G, a4, bb, lane));
+    commit(c, cur.word, decide_chunk(x, G, a4, bb, lane, scan_buf[warp], scan_g[warp]));
     cur = nxt;
   }
   if (rmode && is_chain && lane == 0) atomicAdd(&chains_done, 1);
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     for (int t = 0; t < D; t++) {
       const int c = st_c[t];
       if (c < 0) continue;
-      const unsigned nw = decide_chunk(unpack(stage[t][lane]), Gc, a4, bb, lane);
+      const unsigned nw = decide_chunk(unpack(stage[t][lane]), Gc, a4, bb, lane, scan_buf[warp], scan_g[warp]);
       commit(c, st_w[t], nw);
     }
     const int cta_delta = dl + Gc - g0;
@@ -627,6 +630,8 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
   __shared__ uint32_t tw[kTailMax];
   __shared__ unsigned stage[kTailMax][32];
   __shared__ int tail_delta;
+  __shared__ __align__(16) int2 scan_buf[kNW][32];
+  __shared__ __align__(16) int scan_g[kNW][32];
   __shared__ long long lred[2][kNW];
   __shared__ int last;
   __shared__ uint64_t mbar[kNW];
@@ -687,7 +692,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
     int Gt = static_cast<int>(G0);
 #pragma unroll 1
     for (int t = 0; t < T; t++) {
-      const unsigned nw = decide_chunk(unpack(stage[t][lane]), Gt, a.a4, a.b, lane);
+      const unsigned nw = decide_chunk(unpack(stage[t][lane]), Gt, a.a4, a.b, lane, scan_buf[warp], scan_g[warp]);
       if (lane == 0) tw[t] = nw;
     }
     if (lane == 0) tail_delta = Gt - static_cast<int>(G0);
