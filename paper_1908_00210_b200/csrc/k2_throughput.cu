@@ -556,6 +556,19 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     }
   };
 
+  // the chain with the fewest main chunks decides the tail (sweep-invariant)
+  int jt = 0;
+  {
+    const int nmain0 = nck - cf.tail, nseg = (nmain0 + cf.seg - 1) / cf.seg, L = nmain0 - (nseg - 1) * cf.seg;
+    int best = 1 << 30;
+    for (int q = 0; q < P; q++) {
+      const int cnt = (q < nseg ? (nseg - q + P - 1) / P : 0) * cf.seg - (q == (nseg - 1) % P ? cf.seg - L : 0);
+      if (cnt <= best) {
+        best = cnt;
+        jt = q;
+      }
+    }
+  }
   for (int sweep = 0; sweep < a.sweeps; sweep++) {
     const unsigned long long tm = a.tmask[sweep];
     const bool en = a.thr[sweep] >= 0;
@@ -586,19 +599,6 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     // balanced no more runs of a hub graph: 81% either way, 86% sequential)
     const int T = cf.tail, nmain = nck - T;
     const int kSeg = cf.seg;
-    // the chain with the fewest main chunks decides the tail
-    int jt = 0;
-    {
-      const int nseg = (nmain + kSeg - 1) / kSeg, L = nmain - (nseg - 1) * kSeg;
-      int best = 1 << 30;
-      for (int q = 0; q < P; q++) {
-        const int cnt = (q < nseg ? (nseg - q + P - 1) / P : 0) * kSeg - (q == (nseg - 1) % P ? kSeg - L : 0);
-        if (cnt <= best) {
-          best = cnt;
-          jt = q;
-        }
-      }
-    }
 #pragma unroll 1
     for (int s0 = j * kSeg; s0 < nmain; s0 += P * kSeg) {
       const int c1 = min(nmain, s0 + kSeg);
