@@ -54,4 +54,5 @@ else:
             cuts.append(int(out["cut"][0]))
 print(json.dumps({"recipe": recipe, "part": part, "env": {k: v for k, v in os.environ.items() if k.startswith("GDI_")},
                   "imb_hist": {str(k): imbs.count(k) for k in sorted(set(imbs))}, "mean_cut": float(np.mean(cuts)),
+                  "cuts": cuts,
                   "median_ms": float(np.median(ms)) if ms else None}))
