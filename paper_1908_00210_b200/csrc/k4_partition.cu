@@ -653,40 +653,42 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
       return reinterpret_cast<const uint32_t*>(recv + (wi % W) * rstride + 8)[wi / W];
     return __ldg(gb + wi);  // (read-only in this kernel until the last CTA's tail stores)
   };
-  if (SM) {
-    if (unfused) {
-      for (int wi = threadIdx.x; wi < a.nwp; wi += blockDim.x) sw[wi] = mword(wi);
-    } else {
-      const Slice sl(a.nwp, warp, kNW);
-      Refresher rf{&mbar[warp], 0u, false};
-      if (lane == 0) {
-        mbar_init(&mbar[warp]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      }
-      __syncwarp();
-      rf.issue(sw, gb, sl, lane);
-      rf.drain(lane);
-    }
-    __syncthreads();
-  }
-  // lookups before the tail is decided (tail words: their values before it)
-  auto pre = [&](int wi) -> unsigned { return SM ? sw[wi] : mword(wi); };
-
-  // 1. global tail, replayed identically by every CTA (and every rank):
-  // gathered by T warps, decided in order by warp 0 against the exact counter
+  // 1a. the global tail's visits, gathered by T warps from the global words
+  // (mword) while the shared copy lands: the tail decisions need not wait
+  // for the copy
   const uint64_t seed = a.seeds[r];
+  Refresher rf{&mbar[warp], 0u, false};
+  const Slice sl(a.nwp, warp, kNW);
+  if (SM && !unfused) {
+    if (lane == 0) {
+      mbar_init(&mbar[warp]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    rf.issue(sw, gb, sl, lane);
+  }
   if (warp < T) {
     const int c = nmain + warp;
     Row<WK, KMAX> row;
     load_row<WK, KMAX>(a, gb, c, __ldg(a.sell_off + c), __ldg(a.sell_off + c + 1), lane, row);
-    row.word = pre(c);
+    row.word = mword(c);
     uint64_t spare = 0;
-    const Visit xt = make_visit<WK, KMAX>(a, row, c, pre, lane, sweep, static_cast<uint32_t>(seed),
+    const Visit xt = make_visit<WK, KMAX>(a, row, c, mword, lane, sweep, static_cast<uint32_t>(seed),
                                           static_cast<uint32_t>(seed >> 32), a.tmask[sweep], a.thr[sweep] >= 0,
                                           static_cast<uint32_t>(c), 0, spare, false);
     stage[warp][lane] = pack(xt);
   }
+  if (SM) {
+    if (unfused)
+      for (int wi = threadIdx.x; wi < a.nwp; wi += blockDim.x) sw[wi] = mword(wi);
+    else
+      rf.drain(lane);
+  }
   __syncthreads();
+  // lookups before the tail is decided (tail words: their values before it)
+  auto pre = [&](int wi) -> unsigned { return SM ? sw[wi] : mword(wi); };
+  // 1b. the tail decided in order by warp 0 against the exact counter (every
+  // CTA and every rank replays it identically)
   long long cut = 0, pop = 0;
   if (warp == 0) {
     int Gt = static_cast<int>(G0);
