@@ -18,7 +18,7 @@ CU_SRC   := $(wildcard $(CSRC)/*.cu)
 CU_OBJ   := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRC))
 HOST_SRC := $(wildcard $(CSRC)/host/*.cpp)
 HOST_OBJ := $(patsubst $(CSRC)/host/%.cpp,$(BUILD)/host/%.o,$(HOST_SRC))
-CU_HDR   := $(wildcard $(CSRC)/*.cuh) $(CSRC)/launch.hpp include/gdi.h
+CU_HDR   := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) include/gdi.h
 HOST_HDR := $(wildcard include/ising/*.hpp) $(wildcard $(CSRC)/host/*.hpp) include/gdi.h
 
 LIBGDI   := $(LIBDIR)/libgdi.so
