@@ -549,7 +549,7 @@ int block_plan(const GraphStats& st, int32_t replicas, int64_t a4, int64_t b, in
 }
 
 cudaError_t block_launch(const BlockPlan& plan, const ExactArgs& ex, cudaStream_t stream) {
-  cudaError_t err = cudaFuncSetAttribute(plan.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+  cudaError_t err = allow_max_smem(plan.fn);
   if (err != cudaSuccess) return err;
   BlockArgs a{};
   a.g = ex.g;

@@ -199,8 +199,7 @@ int exact_plan(const GraphStats& st, int32_t replicas, ExactPlan* plan) {
 }
 
 cudaError_t exact_launch(const ExactPlan& plan, const ExactArgs& args, cudaStream_t stream) {
-  cudaError_t err = cudaFuncSetAttribute(plan.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         plan.smem);
+  cudaError_t err = allow_max_smem(plan.fn);
   if (err != cudaSuccess) return err;
   ExactArgs a = args;
   void* params[] = {&a};

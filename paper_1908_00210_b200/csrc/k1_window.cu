@@ -638,7 +638,7 @@ int window_plan(const GraphStats& st, const PipeGraph& pg, int32_t replicas, int
 }
 
 cudaError_t window_launch(const PipePlan& plan, const PipeArgs& args, cudaStream_t stream) {
-  cudaError_t err = cudaFuncSetAttribute(plan.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+  cudaError_t err = allow_max_smem(plan.fn);
   if (err != cudaSuccess) return err;
   PipeArgs a = args;
   a.rc = plan.rc;

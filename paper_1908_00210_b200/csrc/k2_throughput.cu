@@ -809,7 +809,7 @@ int thru_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
 }
 
 cudaError_t thru_launch(const ThruPlan& plan, const ThruArgs& args, cudaStream_t stream) {
-  cudaError_t err = cudaFuncSetAttribute(plan.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+  cudaError_t err = allow_max_smem(plan.fn);
   if (err != cudaSuccess) return err;
   ThruArgs a = args;
   a.a4 = plan.a4;

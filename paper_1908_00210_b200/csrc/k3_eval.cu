@@ -380,9 +380,7 @@ cudaError_t eval_launch(EvalArgs a, int wkind, cudaStream_t stream, int* launche
                                           : reinterpret_cast<const void*>(&k3_sliced<true, false>))
                             : (wkind == 1 ? reinterpret_cast<const void*>(&k3_sliced<false, true>)
                                           : reinterpret_cast<const void*>(&k3_sliced<false, false>));
-    if (smem > 48 * 1024 &&
-        (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))))
-      return e;
+    if (smem > 48 * 1024 && (e = allow_max_smem(fn))) return e;
     void* params[] = {&a};
     if (launches) *launches = 2;
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(S), groups), dim3(kSliceBlock), params, smem, stream);
@@ -403,8 +401,7 @@ cudaError_t eval_launch(EvalArgs a, int wkind, cudaStream_t stream, int* launche
   if (per < 1) per = 1;
   const void* fn = narrow ? (sm ? bits_fn<true, true>(wkind) : bits_fn<true, false>(wkind))
                           : (sm ? bits_fn<false, true>(wkind) : bits_fn<false, false>(wkind));
-  if (smem > 48 * 1024 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))))
-    return e;
+  if (smem > 48 * 1024 && (e = allow_max_smem(fn))) return e;
   void* params[] = {&a};
   if (launches) *launches = 2;
   return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(per), a.R), dim3(kBitsBlock), params, smem, stream);

@@ -333,6 +333,35 @@ struct Refresher {
   }
 };
 
+// The shared spin copy of a cluster of `mc` CTAs (2) fetched once: slice
+// w is read from L2 by CTA (w mod mc) and multicast into every CTA of the
+// cluster (148 SMs re-reading the same 125 KB made a plain copy ~3.7 us).
+// Every thread of the CTA calls this; the cluster barriers order the
+// mbarrier inits before the peers' copies and keep every multicast write
+// landed before any CTA of the cluster moves on.
+__device__ __forceinline__ void cluster_copy(uint32_t* dst, const uint32_t* src, const Slice& sl, uint64_t* mb,
+                                             int warp, int lane, int mc) {
+  unsigned crank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  if (lane == 0) {
+    mbar_init(mb);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (lane == 0 && sl.bytes > 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(mb)), "r"(sl.bytes) : "memory");
+    if (warp % mc == static_cast<int>(crank))
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+          "%4;" ::"r"(saddr(dst + sl.lo)),
+          "l"(src + sl.lo), "r"(sl.bytes), "r"(saddr(mb)), "h"(static_cast<unsigned short>((1u << mc) - 1u))
+          : "memory");
+    mbar_wait(mb, 0u);
+  }
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Initial spins (one Philox draw per vertex: the throughput mode is not
 // bit-exact, so the serial stream-0 walk of anneal.cpp:148-155 is not needed)
 // and the exact initial counter. One thread per position of every word.
@@ -406,7 +435,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
 
   const Slice slice(a.nwp, warp, NW);
   Refresher rf{&mbar[warp], 0u, false};
-  if (SM) {  // the whole copy: every warp its slice
+  if (SM && a.mcast > 1) {
+    cluster_copy(sb, gb, slice, &mbar[warp], warp, lane, a.mcast);
+    rf.phase = slice.bytes > 0 ? 1u : 0u;  // (as after rf.drain)
+  } else if (SM) {  // the whole copy: every warp its slice
     if (lane == 0) {
       mbar_init(&mbar[warp]);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -887,9 +919,8 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
   plan->a4 = static_cast<int32_t>(ra);
   plan->b = static_cast<int32_t>(rb);
   if (plan->smem > 48 * 1024 &&
-      (cudaFuncSetAttribute(plan->sweep_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem) != cudaSuccess ||
-       (plan->fin_smem > 0 && cudaFuncSetAttribute(plan->finish_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   plan->fin_smem) != cudaSuccess)))
+      (allow_max_smem(plan->sweep_fn) != cudaSuccess ||
+       (plan->fin_smem > 0 && allow_max_smem(plan->finish_fn) != cudaSuccess)))
     return -1;
   plan->name = wkind == 0 ? "k4_sweep<unit>" : wkind == 1 ? "k4_sweep<pm1>" : "k4_sweep<weighted>";
   return 0;
@@ -910,6 +941,11 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   a.refresh = plan.refresh;
   a.copy_parts = 1;
   if (const char* e = std::getenv("GDI_K4_PARTS")) a.copy_parts = std::max(1, std::min(8, std::atoi(e)));
+  // sweep CTAs in clusters of two share the initial copy (clusters of four
+  // do not all fit at once: two waves, M1 1.95 ms)
+  a.mcast = plan.smem_copy && plan.ctas % 2 == 0 ? 2 : 1;
+  if (const char* e = std::getenv("GDI_K4_MCAST"))  // A/B: 0 off
+    if (std::atoi(e) == 0) a.mcast = 1;
   const char* dbg = std::getenv("GDI_K4_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
   return a;
@@ -934,7 +970,22 @@ cudaError_t part_sweep_launch(const PartPlan& plan, const PartArgs& args, int sw
   PartArgs a = prepared(plan, args);
   a.sweep = sweep;
   void* p[] = {&a};
-  return cudaLaunchKernel(plan.sweep_fn, dim3(plan.ctas, a.replicas), dim3(plan.block), p, plan.smem, stream);
+  if (a.mcast == 1)
+    return cudaLaunchKernel(plan.sweep_fn, dim3(plan.ctas, a.replicas), dim3(plan.block), p, plan.smem, stream);
+  // clusters of two CTAs (the multicast initial copy)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(plan.ctas, a.replicas);
+  cfg.blockDim = dim3(plan.block);
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.mcast;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, plan.sweep_fn, p);
 }
 
 cudaError_t part_finish_launch(const PartPlan& plan, const PartArgs& args, int sweep, const void* recv,
@@ -943,6 +994,8 @@ cudaError_t part_finish_launch(const PartPlan& plan, const PartArgs& args, int s
   a.sweep = sweep;
   const unsigned char* rv = static_cast<const unsigned char*>(recv);
   void* p[] = {&a, &rv, &stride, &spins_out};
+  // (no clusters here: the multicast copy in the finishing kernel measured
+  // slower, M1 1.191 -> 1.229 ms)
   return cudaLaunchKernel(plan.finish_fn, dim3(plan.fin_grid, a.replicas), dim3(plan.fin_block), p, plan.fin_smem,
                           stream);
 }

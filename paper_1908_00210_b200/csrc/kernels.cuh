@@ -165,6 +165,7 @@ struct PartArgs {
   int32_t cta_tail;                // chains per CTA deferring their last chunk to the CTA tail
   int32_t refresh;                 // 1: the last warp of a CTA re-copies its shared spin copy (0: never)
   int32_t copy_parts;              // bulk copies in flight per refresh
+  int32_t mcast;                   // sweep CTAs per cluster sharing the initial copy (1 or 2)
   int32_t debug;                   // timing experiments only (GDI_K4_DEBUG); 0 in production
   DevTrace* trace;
   unsigned long long* stamps;

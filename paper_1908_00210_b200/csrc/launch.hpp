@@ -9,6 +9,24 @@
 
 namespace gdi {
 
+// Dynamic shared memory above 48 KB needs a per-function opt-in. Sessions on
+// different host threads launch the same kernels with different sizes, so the
+// opt-in is always the device maximum (one value from every thread: setting
+// each launch's own size raced with another thread's launch of the same
+// function, "invalid argument"). The launch's own size is what it uses.
+inline cudaError_t allow_max_smem(const void* fn) {
+  int dev = 0, mx = 0;
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);  // (the opt-in covers static + dynamic)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx - static_cast<int>(fa.sharedSizeBytes));
+  return e;
+}
+
+
 struct GraphStats {
   int32_t n = 0;
   int64_t m = 0;
