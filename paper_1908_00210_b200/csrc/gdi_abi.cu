@@ -1108,6 +1108,7 @@ int gdi_part_create(const gdi_graph* g, const gdi_params* p, int32_t world, int3
     s->plan.chains = ctas * cw;
     s->plan.warps = cw + refresher;
     s->plan.block = 32 * s->plan.warps;
+    part_plan_mcast(&s->plan, 1);
   }
   if ((rc = ensure_part(s->g)) || (rc = part_splits(s->g, &s->plan))) return rc;
   schedule(s->p, s->pf, s->thr, s->tmask);

@@ -923,7 +923,38 @@ int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int
        (plan->fin_smem > 0 && allow_max_smem(plan->finish_fn) != cudaSuccess)))
     return -1;
   plan->name = wkind == 0 ? "k4_sweep<unit>" : wkind == 1 ? "k4_sweep<pm1>" : "k4_sweep<weighted>";
+  part_plan_mcast(plan, R);
   return 0;
+}
+
+// Sweep CTAs in clusters of two sharing the initial copy (multicast): opt-in
+// (GDI_K4_MCAST=2), and only when every cluster of the grid fits at once.
+// Measured on M1: one B200 1.234 -> 1.192 ms with it, another 1.20 -> 1.26 ms
+// (both with every cluster resident by cudaOccupancyMaxActiveClusters), so
+// the plain per-CTA copy stays the default. Clusters of four never all fit
+// (two waves, 1.95 ms).
+void part_plan_mcast(PartPlan* plan, int replicas) {
+  plan->mcast = 1;
+  if (!plan->smem_copy || plan->ctas % 2 != 0) return;
+  const char* e = std::getenv("GDI_K4_MCAST");
+  if (e == nullptr || std::atoi(e) != 2) return;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(plan->ctas, replicas > 0 ? replicas : 1);
+  cfg.blockDim = dim3(plan->block);
+  cfg.dynamicSmemBytes = plan->smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, plan->sweep_fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (2LL * clusters >= static_cast<long long>(plan->ctas) * (replicas > 0 ? replicas : 1)) plan->mcast = 2;
 }
 
 int part_launch_count(const PartPlan&, int32_t sweeps) { return 1 + 2 * sweeps; }
@@ -941,11 +972,7 @@ PartArgs prepared(const PartPlan& plan, const PartArgs& args) {
   a.refresh = plan.refresh;
   a.copy_parts = 1;
   if (const char* e = std::getenv("GDI_K4_PARTS")) a.copy_parts = std::max(1, std::min(8, std::atoi(e)));
-  // sweep CTAs in clusters of two share the initial copy (clusters of four
-  // do not all fit at once: two waves, M1 1.95 ms)
-  a.mcast = plan.smem_copy && plan.ctas % 2 == 0 ? 2 : 1;
-  if (const char* e = std::getenv("GDI_K4_MCAST"))  // A/B: 0 off
-    if (std::atoi(e) == 0) a.mcast = 1;
+  a.mcast = plan.mcast;
   const char* dbg = std::getenv("GDI_K4_DEBUG");
   a.debug = dbg ? std::atoi(dbg) : 0;
   return a;

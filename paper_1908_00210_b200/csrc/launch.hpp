@@ -133,12 +133,15 @@ struct PartPlan {
   int smem = 0;        // dynamic shared memory of the sweep kernel (the spin copy)
   int fin_smem = 0;    // dynamic shared memory of the finishing kernel (0: lookups through L1)
   long long m_main = 0, m_main_multi = 0;  // position-space edges between main vertices (tail / tail_multi)
+  int mcast = 1;       // sweep CTAs per cluster sharing the initial copy (part_plan_mcast)
   bool smem_copy = false;
   int refresh = 1;     // 1: a refresher warp keeps re-copying the shared spin copy (0: never)
   int fresh = 0;       // 1: the last two bands of chunks read from the global words (k4_sweep SMODE 2)
   const char* name = "";
 };
 int part_plan(const GraphStats& st, int wkind, int32_t replicas, int64_t a4, int64_t b, PartPlan* plan);
+// plan->mcast for the plan's sweep grid (after any change of ctas / block)
+void part_plan_mcast(PartPlan* plan, int replicas);
 // Enqueues init + sweeps x (sweep, finish) kernels: 1 + 2 * sweeps launches.
 // spins_out [R][n] receives the final spins in vertex order.
 cudaError_t part_launch(const PartPlan& plan, const PartArgs& args, int8_t* spins_out, cudaStream_t stream);
