@@ -624,7 +624,26 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     bar_sync(bid, bthreads);
     // record_barrier: spin sum and the exact cut from the exact fields
     long long sf = 0, ss = 0;
-    for (int v = j * 32 + lane; v < n; v += bthreads) {
+    int v0 = 0;
+    if (FB == 1 && a.snaps == nullptr) {
+      // four vertices per step: int8 spins x biased byte fields by dp4a
+      // (sum s (f + 128) - 128 sum s)
+      const int n4 = n >> 2;
+      int sfi = 0, ssi = 0;
+      for (int q = j * 32 + lane; q < n4; q += bthreads) {
+        const int s4 = reinterpret_cast<const int*>(s)[q];
+        const unsigned f4 = reinterpret_cast<const unsigned*>(fld)[q];
+        int d, e;
+        asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(s4), "r"(0x01010101), "r"(0));
+        asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(e) : "r"(s4), "r"(f4), "r"(0));  // signed spins x unsigned bytes
+        ssi += d;
+        sfi += e - 128 * d;
+      }
+      sf = sfi;
+      ss = ssi;
+      v0 = 4 * n4;
+    }
+    for (int v = v0 + j * 32 + lane; v < n; v += bthreads) {
       const int sv = s[v];
       sf += sv * fget<FB>(fld, v);
       ss += sv;
