@@ -101,7 +101,7 @@ struct gdi_graph {
   DevCsr csr() const { return DevCsr{off.as<int32_t>(), col.as<int32_t>(), st.unit ? nullptr : w.as<int32_t>(), st.n}; }
   int64_t bytes() const {
     return static_cast<int64_t>(off.bytes + col.bytes + w.bytes + thru.order.bytes + thru.sell.bytes +
-                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + psell.bytes + pdeg.bytes + pedges.bytes + pedge_w.bytes +
+                                thru.sell_off.bytes + thru.sell_w.bytes + thru.edges.bytes + thru.edge_w.bytes + thru.poff.bytes + thru.pcol.bytes + thru.ppos.bytes + psell.bytes + pdeg.bytes + pedges.bytes + pedge_w.bytes +
                                 pipel.win_pos.bytes +
                                 pipel.win_neg.bytes + pipel.fwd_pos.bytes + pipel.fwd_neg.bytes + pipel.wsell.bytes +
                                 pipel.wsell_off.bytes + evl.edges.bytes + evl.w.bytes + brow.bytes);
@@ -773,6 +773,9 @@ int gdi_session_launch(gdi_session* s) {
     a.sell_off = s->g->thru.sell_off.as<int32_t>();
     a.sell_w = s->g->thru.sell_w.as<int4>();
     a.edges = s->g->thru.edges.as<int2>();
+    a.poff = s->g->thru.poff.as<int32_t>();
+    a.pcol = s->g->thru.pcol.as<int32_t>();
+    a.ppos = s->g->thru.ppos.as<int32_t>();
     a.edge_w = s->g->thru.edge_w.as<int32_t>();
     a.m = s->g->st.m;
     a.sweeps = s->p.sweeps;

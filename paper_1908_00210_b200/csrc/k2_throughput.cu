@@ -414,12 +414,15 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
   long long wpart = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = __ldg(a.order + i);
   if (CS) {
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) offs[i] = __ldg(a.g.off + i);
-    const int nnz = __ldg(a.g.off + n);
+    // the shared-memory CSR in position space (row p = vertex order[p],
+    // neighbours as positions): a chunk's lane p reads its own spin, field
+    // and row directly, without the order[] indirection
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) offs[i] = __ldg(a.poff + i);
+    const int nnz = __ldg(a.poff + n);
     for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
-      const int c = __ldg(a.g.col + e);
-      const bool neg = WK == 1 && __ldg(a.g.w + e) < 0;
-      cols[e] = static_cast<uint16_t>(neg ? (c | 0x8000) : c);
+      const int c = __ldg(a.pcol + e);
+      const bool neg = WK == 1 && c < 0;
+      cols[e] = static_cast<uint16_t>(neg ? ((c & 0x7fffffff) | 0x8000) : c);
       wpart += neg ? -1 : 1;
     }
   } else {
@@ -472,7 +475,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
     for (int i = 0; i < n; i++) {
       const int v = (r0.next() >> 63) ? 1 : -1;
       G += v;
-      if ((i & 31) == lane) s[i] = static_cast<int8_t>(v);
+      if ((i & 31) == lane) s[CS ? __ldg(a.ppos + i) : i] = static_cast<int8_t>(v);  // (position space when CS)
     }
     if (lane == 0) rep_G[slot] = G;
   }
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
   }
   bar_sync(bid, bthreads);
   if (a.snaps != nullptr)
-    for (int i = j * 32 + lane; i < n; i += bthreads) a.snaps[rs * (a.sweeps + 1) * n + i] = s[i];
+    for (int i = j * 32 + lane; i < n; i += bthreads) a.snaps[rs * (a.sweeps + 1) * n + (CS ? order[i] : i)] = s[i];
   if (j == 0 && lane == 0 && a.stamps != nullptr) a.stamps[rs * (a.sweeps + 1)] = globaltimer_ns();
 
   // one chunk: visits against counter G (lane order), spin stores and the
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
   auto chunk = [&](int c, int& G, int sweep, unsigned long long tm, bool en) {
     const int p = c * 32 + lane;
     const bool live = p < n;
-    const int v = live ? order[p] : 0;
+    const int v = live ? (CS ? p : order[p]) : 0;
     const int own = live ? s[v] : -1, f = live ? fget<FB>(fld, v) : 0;
     // one Philox4x32-10 call per four chunks (4b .. 4b + 3; counter (sweep,
     // 32b + lane, 2, 0), key = the replica seed), 32 bits per visit: coin =
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
       const int sv = s[v];
       sf += sv * fget<FB>(fld, v);
       ss += sv;
-      if (a.snaps != nullptr) a.snaps[(rs * (a.sweeps + 1) + sweep + 1) * n + v] = static_cast<int8_t>(sv);
+      if (a.snaps != nullptr) a.snaps[(rs * (a.sweeps + 1) + sweep + 1) * n + (CS ? order[v] : v)] = static_cast<int8_t>(sv);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -677,7 +680,7 @@ __global__ void __launch_bounds__(1024, 1) k2_chains(const ThruArgs a, const Cha
       if (sweep + 1 == a.sweeps) a.final_out[rs] = rec;
     }
   }
-  for (int i = j * 32 + lane; i < n; i += bthreads) a.spins_out[rs * n + i] = s[i];
+  for (int i = j * 32 + lane; i < n; i += bthreads) a.spins_out[rs * n + (CS ? order[i] : i)] = s[i];
 }
 
 template <int WK, int FB>

@@ -93,6 +93,9 @@ struct ThruArgs {
   const int4* sell;
   const int32_t* sell_off;         // [chunks+1] in int4 units
   const int4* sell_w;              // nullptr unless general weights
+  const int32_t* poff;             // k2_chains: the CSR in position space (row p = vertex order[p]),
+  const int32_t* pcol;             //   neighbours as positions, bit 31 = weight -1 (+-1 graphs)
+  const int32_t* ppos;             //   vertex -> position
   const int2* edges;               // [m] canonical (u < v) edge list
   const int32_t* edge_w;           // [m] or nullptr (unit)
   int64_t m;

@@ -161,6 +161,28 @@ __global__ void k_block_rows(const int32_t* off, const int32_t* col, const int32
   rows[v] = make_uint4(mp, mn, c[0] | (c[1] << 16), c[2] | (c[3] << 16));
 }
 
+// ---- K2 position-space CSR -----------------------------------------------------
+
+__global__ void k_pos_deg(const int32_t* order, const int32_t* off, int n, int32_t* pos, int32_t* pdeg) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    const int v = order[p];
+    pos[v] = p;
+    pdeg[p] = off[v + 1] - off[v];
+  }
+  if (p == n) pdeg[n] = 0;
+}
+
+__global__ void k_pos_fill(const int32_t* order, const int32_t* off, const int32_t* col, const int32_t* w,
+                           const int32_t* pos, const int32_t* poff, int n, int32_t* pcol) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int v = order[p];
+  int o = poff[p];
+  for (int e = off[v]; e < off[v + 1]; e++)
+    pcol[o++] = pos[col[e]] | (w && w[e] < 0 ? static_cast<int32_t>(0x80000000u) : 0);
+}
+
 // ---- K3 evaluation layout ----------------------------------------------------
 
 // upper-triangle entries of row u by weight class: cnt[0][u] (+1 or any
@@ -356,6 +378,19 @@ cudaError_t build_thru_layout(const DevCsr& g, int64_t m, int wkind, ThruLayout*
   else
     k_sell_fill<2><<<blocks(n), kB, 0, st>>>(g.off, g.col, g.w, L->order.as<int32_t>(), L->sell_off.as<int32_t>(), n,
                                              L->sell.as<int32_t>(), L->sell_w.as<int32_t>());
+  // the CSR in position space (K2's shared-memory copy)
+  {
+    DevBuf pdeg;
+    if ((e = L->ppos.alloc((n > 0 ? n : 1) * sizeof(int32_t))) || (e = pdeg.alloc((n + 1) * sizeof(int32_t))) ||
+        (e = L->poff.alloc((n + 1) * sizeof(int32_t))) || (e = L->pcol.alloc((2 * m > 0 ? 2 * m : 1) * sizeof(int32_t))))
+      return e;
+    k_pos_deg<<<blocks(n + 1), kB, 0, st>>>(L->order.as<int32_t>(), g.off, n, L->ppos.as<int32_t>(),
+                                            pdeg.as<int32_t>());
+    if ((e = exclusive_scan(pdeg.as<int32_t>(), L->poff.as<int32_t>(), n + 1, st))) return e;
+    k_pos_fill<<<blocks(n), kB, 0, st>>>(L->order.as<int32_t>(), g.off, g.col, wkind == 1 ? g.w : nullptr,
+                                         L->ppos.as<int32_t>(), L->poff.as<int32_t>(), n, L->pcol.as<int32_t>());
+    if ((e = cudaGetLastError())) return e;
+  }
   // canonical edge list (u < v, row order): count, scan, fill
   DevBuf ucnt, eoff;
   if ((e = ucnt.alloc((n + 1) * sizeof(int32_t))) || (e = eoff.alloc((n + 1) * sizeof(int32_t)))) return e;

@@ -22,6 +22,9 @@ struct GraphScan {
 
 struct ThruLayout {
   DevBuf order, sell, sell_off, sell_w, edges, edge_w;
+  // the CSR in position space (row p = vertex order[p], neighbours as their
+  // positions, bit 31 = weight -1 on +-1 graphs) and vertex -> position
+  DevBuf poff, pcol, ppos;
   long long slots = 0;  // int4 cells of SELL
 };
 
