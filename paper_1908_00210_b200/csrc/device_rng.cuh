@@ -196,18 +196,10 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
   return {c0, c1, c2, c3};
 }
 
-// Throughput-mode draws: one Philox4x32-10 call (counter (sweep, 32 * pair +
-// lane, 1, 0), key = the replica seed) serves two visits of a lane, the
-// kernel's pair of chunks `pair` (halves 0 and 1), each as one 64-bit
-// uniform u: random flip iff u <= tm, and on a tie the coin is bit 0 of u
-// (tm = thr * 2^11 + 2047, so the flip test ignores u's low 11 bits and the
-// coin is independent of it). Halves the Philox work per visit.
-__device__ __forceinline__ void pair_draws(uint32_t sweep, uint32_t pair, int lane, uint32_t k0, uint32_t k1,
-                                           uint64_t& u0, uint64_t& u1) {
-  const Philox4 x = philox4x32_10(sweep, pair * 32u + static_cast<uint32_t>(lane), 1u, 0u, k0, k1);
-  u0 = (static_cast<uint64_t>(x.x) << 32) | x.y;
-  u1 = (static_cast<uint64_t>(x.z) << 32) | x.w;
-}
+// Throughput-mode draws (K2, K4): one Philox4x32-10 call per four visits of a
+// lane (counter (sweep, 32 * quad + lane, 2, 0), key = the replica seed), 32
+// bits per visit: tie coin = bit 0, a 31-bit uniform against the flip
+// threshold's top 31 bits (tm >> 33; tm = thr * 2^11 + 2047).
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

@@ -162,15 +162,16 @@ __device__ __forceinline__ int long_rows(const PartArgs& a, const Row<WK, KMAX>&
 // The spin-word loads of the register bucket are issued first and consumed
 // after the Philox draw, so their latency (an LDS, or an L2 round trip for
 // the fresh bands of SMODE 2) overlaps the RNG.
-// Draws (pair_draws): chain chunks k and k + 1 (k even) of chain J share one
-// Philox call, pair id = the pair's first chunk J + k * P; a visit whose
-// pair was drawn just before takes the kept half (use_spare), else draws and
-// keeps the other half in `spare`. Global-tail chunks (>= nmain, no chain)
-// draw alone (pair id = the chunk).
+// Draws: chain chunks k .. k + 3 (k a multiple of 4) of chain J share one
+// Philox4x32-10 call (counter (sweep, 32 * quad + lane, 2, 0), quad id = the
+// first chunk J + k * P), 32 bits per visit as in K2 (coin = bit 0, a 31-bit
+// uniform against tm >> 33); a visit whose quad was drawn before takes its
+// word from `qd` (have), else draws and keeps all four. Global-tail chunks
+// (>= nmain, no chain) draw alone (quad id = the chunk, word 0).
 template <int WK, int KMAX, typename Word>
 __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMAX>& r, int c, Word word, int lane,
                                             int sweep, uint32_t k0, uint32_t k1, unsigned long long tm,
-                                            bool en, uint32_t pair, int half, uint64_t& spare, bool use_spare) {
+                                            bool en, uint32_t quad, int idx, uint4& qd, bool have) {
   Visit x;
   x.live = c * 32 + lane < a.g.n;
   x.own = x.live ? (((r.word >> lane) & 1u) ? 1 : -1) : -1;
@@ -184,17 +185,14 @@ __device__ __forceinline__ Visit make_visit(const PartArgs& a, const Row<WK, KMA
       wv[4 * k + 2] = word(pos(r.g[k].z) >> 5);
       wv[4 * k + 3] = word(pos(r.g[k].w) >> 5);
     }
-  uint64_t u;
-  if (use_spare) {
-    u = spare;
-  } else {
-    uint64_t u0, u1;
-    pair_draws(static_cast<uint32_t>(sweep), pair, lane, k0, k1, u0, u1);
-    u = half ? u1 : u0;
-    spare = u1;
+  if (!have) {
+    const Philox4 ph = philox4x32_10(static_cast<uint32_t>(sweep), quad * 32u + static_cast<uint32_t>(lane), 2u, 0u,
+                                     k0, k1);
+    qd = make_uint4(ph.x, ph.y, ph.z, ph.w);
   }
-  x.coin = (u & 1u) != 0;
-  x.flip = en && u <= tm;
+  const unsigned w32 = idx == 0 ? qd.x : idx == 1 ? qd.y : idx == 2 ? qd.z : qd.w;
+  x.coin = (w32 & 1u) != 0;
+  x.flip = en && (w32 >> 1) <= static_cast<unsigned>(tm >> 33);
   auto bit = [](int e, int w, unsigned wd) {
     const unsigned sh = __funnelshift_r(wd, 0u, WK == 1 ? (e & 0x7fffffff) : e);
     if (WK == 2) return (sh & 1u) ? w : -w;
@@ -524,7 +522,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     bounds(0, c0, c1);
     load_row<WK, KMAX>(a, gb, J, c0, c1, lane, cur);
   }
-  uint64_t spare = 0;
+  uint4 qd = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll 1
   for (int k = 0; k < Km; k++) {
     const int c = J + k * P;
@@ -536,7 +534,7 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     blo = (k - 1) * P;
     bhi = (k + 1) * P;
     const Visit x = make_visit<WK, KMAX>(a, cur, c, word, lane, sweep, k0, k1, tm, en,
-                                         static_cast<uint32_t>(J + (k & ~1) * P), k & 1, spare, (k & 1) != 0);
+                                         static_cast<uint32_t>(J + (k & ~3) * P), k & 3, qd, (k & 3) != 0);
     commit(c, cur.word, decide_chunk(x, G, a4, bb, lane, scan_buf[warp], scan_g[warp]));
     cur = nxt;
   }
@@ -549,10 +547,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_sweep(const PartArgs a) {
     const int ct = J + (K - 1) * P;
     blo = (K - 2) * P;
     bhi = K * P;
-    // (its pair's first chunk K - 2 was drawn by the loop above when K - 1 is odd)
+    // (its quad was drawn by the loop above when K - 1 is not a multiple of 4)
     const Visit xt = K > 0 ? make_visit<WK, KMAX>(a, cur, ct, word, lane, sweep, k0, k1, tm, en,
-                                                  static_cast<uint32_t>(J + ((K - 1) & ~1) * P), (K - 1) & 1, spare,
-                                                  ((K - 1) & 1) != 0)
+                                                  static_cast<uint32_t>(J + ((K - 1) & ~3) * P), (K - 1) & 3, qd,
+                                                  ((K - 1) & 3) != 0)
                            : Visit{-1, 0, false, false, false};
     stage[warp][lane] = pack(xt);
     if (lane == 0) {
@@ -704,10 +702,10 @@ __global__ void __launch_bounds__(32 * kNW, 1) k4_finish(const PartArgs a, const
     Row<WK, KMAX> row;
     load_row<WK, KMAX>(a, gb, c, __ldg(a.sell_off + c), __ldg(a.sell_off + c + 1), lane, row);
     row.word = mword(c);
-    uint64_t spare = 0;
+    uint4 qd = make_uint4(0u, 0u, 0u, 0u);
     const Visit xt = make_visit<WK, KMAX>(a, row, c, mword, lane, sweep, static_cast<uint32_t>(seed),
                                           static_cast<uint32_t>(seed >> 32), a.tmask[sweep], a.thr[sweep] >= 0,
-                                          static_cast<uint32_t>(c), 0, spare, false);
+                                          static_cast<uint32_t>(c), 0, qd, false);
     stage[warp][lane] = pack(xt);
   }
   if (SM) {
