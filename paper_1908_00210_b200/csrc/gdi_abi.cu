@@ -1019,16 +1019,24 @@ int gdi_evaluate_device(const gdi_graph* g, const int8_t* d_spins, int32_t repli
   // per-thread scratch kept between calls (the bench times back-to-back
   // calls); a call on another stream first waits for the previous call's
   // kernels (the scratch is reused)
-  thread_local DevBuf work;
-  thread_local int work_dev = -1;
-  thread_local cudaEvent_t done = nullptr;
-  if (work_dev != g->device) {
-    if (done) cudaEventDestroy(done);
-    done = nullptr;
+  struct Scratch {
+    DevBuf work;
+    int dev = -1;
+    cudaEvent_t done = nullptr;
+    ~Scratch() {
+      if (done) cudaEventDestroy(done);
+    }
+  };
+  thread_local Scratch sc;
+  DevBuf& work = sc.work;
+  if (sc.dev != g->device) {
+    if (sc.done) cudaEventDestroy(sc.done);
+    sc.done = nullptr;
     work.reset();
-    work_dev = g->device;
+    sc.dev = g->device;
   }
-  if (!done) GDI_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  if (!sc.done) GDI_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
+  cudaEvent_t done = sc.done;
   GDI_CUDA(cudaStreamWaitEvent(st, done, 0));
   const size_t ww = static_cast<size_t>(eval_work_words(g->st.n, replicas, g->wkind)) * 4 + 16;
   if (work.bytes < ww) {
