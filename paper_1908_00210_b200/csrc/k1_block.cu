@@ -518,8 +518,15 @@ int block_plan(const GraphStats& st, int32_t replicas, int64_t a4, int64_t b, in
   rc = rc < 1 ? 1 : rc > 16 ? 16 : rc;
   const int cap = 227 * 1024;
   // the CSR and window masks in shared memory next to the replicas, else
-  // (degree <= 4) row records in global memory (ROWS)
+  // (degree <= 4) row records in global memory (ROWS). With more replicas
+  // than fit one wave (R > 148 x the replicas a CTA holds), fewer replicas
+  // per CTA and several waves rather than the global-memory kernels (4096
+  // replicas x 1000 sweeps: G55 412 -> 265 ms, G81+-1 3033 -> 1099 ms, G1 58
+  // -> 34 ms)
   int rows = 0;
+  while (rc > 1 && BlkLayout::make(st.n, nnz, rc, fb, sgn).total > cap &&
+         !(st.max_degree <= 4 && BlkLayout::make(st.n, nnz, rc, fb, sgn, 4).total <= cap))
+    rc--;
   if (BlkLayout::make(st.n, nnz, rc, fb, sgn).total > cap) {
     if (st.max_degree > 4 || BlkLayout::make(st.n, nnz, rc, fb, sgn, 4).total > cap) return -1;
     rows = 4;
